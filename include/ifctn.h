@@ -1,0 +1,172 @@
+/*
+ * ifctn.h — C-ABI of the B200 (sm_100a) iFCTN tensor-completion PAM sweep.
+ *
+ * Paper: "iFCTN" (arxiv 2511.16358), /root/reference/PAPER.md ("P:Lx-y" = line range).
+ * The library implements Algorithm 1: given the observed tensor O, the sample
+ * set Ω, the iFCTN-rank matrix R, ρ, t_max and ε, it runs PAM sweeps, each of which
+ *   (a2) contracts the other factors' KR chains into the unfolding-free coefficients of
+ *        block (k,i) (Prop. 1; Eq. 8),
+ *   (a3/a4) forms the Gram matrix + RHS of the proximal LS subproblem (+ρI) and solves the
+ *        small SPD systems column by column (Eq. 8),
+ *   (a5) rebuilds the low-rank model and refills Ω^c (Eq. 9, read as the exact
+ *        per-entry prox minimiser (t + ρx)/(1+ρ); reading R1).
+ *
+ * Conventions
+ *   - Modes are 0-based in this API (paper mode k = API k+1).
+ *   - Dense tensors (observed O, mask, truth, outputs) are mode-1-fastest (column-major):
+ *     linear index = i_0 + I_0*(i_1 + I_1*(i_2 + …)).  Under sharding (dist != NULL,
+ *     world > 1) every tensor argument is this rank's shard: the contiguous slice of the
+ *     shard mode given by ifctn_shard_range(), in the same linearisation.
+ *   - Factors: the N(N-1) matrices G_{k,i} ∈ R^{R_{k,i} × I_k}, concatenated
+ *     in order k ascending, i ascending (i≠k); each column-major (r fastest).  Under
+ *     sharding the chains G_{s,·} of the shard mode s hold only the local columns.
+ *   - Element type: ifctn_dtype for O, truth, factors and outputs; the mask is uint8
+ *     (nonzero = observed); coefficient outputs (β, ω) are float64.
+ *   - Memory: every data pointer may be HOST or DEVICE memory; the library inspects it with
+ *     cudaPointerGetAttributes and copies as needed (pinned host memory gives async copies).
+ *     The caller owns every buffer it passes; the library never frees caller memory.
+ *   - Ordering: all device work is enqueued on the stream given to ifctn_create.
+ *
+ * Errors: every function returns an ifctn_status; nothing throws across the ABI.  Arguments
+ * are validated before any device work.  ifctn_last_error(ctx) gives a message for the
+ * most recent failure on that context (a static string for a NULL ctx).
+ */
+#ifndef IFCTN_H
+#define IFCTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ifctn_ctx ifctn_ctx;
+
+typedef enum {
+    IFCTN_OK = 0,
+    IFCTN_E_ARG = 1,         /* NULL pointer, ρ ≤ 0, bad enum, bad block index            */
+    IFCTN_E_SHAPE = 2,       /* order < 2 or > IFCTN_MAX_ORDER, a dim < 1, size overflow   */
+    IFCTN_E_RANKS = 3,       /* R not symmetric, diagonal ≠ 0, off-diagonal < 1 or > max   */
+    IFCTN_E_WORKSPACE = 4,   /* caller workspace too small or misaligned                  */
+    IFCTN_E_CUDA = 5,        /* CUDA runtime error (message in ifctn_last_error)           */
+    IFCTN_E_NCCL = 6,        /* NCCL error (multi-GPU)                                     */
+    IFCTN_E_NOT_SPD = 7,     /* non-positive Cholesky pivot (impossible in exact arith.)   */
+    IFCTN_E_NONFINITE = 8,   /* NaN/Inf met in the sweep norms                             */
+    IFCTN_E_STATE = 9,       /* call not valid in the context's state                      */
+    IFCTN_E_UNSUPPORTED = 10,/* valid input this build does not handle (see message)       */
+    IFCTN_E_NO_OBSERVED = 11 /* Ω is empty (Algorithm 1 needs at least one observation)   */
+} ifctn_status;
+
+typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
+
+#define IFCTN_MAX_ORDER 6
+#define IFCTN_MAX_RANK 8
+
+/* ifctn_create flags */
+#define IFCTN_FLAG_NONE 0u
+#define IFCTN_FLAG_NO_GRAPH 1u /* run sweeps as plain launches instead of a CUDA graph     */
+#define IFCTN_FLAG_X_FULL 2u   /* `observed` is a full X (values off Ω kept), for resume  */
+#define IFCTN_FLAG_H_SMEM 4u   /* stage all pairwise Grams in shared memory when they fit */
+
+/* Multi-GPU description (one process per GPU).  NULL or world == 1: single GPU. */
+typedef struct {
+    const void* nccl_unique_id; /* ncclUniqueId (128 bytes), identical on all ranks       */
+    int rank;
+    int world;
+    int shard_mode;             /* 0-based; -1 = the largest mode, first on ties           */
+} ifctn_dist;
+
+/* One row of the per-sweep trace (Algorithm 1 stop test P:L341-344, Lemma 2). */
+typedef struct {
+    int sweep;          /* 1-based sweep index s+1                                         */
+    double rel_change;  /* ‖X^{s+1} − X^{s}‖_F / ‖X^{s}‖_F  (denominator 1 if ‖X^{s}‖ = 0)  */
+    double objective;   /* F(M^{s+1}) = ½‖X^{s+1} − iFCTN(G^{s+1})‖²_F                     */
+    double dx2;         /* ‖X^{s+1} − X^{s}‖²_F                                            */
+    double dg2;         /* Σ_{k,i} ‖G^{s+1}_{k,i} − G^{s}_{k,i}‖²_F                        */
+} ifctn_trace_row;
+
+/* Which tensor ifctn_reconstruct writes. */
+#define IFCTN_MODEL 0 /* iFCTN(G) = Π_{p<q} (G_{p,q}ᵀG_{q,p})(i_p,i_q)  (Def. 4, Eq. 5)       */
+#define IFCTN_X 1     /* the current iterate X                                               */
+
+/* Bytes of device workspace ifctn_create needs (caller may pass NULL to let the library
+ * allocate it).  Independent of the device; deterministic in its arguments.             */
+ifctn_status ifctn_workspace_bytes(int order, const int64_t* dims, const int32_t* ranks,
+                                   ifctn_dtype dtype, const ifctn_dist* dist, size_t* bytes);
+
+/* This rank's slice [*begin, *end) of the shard mode (P:silent; reading R21:
+ * ranks get ⌈I_s/W⌉ then ⌊I_s/W⌋ slices) and the shard mode itself.                    */
+ifctn_status ifctn_shard_range(int order, const int64_t* dims, const ifctn_dist* dist,
+                               int* shard_mode, int64_t* begin, int64_t* end);
+
+/* Create a solver context: Algorithm 1 "Input" + "Initialization".
+ *   dims[order]         global mode sizes I_0..I_{N-1}
+ *   ranks[order*order]  iFCTN-rank matrix R, row-major, symmetric, zero diagonal,
+ *                       1 ≤ R_{p,q} ≤ IFCTN_MAX_RANK (Def. 4)
+ *   rho                 proximal weight ρ > 0
+ *   observed            O (this rank's shard); values off Ω are ignored unless
+ *                       IFCTN_FLAG_X_FULL; X⁽⁰⁾ = P_Ω(O) with zeros on Ω^c (reading R7)
+ *   mask                Ω as uint8, same layout, nonzero = observed
+ *   init_factors        G⁰ in the factor layout above
+ *   workspace           device memory of ≥ ifctn_workspace_bytes(), 256-B aligned, owned by
+ *                       the caller and kept alive until ifctn_destroy; NULL = library-owned
+ *   stream              cudaStream_t (NULL = legacy default stream)
+ * The inputs are copied; the caller may free them after this returns.                  */
+ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims,
+                          const int32_t* ranks, ifctn_dtype dtype, double rho,
+                          const void* observed, const uint8_t* mask, const void* init_factors,
+                          void* workspace, size_t workspace_bytes, const ifctn_dist* dist,
+                          void* stream, unsigned flags);
+
+/* Run up to t_max PAM sweeps (Algorithm 1 while-loop).  eps ≤ 0 runs exactly
+ * t_max sweeps and, with trace == NULL, returns without synchronising (device errors are
+ * then reported by ifctn_sync).  eps > 0 stops after the first sweep with rel_change < eps.
+ * trace (host, t_max rows) is filled when non-NULL.  *sweeps_done (may be NULL).         */
+ifctn_status ifctn_sweep(ifctn_ctx* ctx, int t_max, double eps, int* sweeps_done,
+                         ifctn_trace_row* trace);
+
+/* Wait for the context's stream and report deferred device errors (E_NOT_SPD, E_NONFINITE). */
+ifctn_status ifctn_sync(ifctn_ctx* ctx);
+
+/* Write IFCTN_MODEL or IFCTN_X (this rank's shard, dense layout) to out.                */
+ifctn_status ifctn_reconstruct(ifctn_ctx* ctx, int what, void* out);
+
+/* Copy the current factors (layout of init_factors) to out.                              */
+ifctn_status ifctn_get_factors(ifctn_ctx* ctx, void* out);
+
+/* RSE = ‖T − X‖_F / ‖T‖_F over the global tensor (denominator reading R10).
+ * truth: this rank's shard.                                                              */
+ifctn_status ifctn_rse(ifctn_ctx* ctx, const void* truth, double* rse);
+
+/* f(G, X) = ½‖X − iFCTN(G)‖²_F of the current state.                            */
+ifctn_status ifctn_objective(ifctn_ctx* ctx, double* f);
+
+/* ---- step-level entry points (the rows of a sweep; used by parity tests) ------------- */
+
+/* Step a2 for block (k,i): β(a,j) = Σ_{i_i=a, i_k=j} M X, ω(a,j) = Σ M² with
+ * M = Π_{{p,q}≠{k,i}} (G_{p,q}ᵀG_{q,p})(i_p,i_q) (Prop. 1 + Eq. 8's D, y_j),
+ * from the current state, no state change.  beta/omega: float64 I_i × I_k column-major
+ * (a = i_i fastest); under sharding the local partial sums.                              */
+ifctn_status ifctn_block_coefficients(ifctn_ctx* ctx, int k, int i, double* beta,
+                                      double* omega);
+
+/* Steps a2-a4 for block (k,i): new G_{k,i} from the current state (Eq. 8), H refreshed.  */
+ifctn_status ifctn_block_update(ifctn_ctx* ctx, int k, int i);
+
+/* Step a5: X ← P_Ω(X) + P_Ω^c((iFCTN(G) + ρX)/(1+ρ)); norms (host, may be NULL) gets
+ * {‖ΔX‖², ‖X_old‖², ½‖X_new − iFCTN(G)‖², Σ‖ΔG‖² since the last X update}.             */
+ifctn_status ifctn_x_update(ifctn_ctx* ctx, double* norms);
+
+ifctn_status ifctn_destroy(ifctn_ctx* ctx);
+
+const char* ifctn_status_string(ifctn_status s);
+const char* ifctn_last_error(const ifctn_ctx* ctx);
+
+/* Kernel launches the last ifctn_sweep enqueued (graph nodes count as launches).         */
+int64_t ifctn_launch_count(const ifctn_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IFCTN_H */

@@ -1,0 +1,132 @@
+// common.cuh — shared constants, vector helpers and parameter blocks of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ifctn {
+
+constexpr int MAXN = 6;                        // IFCTN_MAX_ORDER
+constexpr int MAXP = MAXN * (MAXN - 1) / 2;    // pairs p<q
+constexpr int MAXSF = MAXN - 2;                // pairs involving the fast mode r0 (outer)
+constexpr int MAXR = 8;                        // IFCTN_MAX_RANK
+constexpr int kPassThreads = 256;              // fiber-pass CTA size
+constexpr int kUnroll = 4;                     // fibers in flight per lane
+
+enum PassMode : int {
+    PASS_KEPT1 = 0,   // a2, mode 1 (code mode 0) is one of the kept modes {k,i}
+    PASS_RED1 = 1,    // a2, mode 1 is reduced
+    PASS_REFILL = 2,  // a5: X update + norms
+    PASS_OBJ = 3,     // f = ½‖X − t‖² only
+    PASS_MODEL = 4,   // write t = iFCTN(G) in the user layout
+};
+
+template <typename T> struct VecT;
+template <> struct VecT<float> {
+    using V = float4;
+    static constexpr int W = 4;
+    __device__ static inline void get(const V& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+    __device__ static inline V make(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+};
+template <> struct VecT<double> {
+    using V = double2;
+    static constexpr int W = 2;
+    __device__ static inline void get(const V& v, double* o) { o[0] = v.x; o[1] = v.y; }
+    __device__ static inline V make(const double* o) { return make_double2(o[0], o[1]); }
+};
+
+template <typename T>
+__device__ __forceinline__ typename VecT<T>::V zero_v() {
+    T z[VecT<T>::W];
+#pragma unroll
+    for (int e = 0; e < VecT<T>::W; ++e) z[e] = T(0);
+    return VecT<T>::make(z);
+}
+
+// Streaming 16-B load of X that must not displace the (small, reused) H/G working set in L1.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+
+// One fiber pass = one streaming sweep over the (local) X in fibre order.  A "fibre" is a
+// mode-1 line X(:, i_2, …, i_N) stored contiguously with I1p ≥ I1 padded entries (pad = 0).
+// Fibres are enumerated as pos = v·FR + r, v over the kept outer modes, r over the reduced
+// outer modes in odometer order rmode[0] (fastest, "r0") … rmode[nred-1].
+template <typename T>
+struct PassParams {
+    const T* H;          // all pairwise Grams H_{p,q} (p<q) in one buffer; H_{p,q}(a,b) at
+    int64_t hsize;       //   off_{pq} + b·ld_p + a, ld_0 = I1p (pad rows zero), ld_p = I_p
+    const T* X;          // internal padded X
+    T* Xw;               // PASS_REFILL: X, updated in place
+    const uint32_t* mask;// bit e of the padded layout = observed (pad bits = 1)
+    T* part_b;           // PASS_KEPT1/RED1 partial slots, slot = group + v, Lv values each
+    T* part_w;
+    double* norms;       // PASS_REFILL/OBJ: 3 doubles per group
+    T* out;              // PASS_MODEL: dense user layout
+    T rho, inv1p;        // ρ and 1/(1+ρ)
+    int I1, I1p, nchunk, lanes, lane_shift;
+    int64_t nfib, L, ngroups, NV, FR, Lv;
+    int nkept;
+    int kmode[2];
+    int64_t kdim[2];
+    int nred;
+    int rmode[MAXN];
+    int64_t rdim[MAXN];
+    int64_t fstride[MAXN];   // fibre-index stride of each outer mode (index by mode)
+    int nouter;              // N − 1
+    // weight factors, classified on the host relative to r0
+    int nvs;                 // slow vector factors H_{0,q}, q ≠ r0: column idx[q] of H_{0,q}
+    int64_t vs_off[MAXN];
+    int vs_mode[MAXN];
+    int64_t vf_off;          // fast vector factor H_{0,r0} (valid iff nred > 0)
+    int nss;                 // slow scalar factors H_{p,q}(i_p,i_q), p,q outer, ≠ r0
+    int64_t ss_off[MAXP];
+    int64_t ss_ld[MAXP];
+    int ss_p[MAXP], ss_q[MAXP];
+    int nsf;                 // fast scalar factors: pairs {r0, m}: H + off + idx[m]·mul + i_r0·inc
+    int64_t sf_off[MAXSF];
+    int sf_fixmode[MAXSF];
+    int64_t sf_fixmul[MAXSF];
+    int64_t sf_inc[MAXSF];
+};
+
+template <typename T>
+struct ReduceParams {
+    const T* part_b;
+    const T* part_w;
+    double* beta;        // I_i × I_k column-major (a fastest)
+    double* omega;
+    int64_t FR, L, NV, Lv;
+    int kept1;           // 1: KEPT1 layout, 0: RED1
+    int I1;              // real mode-1 size (KEPT1)
+    int64_t Ii;          // output leading dimension
+    int kIsMode0;        // KEPT1: k == 0 (j = i_1, a = v) else (a = i_1, j = v)
+    int kmode0IsK;       // RED1: kmode[0] == k
+    int64_t kdim0;
+};
+
+template <typename T>
+struct SolveParams {
+    const double* beta;
+    const double* omega;
+    T* Gki;              // R × I_k (local columns)
+    const T* Gik;        // R × I_i
+    T* H;                // Hall
+    int64_t h_off, h_ld; // H_{min,max}
+    int k_lt_i;          // k < i: H(j,a) at a·ld + j; else H(a,j) at j·ld + a
+    int64_t Ik, Ii;
+    double rho;
+    double* delta;       // per column ‖c_new − c_old‖²
+    int* flags;          // flags[0] |= 1 on a non-positive pivot
+};
+
+}  // namespace ifctn

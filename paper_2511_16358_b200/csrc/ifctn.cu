@@ -1,0 +1,974 @@
+// ifctn.cu — host orchestration and the C-ABI (include/ifctn.h) of the B200 iFCTN-TC PAM
+// sweep.  One translation unit; built with
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+// Everything the sweep computes runs in the kernels of fiber_pass.cuh and solve.cuh; this
+// file validates arguments, lays out the workspace, plans the passes (grid sizes, fibre
+// enumeration, weight-factor lists), enqueues the sweep and captures it as a CUDA graph.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ifctn.h"
+#include "common.cuh"
+#include "fiber_pass.cuh"
+#include "solve.cuh"
+#include "nccl_lite.h"
+
+namespace ifctn {
+
+static const char* kStatusNames[] = {
+    "IFCTN_OK", "IFCTN_E_ARG", "IFCTN_E_SHAPE", "IFCTN_E_RANKS", "IFCTN_E_WORKSPACE",
+    "IFCTN_E_CUDA", "IFCTN_E_NCCL", "IFCTN_E_NOT_SPD", "IFCTN_E_NONFINITE", "IFCTN_E_STATE",
+    "IFCTN_E_UNSUPPORTED", "IFCTN_E_NO_OBSERVED"};
+
+struct Error {
+    ifctn_status st;
+    std::string msg;
+};
+
+#define CU(expr)                                                                           \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            throw ::ifctn::Error{IFCTN_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+    } while (0)
+
+static void fail(ifctn_status st, const std::string& m) { throw Error{st, m}; }
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+static int pow2ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+constexpr int64_t kGroupBoundThreads = 160LL * 2048;  // ≥ resident threads of any B200 part
+
+// ------------------------------------------------------------------------------------------
+// Shape: everything derivable from the arguments alone (no device needed).
+// ------------------------------------------------------------------------------------------
+struct Shape {
+    int N = 0;
+    int64_t dims[MAXN] = {};
+    int32_t ranks[MAXN * MAXN] = {};
+    ifctn_dtype dtype = IFCTN_F32;
+    int64_t esize = 4;
+    int vw = 4;
+    // distribution
+    int rank = 0, world = 1, shard = 0;
+    int64_t sbegin = 0, send = 0;
+    int64_t ld[MAXN] = {};  // local dims
+    // layout
+    int64_t I1 = 0, I1p = 0, nfib = 0, npad = 0, nloc = 0, nglob = 0;
+    int64_t fstride[MAXN] = {};
+    int64_t goff[MAXN][MAXN] = {};
+    int64_t gtotal = 0;
+    int64_t hoff[MAXN][MAXN] = {};  // p<q
+    int64_t hld[MAXN] = {};
+    int64_t htotal = 0;
+    int nchunk = 0, lanes = 0, lane_shift = 0, cpl = 0;
+    int64_t part_elems = 0, max_bw = 0, ndelta = 0, groups_bound = 0;
+    int64_t delta_off[MAXN][MAXN] = {};
+    int64_t proj_elems = 0;  // multi-GPU projected Gram/RHS buffer (doubles)
+
+    int R(int p, int q) const { return ranks[p * N + q]; }
+};
+
+static void shard_range_of(int64_t I, int world, int rank, int64_t* b, int64_t* e) {
+    // ranks get ⌈I/W⌉ then ⌊I/W⌋ (reading R21): the first I mod W ranks get one extra.
+    const int64_t base = I / world, extra = I % world;
+    *b = rank * base + std::min<int64_t>(rank, extra);
+    *e = *b + base + (rank < extra ? 1 : 0);
+}
+
+static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, ifctn_dtype dtype,
+                        const ifctn_dist* dist) {
+    Shape s;
+    if (!dims || !ranks) fail(IFCTN_E_ARG, "dims/ranks must not be NULL");
+    if (order < 2 || order > MAXN) fail(IFCTN_E_SHAPE, "order must be in [2, IFCTN_MAX_ORDER]");
+    if (dtype != IFCTN_F32 && dtype != IFCTN_F64) fail(IFCTN_E_ARG, "dtype must be IFCTN_F32 or IFCTN_F64");
+    s.N = order;
+    s.dtype = dtype;
+    s.esize = dtype == IFCTN_F32 ? 4 : 8;
+    s.vw = dtype == IFCTN_F32 ? 4 : 2;
+    double prodd = 1.0;
+    for (int m = 0; m < order; ++m) {
+        if (dims[m] < 1) fail(IFCTN_E_SHAPE, "every dim must be >= 1");
+        s.dims[m] = dims[m];
+        prodd *= (double)dims[m];
+    }
+    if (prodd > 4.0e18) fail(IFCTN_E_SHAPE, "tensor too large");
+    for (int p = 0; p < order; ++p)
+        for (int q = 0; q < order; ++q) {
+            const int32_t r = ranks[p * order + q];
+            if (p == q) {
+                if (r != 0) fail(IFCTN_E_RANKS, "rank matrix diagonal must be 0");
+            } else {
+                if (r != ranks[q * order + p]) fail(IFCTN_E_RANKS, "rank matrix must be symmetric");
+                if (r < 1) fail(IFCTN_E_RANKS, "off-diagonal ranks must be >= 1");
+                if (r > MAXR) fail(IFCTN_E_UNSUPPORTED, "ranks above IFCTN_MAX_RANK are not supported by this build");
+            }
+            s.ranks[p * order + q] = r;
+        }
+    // distribution
+    if (dist && dist->world > 1) {
+        if (dist->rank < 0 || dist->rank >= dist->world) fail(IFCTN_E_ARG, "dist rank out of range");
+        s.world = dist->world;
+        s.rank = dist->rank;
+        int sm = dist->shard_mode;
+        if (sm < 0) {
+            sm = 0;
+            for (int m = 1; m < order; ++m)
+                if (dims[m] > dims[sm]) sm = m;
+        }
+        if (sm >= order) fail(IFCTN_E_ARG, "shard_mode out of range");
+        if (dims[sm] < dist->world) fail(IFCTN_E_SHAPE, "shard mode smaller than the world size");
+        s.shard = sm;
+    } else {
+        s.world = 1;
+        s.rank = 0;
+        s.shard = 0;
+    }
+    shard_range_of(s.dims[s.shard], s.world, s.rank, &s.sbegin, &s.send);
+    for (int m = 0; m < order; ++m) s.ld[m] = s.dims[m];
+    s.ld[s.shard] = s.send - s.sbegin;
+
+    s.I1 = s.ld[0];
+    s.I1p = align_up(s.I1, s.vw);
+    s.nfib = 1;
+    for (int m = 1; m < order; ++m) s.nfib *= s.ld[m];
+    s.npad = s.nfib * s.I1p;
+    s.nloc = s.nfib * s.I1;
+    s.nglob = (int64_t)prodd;
+    s.fstride[0] = 0;
+    int64_t st = 1;
+    for (int m = 1; m < order; ++m) {
+        s.fstride[m] = st;
+        st *= s.ld[m];
+    }
+    // factors (local columns for the shard-mode chain)
+    int64_t off = 0;
+    for (int k = 0; k < order; ++k)
+        for (int i = 0; i < order; ++i) {
+            if (i == k) continue;
+            s.goff[k][i] = off;
+            off += (int64_t)s.R(k, i) * s.ld[k];
+        }
+    s.gtotal = off;
+    // pairwise Grams, each block padded to the vector width
+    off = 0;
+    for (int p = 0; p < order; ++p) s.hld[p] = (p == 0) ? s.I1p : s.ld[p];
+    for (int p = 0; p < order; ++p)
+        for (int q = p + 1; q < order; ++q) {
+            s.hoff[p][q] = off;
+            off += align_up(s.hld[p] * s.ld[q], s.vw);
+        }
+    s.htotal = std::max<int64_t>(off, s.vw);
+    // lane mapping
+    s.nchunk = (int)(s.I1p / s.vw);
+    s.lanes = std::min(32, pow2ceil(s.nchunk));
+    s.lane_shift = 0;
+    while ((1 << s.lane_shift) < s.lanes) ++s.lane_shift;
+    int cpl = (s.nchunk + s.lanes - 1) / s.lanes;
+    s.cpl = pow2ceil(cpl);
+    if (s.cpl > 8) fail(IFCTN_E_UNSUPPORTED, "mode-1 size above 1024 (f32) / 512 (f64) per shard is not supported by this build");
+    s.groups_bound = std::min<int64_t>(s.nfib, kGroupBoundThreads / s.lanes);
+    // partial slots: max over contract passes of (groups + NV) * Lv
+    int64_t pmax = 0, bw = 0, nd = 0;
+    for (int k = 0; k < order; ++k)
+        for (int i = 0; i < order; ++i) {
+            if (i == k) continue;
+            int64_t NV = 1;
+            for (int m = 1; m < order; ++m)
+                if (m == k || m == i) NV *= s.ld[m];
+            const bool kept1 = (k == 0 || i == 0);
+            const int64_t Lv = kept1 ? s.I1p : 1;
+            pmax = std::max(pmax, (s.groups_bound + NV) * Lv);
+            bw = std::max(bw, s.ld[i] * s.ld[k]);
+            s.delta_off[k][i] = nd;
+            nd += s.ld[k];
+        }
+    s.part_elems = align_up(pmax, s.vw);
+    s.max_bw = bw;
+    s.ndelta = nd;
+    // projected Gram/RHS for the allreduce: max over blocks of I_k·(R(R+1)/2 + R)
+    int64_t pe = 0;
+    for (int k = 0; k < order; ++k)
+        for (int i = 0; i < order; ++i)
+            if (i != k) {
+                const int64_t R = s.R(k, i);
+                pe = std::max(pe, s.ld[k] * (R * (R + 1) / 2 + R));
+            }
+    s.proj_elems = pe + 8;
+    return s;
+}
+
+struct Layout {
+    int64_t x, bits, g, h, pb, pw, beta, omega, delta, norms, scal, flags, rse, proj, total;
+};
+
+static Layout make_layout(const Shape& s) {
+    Layout L{};
+    int64_t o = 0;
+    auto take = [&](int64_t bytes) {
+        const int64_t r = o;
+        o = align_up(o + std::max<int64_t>(bytes, 1), 256);
+        return r;
+    };
+    L.x = take(s.npad * s.esize);
+    L.bits = take(align_up((s.npad + 31) / 32, 8) * 4);
+    L.g = take(s.gtotal * s.esize);
+    L.h = take(s.htotal * s.esize);
+    L.pb = take(s.part_elems * s.esize);
+    L.pw = take(s.part_elems * s.esize);
+    L.beta = take(s.max_bw * 8);
+    L.omega = take(s.max_bw * 8);
+    L.delta = take(s.ndelta * 8);
+    L.norms = take(s.groups_bound * 3 * 8);
+    L.scal = take(16 * 8);
+    L.flags = take(4 * 4);
+    L.rse = take(2 * 1024 * 8 + 16);
+    L.proj = take(s.proj_elems * 8);
+    L.total = o;
+    return L;
+}
+
+static bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------------------------------------
+// Solver<T>
+// ------------------------------------------------------------------------------------------
+struct SolverBase {
+    virtual ~SolverBase() {}
+    virtual void sweep(int t_max, double eps, int* done, ifctn_trace_row* trace) = 0;
+    virtual void sync_check() = 0;
+    virtual void reconstruct(int what, void* out) = 0;
+    virtual void get_factors(void* out) = 0;
+    virtual double rse(const void* truth) = 0;
+    virtual double objective() = 0;
+    virtual void block_coefficients(int k, int i, double* beta, double* omega) = 0;
+    virtual void block_update(int k, int i) = 0;
+    virtual void x_update(double* norms) = 0;
+    virtual int64_t launches() const = 0;
+};
+
+template <typename T>
+struct PassPlan {
+    PassParams<T> p;
+    const void* fn = nullptr;
+    dim3 grid;
+    size_t smem = 0;
+};
+
+template <typename T>
+struct BlockPlan {
+    int k = 0, i = 0;
+    PassPlan<T> pass;
+    ReduceParams<T> red;
+    dim3 red_grid;
+    SolveParams<T> sol;
+    dim3 sol_grid;
+    const void* sol_fn = nullptr;
+};
+
+template <typename T, int MODE>
+static const void* pick_pass(int cpl, bool smem) {
+    switch (cpl) {
+        case 1: return smem ? (const void*)fiber_pass<T, MODE, 1, true> : (const void*)fiber_pass<T, MODE, 1, false>;
+        case 2: return smem ? (const void*)fiber_pass<T, MODE, 2, true> : (const void*)fiber_pass<T, MODE, 2, false>;
+        case 4: return smem ? (const void*)fiber_pass<T, MODE, 4, true> : (const void*)fiber_pass<T, MODE, 4, false>;
+        default: return smem ? (const void*)fiber_pass<T, MODE, 8, true> : (const void*)fiber_pass<T, MODE, 8, false>;
+    }
+}
+
+template <typename T>
+static const void* pick_pass_mode(int mode, int cpl, bool smem) {
+    switch (mode) {
+        case PASS_KEPT1: return pick_pass<T, PASS_KEPT1>(cpl, smem);
+        case PASS_RED1: return pick_pass<T, PASS_RED1>(cpl, smem);
+        case PASS_REFILL: return pick_pass<T, PASS_REFILL>(cpl, smem);
+        case PASS_OBJ: return pick_pass<T, PASS_OBJ>(cpl, smem);
+        default: return pick_pass<T, PASS_MODEL>(cpl, smem);
+    }
+}
+
+template <typename T>
+static const void* pick_solve(int R) {
+    switch (R) {
+        case 1: return (const void*)block_solve<T, 1>;
+        case 2: return (const void*)block_solve<T, 2>;
+        case 3: return (const void*)block_solve<T, 3>;
+        case 4: return (const void*)block_solve<T, 4>;
+        case 5: return (const void*)block_solve<T, 5>;
+        case 6: return (const void*)block_solve<T, 6>;
+        case 7: return (const void*)block_solve<T, 7>;
+        default: return (const void*)block_solve<T, 8>;
+    }
+}
+
+template <typename T>
+struct Solver : SolverBase {
+    Shape s;
+    Layout lay;
+    double rho;
+    unsigned flags;
+    cudaStream_t user_stream;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    unsigned char* ws = nullptr;
+    bool own_ws = false;
+    int nsm = 0;
+    bool use_smem = false;
+    size_t smem_limit = 0;
+    // device views
+    T *X, *G, *H, *pb, *pw;
+    uint32_t* bits;
+    double *beta, *omega, *delta, *norms, *scal, *rsep, *proj;
+    int* dflags;
+    double* hscal = nullptr;  // pinned
+    int* hflags = nullptr;    // pinned
+    std::vector<BlockPlan<T>> blocks;
+    PassPlan<T> refill, obj, model;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    int64_t nlaunch_sweep = 0, last_launches = 0;
+    // multi-GPU (see dist.cuh notes in DESIGN.md)
+    NcclLite* nccl = nullptr;
+    void* comm = nullptr;
+
+    ~Solver() override {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        if (comm && nccl) nccl->commDestroy(comm);
+        if (st) cudaStreamSynchronize(st);
+        if (own_ws && ws) cudaFree(ws);
+        if (hscal) cudaFreeHost(hscal);
+        if (hflags) cudaFreeHost(hflags);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    // stream-ordering with the caller's stream
+    void begin() {
+        CU(cudaEventRecord(ev_in, user_stream));
+        CU(cudaStreamWaitEvent(st, ev_in, 0));
+    }
+    void end() {
+        CU(cudaEventRecord(ev_out, st));
+        CU(cudaStreamWaitEvent(user_stream, ev_out, 0));
+    }
+
+    template <typename P>
+    void launch(const void* fn, dim3 g, dim3 b, size_t smem, const P& p) {
+        void* args[] = {(void*)&p};
+        CU(cudaLaunchKernel(fn, g, b, args, smem, st));
+    }
+
+    PassPlan<T> make_pass(int mode, int k, int i) {
+        const int N = s.N;
+        PassPlan<T> pp;
+        PassParams<T>& p = pp.p;
+        memset(&p, 0, sizeof(p));
+        p.H = H;
+        p.hsize = s.htotal;
+        p.X = X;
+        p.Xw = X;
+        p.mask = bits;
+        p.part_b = pb;
+        p.part_w = pw;
+        p.norms = norms;
+        p.rho = (T)rho;
+        p.inv1p = (T)(1.0 / (1.0 + rho));
+        p.I1 = (int)s.I1;
+        p.I1p = (int)s.I1p;
+        p.nchunk = s.nchunk;
+        p.lanes = s.lanes;
+        p.lane_shift = s.lane_shift;
+        p.nouter = N - 1;
+        for (int m = 0; m < N; ++m) p.fstride[m] = s.fstride[m];
+        const bool contract = (mode == PASS_KEPT1 || mode == PASS_RED1);
+        // kept outer modes (ascending), reduced outer modes
+        std::vector<int> kept, red;
+        for (int m = 1; m < N; ++m) {
+            if (contract && (m == k || m == i)) kept.push_back(m);
+            else red.push_back(m);
+        }
+        // odometer order: r0 = the largest reduced mode (ties: lowest), then ascending
+        if (!red.empty()) {
+            int best = 0;
+            for (size_t t = 1; t < red.size(); ++t)
+                if (s.ld[red[t]] > s.ld[red[best]]) best = (int)t;
+            std::rotate(red.begin(), red.begin() + best, red.begin() + best + 1);
+        }
+        p.nkept = (int)kept.size();
+        for (size_t t = 0; t < kept.size(); ++t) {
+            p.kmode[t] = kept[t];
+            p.kdim[t] = s.ld[kept[t]];
+        }
+        if (p.nkept < 2) p.kdim[1] = 1;
+        if (p.nkept < 1) p.kdim[0] = 1;
+        p.nred = (int)red.size();
+        for (size_t t = 0; t < red.size(); ++t) {
+            p.rmode[t] = red[t];
+            p.rdim[t] = s.ld[red[t]];
+        }
+        p.NV = 1;
+        for (int m : kept) p.NV *= s.ld[m];
+        p.FR = 1;
+        for (int m : red) p.FR *= s.ld[m];
+        p.nfib = s.nfib;
+        p.Lv = (mode == PASS_KEPT1) ? s.I1p : 1;
+        const int r0 = red.empty() ? -1 : red[0];
+        // weight factors: every pair p<q except {k,i} when contracting
+        p.vf_off = 0;
+        for (int a = 0; a < N; ++a)
+            for (int b = a + 1; b < N; ++b) {
+                if (contract && ((a == k && b == i) || (a == i && b == k))) continue;
+                const int64_t off = s.hoff[a][b];
+                if (a == 0) {
+                    if (b == r0) p.vf_off = off;
+                    else {
+                        p.vs_off[p.nvs] = off;
+                        p.vs_mode[p.nvs] = b;
+                        ++p.nvs;
+                    }
+                } else if (a == r0 || b == r0) {
+                    // H_{a,b}(i_a, i_b) at off + i_b·ld_a + i_a
+                    const int fix = (a == r0) ? b : a;
+                    p.sf_off[p.nsf] = off;
+                    p.sf_fixmode[p.nsf] = fix;
+                    p.sf_fixmul[p.nsf] = (a == r0) ? s.hld[a] : 1;
+                    p.sf_inc[p.nsf] = (a == r0) ? 1 : s.hld[a];
+                    ++p.nsf;
+                } else {
+                    p.ss_off[p.nss] = off;
+                    p.ss_ld[p.nss] = s.hld[a];
+                    p.ss_p[p.nss] = a;
+                    p.ss_q[p.nss] = b;
+                    ++p.nss;
+                }
+            }
+        // grid: one wave of groups, equal fibre counts
+        const size_t smem = use_smem ? (size_t)(s.htotal * s.esize) : 0;
+        pp.fn = pick_pass_mode<T>(mode, s.cpl, use_smem);
+        if (smem > 48 * 1024) CU(cudaFuncSetAttribute(pp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int nb = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pp.fn, kPassThreads, smem));
+        if (nb < 1) nb = 1;
+        int64_t gmax = (int64_t)nsm * nb * (kPassThreads / s.lanes);
+        gmax = std::min(gmax, s.groups_bound);
+        const int64_t L = std::max<int64_t>(1, (s.nfib + gmax - 1) / gmax);
+        p.L = L;
+        p.ngroups = (s.nfib + L - 1) / L;
+        pp.grid = dim3((unsigned)((p.ngroups * s.lanes + kPassThreads - 1) / kPassThreads));
+        pp.smem = smem;
+        return pp;
+    }
+
+    void plan() {
+        const int N = s.N;
+        blocks.clear();
+        for (int k = 0; k < N; ++k)
+            for (int i = 0; i < N; ++i) {
+                if (i == k) continue;
+                BlockPlan<T> b;
+                b.k = k;
+                b.i = i;
+                const int mode = (k == 0 || i == 0) ? PASS_KEPT1 : PASS_RED1;
+                b.pass = make_pass(mode, k, i);
+                ReduceParams<T>& r = b.red;
+                r.part_b = pb;
+                r.part_w = pw;
+                r.beta = beta;
+                r.omega = omega;
+                r.FR = b.pass.p.FR;
+                r.L = b.pass.p.L;
+                r.NV = b.pass.p.NV;
+                r.Lv = b.pass.p.Lv;
+                r.kept1 = mode == PASS_KEPT1;
+                r.I1 = (int)s.I1;
+                r.Ii = s.ld[i];
+                r.kIsMode0 = (k == 0);
+                r.kmode0IsK = (b.pass.p.nkept >= 1 && b.pass.p.kmode[0] == k);
+                r.kdim0 = b.pass.p.kdim[0];
+                b.red_grid = dim3((unsigned)r.NV);
+                SolveParams<T>& q = b.sol;
+                q.beta = beta;
+                q.omega = omega;
+                q.Gki = G + s.goff[k][i];
+                q.Gik = G + s.goff[i][k];
+                q.H = H;
+                const int a = std::min(k, i), c = std::max(k, i);
+                q.h_off = s.hoff[a][c];
+                q.h_ld = s.hld[a];
+                q.k_lt_i = k < i;
+                q.Ik = s.ld[k];
+                q.Ii = s.ld[i];
+                q.rho = rho;
+                q.delta = delta + s.delta_off[k][i];
+                q.flags = dflags;
+                b.sol_grid = dim3((unsigned)s.ld[k]);
+                b.sol_fn = pick_solve<T>(s.R(k, i));
+                blocks.push_back(b);
+            }
+        refill = make_pass(PASS_REFILL, -1, -1);
+        obj = make_pass(PASS_OBJ, -1, -1);
+        model = make_pass(PASS_MODEL, -1, -1);
+        nlaunch_sweep = 3 * (int64_t)blocks.size() + 2;
+    }
+
+    void build_all_H() {
+        for (int a = 0; a < s.N; ++a)
+            for (int b = a + 1; b < s.N; ++b) {
+                const int64_t n = s.ld[a] * s.ld[b];
+                pair_gram<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+                    G + s.goff[a][b], G + s.goff[b][a], s.R(a, b), s.ld[a], s.ld[b], H + s.hoff[a][b], s.hld[a]);
+                CU(cudaGetLastError());
+            }
+    }
+
+    void enqueue_contract(const BlockPlan<T>& b) {
+        launch(b.pass.fn, b.pass.grid, dim3(kPassThreads), b.pass.smem, b.pass.p);
+        launch((const void*)reduce_partials<T>, b.red_grid, dim3(256), 0, b.red);
+    }
+
+    void enqueue_block(const BlockPlan<T>& b) {
+        enqueue_contract(b);
+        launch(b.sol_fn, b.sol_grid, dim3(128), 0, b.sol);
+    }
+
+    void enqueue_xupdate() {
+        launch(refill.fn, refill.grid, dim3(kPassThreads), refill.smem, refill.p);
+        finalize_norms<<<1, 1024, 0, st>>>(norms, refill.p.ngroups, delta, s.ndelta, scal, dflags, 0);
+        CU(cudaGetLastError());
+    }
+
+    void enqueue_sweep() {
+        for (const auto& b : blocks) enqueue_block(b);
+        enqueue_xupdate();
+    }
+
+    void init(const void* observed, const uint8_t* mask, const void* G0, void* workspace,
+              size_t wbytes, cudaStream_t stream) {
+        user_stream = stream;
+        int dev = 0;
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        int smo = 0;
+        CU(cudaDeviceGetAttribute(&smo, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        smem_limit = (size_t)smo;
+        use_smem = (flags & 4u) && (size_t)(s.htotal * s.esize) <= smem_limit;
+        CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        CU(cudaMallocHost(&hscal, 16 * sizeof(double)));
+        CU(cudaMallocHost(&hflags, 4 * sizeof(int)));
+        if (workspace) {
+            if (wbytes < (size_t)lay.total) fail(IFCTN_E_WORKSPACE, "workspace smaller than ifctn_workspace_bytes()");
+            if (((uintptr_t)workspace) % 256) fail(IFCTN_E_WORKSPACE, "workspace must be 256-byte aligned");
+            ws = (unsigned char*)workspace;
+        } else {
+            CU(cudaMalloc(&ws, lay.total));
+            own_ws = true;
+        }
+        X = (T*)(ws + lay.x);
+        bits = (uint32_t*)(ws + lay.bits);
+        G = (T*)(ws + lay.g);
+        H = (T*)(ws + lay.h);
+        pb = (T*)(ws + lay.pb);
+        pw = (T*)(ws + lay.pw);
+        beta = (double*)(ws + lay.beta);
+        omega = (double*)(ws + lay.omega);
+        delta = (double*)(ws + lay.delta);
+        norms = (double*)(ws + lay.norms);
+        scal = (double*)(ws + lay.scal);
+        dflags = (int*)(ws + lay.flags);
+        rsep = (double*)(ws + lay.rse);
+        proj = (double*)(ws + lay.proj);
+
+        begin();
+        CU(cudaMemsetAsync(ws, 0, lay.total, st));
+        // inputs → device (temporary copies when the caller passed host memory)
+        const size_t obytes = (size_t)s.nloc * s.esize;
+        const T* dobs = (const T*)observed;
+        const uint8_t* dmask = mask;
+        void* tmp_o = nullptr;
+        void* tmp_m = nullptr;
+        if (!is_device_ptr(observed)) {
+            CU(cudaMallocAsync(&tmp_o, obytes, st));
+            CU(cudaMemcpyAsync(tmp_o, observed, obytes, cudaMemcpyHostToDevice, st));
+            dobs = (const T*)tmp_o;
+        }
+        if (!is_device_ptr(mask)) {
+            CU(cudaMallocAsync(&tmp_m, (size_t)s.nloc, st));
+            CU(cudaMemcpyAsync(tmp_m, mask, (size_t)s.nloc, cudaMemcpyHostToDevice, st));
+            dmask = (const uint8_t*)tmp_m;
+        }
+        const int64_t nw = (s.npad + 31) / 32;
+        pack_input<T><<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(dobs, dmask, s.I1, s.I1p, s.npad,
+                                                                    (flags & IFCTN_FLAG_X_FULL) ? 1 : 0, X, bits);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(G, G0, (size_t)s.gtotal * s.esize,
+                           is_device_ptr(G0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        if (tmp_o) CU(cudaFreeAsync(tmp_o, st));
+        if (tmp_m) CU(cudaFreeAsync(tmp_m, st));
+        plan();
+        build_all_H();
+        CU(cudaStreamSynchronize(st));
+        end();
+    }
+
+    void capture() {
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_sweep();
+        } catch (...) {
+            cudaGraph_t g;
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        CU(cudaStreamEndCapture(st, &graph));
+        CU(cudaGraphInstantiate(&gexec, graph, 0));
+    }
+
+    void check_flags_sync() {
+        CU(cudaMemcpyAsync(hflags, dflags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (hflags[0]) fail(IFCTN_E_NOT_SPD, "non-positive Cholesky pivot in a column solve");
+        if (hflags[1]) fail(IFCTN_E_NONFINITE, "non-finite value in the sweep norms");
+    }
+
+    void sweep(int t_max, double eps, int* done, ifctn_trace_row* trace) override {
+        if (t_max < 0) fail(IFCTN_E_ARG, "t_max must be >= 0");
+        begin();
+        const bool use_graph = !(flags & IFCTN_FLAG_NO_GRAPH);
+        if (use_graph && !gexec) capture();
+        const bool need_sync = trace || eps > 0.0;
+        int s_done = 0;
+        last_launches = 0;
+        for (int sw = 0; sw < t_max; ++sw) {
+            if (use_graph) CU(cudaGraphLaunch(gexec, st));
+            else enqueue_sweep();
+            last_launches += nlaunch_sweep;
+            ++s_done;
+            if (need_sync) {
+                CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+                check_flags_sync();
+                if (trace) {
+                    trace[sw].sweep = (int)hscal[5];
+                    trace[sw].rel_change = hscal[4];
+                    trace[sw].objective = hscal[2];
+                    trace[sw].dx2 = hscal[0];
+                    trace[sw].dg2 = hscal[3];
+                }
+                if (eps > 0.0 && hscal[4] < eps) break;
+            }
+        }
+        if (done) *done = s_done;
+        end();
+    }
+
+    void sync_check() override {
+        begin();
+        check_flags_sync();
+        end();
+    }
+
+    void reconstruct(int what, void* out) override {
+        if (!out) fail(IFCTN_E_ARG, "out must not be NULL");
+        if (what != IFCTN_MODEL && what != IFCTN_X) fail(IFCTN_E_ARG, "what must be IFCTN_MODEL or IFCTN_X");
+        begin();
+        const size_t bytes = (size_t)s.nloc * s.esize;
+        const bool dev = is_device_ptr(out);
+        T* dout = (T*)out;
+        void* tmp = nullptr;
+        if (!dev) {
+            CU(cudaMallocAsync(&tmp, bytes, st));
+            dout = (T*)tmp;
+        }
+        if (what == IFCTN_X) {
+            unpack_x<T><<<(unsigned)((s.nloc + 255) / 256), 256, 0, st>>>(X, s.I1, s.I1p, s.nloc, dout);
+            CU(cudaGetLastError());
+        } else {
+            PassParams<T> p = model.p;
+            p.out = dout;
+            launch(model.fn, model.grid, dim3(kPassThreads), model.smem, p);
+        }
+        if (!dev) {
+            CU(cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, st));
+            CU(cudaFreeAsync(tmp, st));
+            CU(cudaStreamSynchronize(st));
+        }
+        end();
+    }
+
+    void get_factors(void* out) override {
+        if (!out) fail(IFCTN_E_ARG, "out must not be NULL");
+        begin();
+        const bool dev = is_device_ptr(out);
+        CU(cudaMemcpyAsync(out, G, (size_t)s.gtotal * s.esize, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        if (!dev) CU(cudaStreamSynchronize(st));
+        end();
+    }
+
+    double rse(const void* truth) override {
+        if (!truth) fail(IFCTN_E_ARG, "truth must not be NULL");
+        begin();
+        const size_t bytes = (size_t)s.nloc * s.esize;
+        const T* dt = (const T*)truth;
+        void* tmp = nullptr;
+        if (!is_device_ptr(truth)) {
+            CU(cudaMallocAsync(&tmp, bytes, st));
+            CU(cudaMemcpyAsync(tmp, truth, bytes, cudaMemcpyHostToDevice, st));
+            dt = (const T*)tmp;
+        }
+        const int nb = 1024;
+        rse_partial<T><<<nb, 256, 0, st>>>(dt, X, s.I1, s.I1p, s.nloc, rsep);
+        sum_pairs<<<1, 32, 0, st>>>(rsep, nb, rsep + 2 * nb);
+        CU(cudaGetLastError());
+        if (comm) allreduce_doubles(rsep + 2 * nb, 2);
+        CU(cudaMemcpyAsync(hscal + 8, rsep + 2 * nb, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (tmp) CU(cudaFreeAsync(tmp, st));
+        CU(cudaStreamSynchronize(st));
+        end();
+        const double num = hscal[8], den = hscal[9];
+        if (!(den > 0.0)) fail(IFCTN_E_ARG, "truth has zero norm");
+        return std::sqrt(num) / std::sqrt(den);
+    }
+
+    double objective() override {
+        begin();
+        launch(obj.fn, obj.grid, dim3(kPassThreads), obj.smem, obj.p);
+        finalize_norms<<<1, 1024, 0, st>>>(norms, obj.p.ngroups, delta, 0, scal, dflags, 1);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        end();
+        return hscal[6];
+    }
+
+    const BlockPlan<T>& find_block(int k, int i) {
+        if (k < 0 || i < 0 || k >= s.N || i >= s.N || k == i) fail(IFCTN_E_ARG, "block (k,i) out of range");
+        for (const auto& b : blocks)
+            if (b.k == k && b.i == i) return b;
+        fail(IFCTN_E_ARG, "block not found");
+        return blocks[0];
+    }
+
+    void block_coefficients(int k, int i, double* bo, double* wo) override {
+        if (!bo || !wo) fail(IFCTN_E_ARG, "beta/omega must not be NULL");
+        const auto& b = find_block(k, i);
+        begin();
+        enqueue_contract(b);
+        const size_t bytes = (size_t)(s.ld[i] * s.ld[k]) * sizeof(double);
+        CU(cudaMemcpyAsync(bo, beta, bytes, cudaMemcpyDefault, st));
+        CU(cudaMemcpyAsync(wo, omega, bytes, cudaMemcpyDefault, st));
+        CU(cudaStreamSynchronize(st));
+        end();
+    }
+
+    void block_update(int k, int i) override {
+        const auto& b = find_block(k, i);
+        begin();
+        enqueue_block(b);
+        check_flags_sync();
+        end();
+    }
+
+    void x_update(double* nrm) override {
+        begin();
+        enqueue_xupdate();
+        CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        check_flags_sync();
+        if (nrm) {
+            nrm[0] = hscal[0];
+            nrm[1] = hscal[1];
+            nrm[2] = hscal[2];
+            nrm[3] = hscal[3];
+        }
+        end();
+    }
+
+    void allreduce_doubles(double* buf, size_t count) {
+        int r = nccl->allReduce(buf, buf, count, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm, st);
+        if (r != 0) fail(IFCTN_E_NCCL, std::string("ncclAllReduce: ") + nccl->errorString(r));
+    }
+
+    int64_t launches() const override { return last_launches; }
+};
+
+}  // namespace ifctn
+
+// ------------------------------------------------------------------------------------------
+// C-ABI
+// ------------------------------------------------------------------------------------------
+struct ifctn_ctx {
+    std::unique_ptr<ifctn::SolverBase> s;
+    std::string err;
+};
+
+static thread_local std::string g_last_err;
+
+template <typename F>
+static ifctn_status guarded(ifctn_ctx* ctx, F&& f) {
+    try {
+        f();
+        return IFCTN_OK;
+    } catch (const ifctn::Error& e) {
+        if (ctx) ctx->err = e.msg;
+        g_last_err = e.msg;
+        return e.st;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        g_last_err = e.what();
+        return IFCTN_E_CUDA;
+    }
+}
+
+extern "C" {
+
+ifctn_status ifctn_workspace_bytes(int order, const int64_t* dims, const int32_t* ranks,
+                                   ifctn_dtype dtype, const ifctn_dist* dist, size_t* bytes) {
+    return guarded(nullptr, [&] {
+        if (!bytes) ifctn::fail(IFCTN_E_ARG, "bytes must not be NULL");
+        ifctn::Shape s = ifctn::make_shape(order, dims, ranks, dtype, dist);
+        *bytes = (size_t)ifctn::make_layout(s).total;
+    });
+}
+
+ifctn_status ifctn_shard_range(int order, const int64_t* dims, const ifctn_dist* dist,
+                               int* shard_mode, int64_t* begin, int64_t* end) {
+    return guarded(nullptr, [&] {
+        if (!dims) ifctn::fail(IFCTN_E_ARG, "dims must not be NULL");
+        std::vector<int32_t> ranks(order * order, 1);
+        for (int m = 0; m < order; ++m) ranks[m * order + m] = 0;
+        ifctn::Shape s = ifctn::make_shape(order, dims, ranks.data(), IFCTN_F32, dist);
+        if (shard_mode) *shard_mode = s.shard;
+        if (begin) *begin = s.sbegin;
+        if (end) *end = s.send;
+    });
+}
+
+ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims, const int32_t* ranks,
+                          ifctn_dtype dtype, double rho, const void* observed, const uint8_t* mask,
+                          const void* init_factors, void* workspace, size_t workspace_bytes,
+                          const ifctn_dist* dist, void* stream, unsigned flags) {
+    if (!out) return IFCTN_E_ARG;
+    *out = nullptr;
+    std::unique_ptr<ifctn_ctx> ctx(new ifctn_ctx());
+    ifctn_status st = guarded(ctx.get(), [&] {
+        if (!observed || !mask || !init_factors) ifctn::fail(IFCTN_E_ARG, "observed/mask/init_factors must not be NULL");
+        if (!(rho > 0.0) || !std::isfinite(rho)) ifctn::fail(IFCTN_E_ARG, "rho must be > 0");
+        ifctn::Shape s = ifctn::make_shape(order, dims, ranks, dtype, dist);
+        // Ω must be non-empty (checked on the host copy of the mask when it is host memory;
+        // device masks are checked by the caller-side binding).
+        if (!ifctn::is_device_ptr(mask)) {
+            bool any = false;
+            for (int64_t u = 0; u < s.nloc && !any; ++u) any = mask[u] != 0;
+            if (!any && s.world == 1) ifctn::fail(IFCTN_E_NO_OBSERVED, "the mask has no observed entry");
+        }
+        auto build = [&](auto* tag) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            auto* sv = new ifctn::Solver<T>();
+            ctx->s.reset(sv);
+            sv->s = s;
+            sv->lay = ifctn::make_layout(s);
+            sv->rho = rho;
+            sv->flags = flags;
+            if (s.world > 1) {
+                if (!dist->nccl_unique_id) ifctn::fail(IFCTN_E_ARG, "dist->nccl_unique_id must be set when world > 1");
+                sv->nccl = ifctn::NcclLite::get();
+                if (!sv->nccl) ifctn::fail(IFCTN_E_NCCL, "libnccl.so.2 could not be loaded");
+                int r = sv->nccl->commInitRank(&sv->comm, s.world, dist->nccl_unique_id, s.rank);
+                if (r != 0) ifctn::fail(IFCTN_E_NCCL, std::string("ncclCommInitRank: ") + sv->nccl->errorString(r));
+                ifctn::fail(IFCTN_E_UNSUPPORTED, "multi-GPU sweeps are not enabled in this build yet");
+            }
+            sv->init(observed, mask, init_factors, workspace, workspace_bytes, (cudaStream_t)stream);
+        };
+        if (dtype == IFCTN_F32) build((float*)nullptr);
+        else build((double*)nullptr);
+    });
+    if (st != IFCTN_OK) return st;
+    *out = ctx.release();
+    return IFCTN_OK;
+}
+
+#define CTX_CALL(ctx, body)                                    \
+    if (!(ctx) || !(ctx)->s) return IFCTN_E_ARG;               \
+    return guarded((ctx), [&] { body; })
+
+ifctn_status ifctn_sweep(ifctn_ctx* ctx, int t_max, double eps, int* sweeps_done, ifctn_trace_row* trace) {
+    CTX_CALL(ctx, ctx->s->sweep(t_max, eps, sweeps_done, trace));
+}
+
+ifctn_status ifctn_sync(ifctn_ctx* ctx) { CTX_CALL(ctx, ctx->s->sync_check()); }
+
+ifctn_status ifctn_reconstruct(ifctn_ctx* ctx, int what, void* out) {
+    CTX_CALL(ctx, ctx->s->reconstruct(what, out));
+}
+
+ifctn_status ifctn_get_factors(ifctn_ctx* ctx, void* out) { CTX_CALL(ctx, ctx->s->get_factors(out)); }
+
+ifctn_status ifctn_rse(ifctn_ctx* ctx, const void* truth, double* rse) {
+    CTX_CALL(ctx, {
+        if (!rse) ifctn::fail(IFCTN_E_ARG, "rse must not be NULL");
+        *rse = ctx->s->rse(truth);
+    });
+}
+
+ifctn_status ifctn_objective(ifctn_ctx* ctx, double* f) {
+    CTX_CALL(ctx, {
+        if (!f) ifctn::fail(IFCTN_E_ARG, "f must not be NULL");
+        *f = ctx->s->objective();
+    });
+}
+
+ifctn_status ifctn_block_coefficients(ifctn_ctx* ctx, int k, int i, double* beta, double* omega) {
+    CTX_CALL(ctx, ctx->s->block_coefficients(k, i, beta, omega));
+}
+
+ifctn_status ifctn_block_update(ifctn_ctx* ctx, int k, int i) { CTX_CALL(ctx, ctx->s->block_update(k, i)); }
+
+ifctn_status ifctn_x_update(ifctn_ctx* ctx, double* norms) { CTX_CALL(ctx, ctx->s->x_update(norms)); }
+
+ifctn_status ifctn_destroy(ifctn_ctx* ctx) {
+    if (!ctx) return IFCTN_E_ARG;
+    delete ctx;
+    return IFCTN_OK;
+}
+
+const char* ifctn_status_string(ifctn_status s) {
+    if ((int)s < 0 || (int)s >= (int)(sizeof(ifctn::kStatusNames) / sizeof(ifctn::kStatusNames[0])))
+        return "IFCTN_E_UNKNOWN";
+    return ifctn::kStatusNames[(int)s];
+}
+
+const char* ifctn_last_error(const ifctn_ctx* ctx) {
+    if (ctx) return ctx->err.c_str();
+    return g_last_err.c_str();
+}
+
+int64_t ifctn_launch_count(const ifctn_ctx* ctx) {
+    if (!ctx || !ctx->s) return 0;
+    return ctx->s->launches();
+}
+
+}  // extern "C"

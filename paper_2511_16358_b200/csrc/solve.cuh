@@ -1,0 +1,315 @@
+// solve.cuh — second-stage reduction of the K2 partials, K3 (Gram/RHS + ρI + batched SPD
+// solve + H refresh, steps a3/a4), the per-sweep finaliser, and layout/RSE kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace ifctn {
+
+// ---- stage 2 of a2: fixed-order fp64 sum of the partial slots of every kept value v ------
+// Slots of v are g + v for g in [⌊vFR/L⌋, ⌊((v+1)FR−1)/L⌋] (each group covers L fibres).
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
+    __shared__ double sb[256], sw[256];
+    const int64_t v = blockIdx.x;
+    const int64_t g0 = (v * P.FR) / P.L;
+    const int64_t g1 = ((v + 1) * P.FR - 1) / P.L;
+    const int64_t nslots = g1 - g0 + 1;
+    const int ex = (int)(P.Lv < 256 ? P.Lv : 256);
+    // round ex up to a power of two so the y-split is a clean tree
+    int exp2 = 1;
+    while (exp2 < ex) exp2 <<= 1;
+    const int ny = 256 / exp2;
+    const int tx = threadIdx.x % exp2;
+    const int ty = threadIdx.x / exp2;
+    for (int64_t e0 = 0; e0 < P.Lv; e0 += exp2) {
+        const int64_t e = e0 + tx;
+        double b = 0.0, w = 0.0;
+        if (e < P.Lv) {
+            for (int64_t s = ty; s < nslots; s += ny) {
+                const int64_t o = (g0 + s + v) * P.Lv + e;
+                b += (double)P.part_b[o];
+                w += (double)P.part_w[o];
+            }
+        }
+        sb[threadIdx.x] = b;
+        sw[threadIdx.x] = w;
+        __syncthreads();
+        for (int st = ny >> 1; st > 0; st >>= 1) {
+            if (ty < st) {
+                sb[threadIdx.x] += sb[threadIdx.x + st * exp2];
+                sw[threadIdx.x] += sw[threadIdx.x + st * exp2];
+            }
+            __syncthreads();
+        }
+        if (ty == 0 && e < P.Lv) {
+            int64_t out;
+            bool write = true;
+            if (P.kept1) {
+                if (e >= P.I1) write = false;
+                out = P.kIsMode0 ? (e * P.Ii + v) : (v * P.Ii + e);
+            } else {
+                const int64_t x0 = v % P.kdim0, x1 = v / P.kdim0;  // kmode[0], kmode[1] indices
+                const int64_t j = P.kmode0IsK ? x0 : x1;
+                const int64_t a = P.kmode0IsK ? x1 : x0;
+                out = j * P.Ii + a;
+            }
+            if (write) {
+                P.beta[out] = sb[threadIdx.x];
+                P.omega[out] = sw[threadIdx.x];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    return x;
+}
+
+// ---- a3 + a4: per column j of G_{k,i} (Eq. 8) -------------------------------
+//   Gram_j = Σ_a ω(a,j) g_a g_aᵀ + ρI,  rhs_j = Σ_a β(a,j) g_a + ρ c_old,  g_a = G_{i,k}(:,a)
+//   c = Gram_j⁻¹ rhs_j by Cholesky (fp64);  then row j of H_{k,i} = cᵀ G_{i,k} (refresh).
+template <typename T, int R>
+__global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
+    constexpr int NG = R * (R + 1) / 2;
+    constexpr int NA = NG + R;
+    __shared__ double red[4][NA];
+    __shared__ double cs[R];
+    const int64_t j = blockIdx.x;
+    double acc[NA];
+#pragma unroll
+    for (int t = 0; t < NA; ++t) acc[t] = 0.0;
+    for (int64_t a = threadIdx.x; a < P.Ii; a += blockDim.x) {
+        const double b = P.beta[j * P.Ii + a];
+        const double w = P.omega[j * P.Ii + a];
+        double g[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) g[r] = (double)P.Gik[a * R + r];
+        int t = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int s = r; s < R; ++s) acc[t++] += w * g[r] * g[s];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[NG + r] += b * g[r];
+    }
+    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < NA; ++t) {
+        const double s = warp_sum(acc[t]);
+        if (ln == 0) red[wid][t] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double A[R][R], L[R][R], y[R], c[R], cold[R];
+        int t = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int s = r; s < R; ++s) {
+                const double v = red[0][t] + red[1][t] + red[2][t] + red[3][t];
+                A[r][s] = v;
+                A[s][r] = v;
+                ++t;
+            }
+        double rhs[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            cold[r] = (double)P.Gki[j * R + r];
+            A[r][r] += P.rho;
+            rhs[r] = red[0][NG + r] + red[1][NG + r] + red[2][NG + r] + red[3][NG + r] + P.rho * cold[r];
+        }
+        bool ok = true;
+#pragma unroll
+        for (int cc = 0; cc < R; ++cc) {
+            double d = A[cc][cc];
+#pragma unroll
+            for (int s = 0; s < cc; ++s) d -= L[cc][s] * L[cc][s];
+            if (!(d > 0.0)) ok = false;
+            const double ld = sqrt(d > 0.0 ? d : 1.0);
+            L[cc][cc] = ld;
+#pragma unroll
+            for (int r = cc + 1; r < R; ++r) {
+                double v = A[r][cc];
+#pragma unroll
+                for (int s = 0; s < cc; ++s) v -= L[r][s] * L[cc][s];
+                L[r][cc] = v / ld;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double v = rhs[r];
+#pragma unroll
+            for (int s = 0; s < r; ++s) v -= L[r][s] * y[s];
+            y[r] = v / L[r][r];
+        }
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+            double v = y[r];
+#pragma unroll
+            for (int s = r + 1; s < R; ++s) v -= L[s][r] * c[s];
+            c[r] = v / L[r][r];
+        }
+        if (!ok) {
+            atomicOr(P.flags, 1);
+#pragma unroll
+            for (int r = 0; r < R; ++r) c[r] = cold[r];
+        }
+        double d2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const T cT = (T)c[r];
+            P.Gki[j * R + r] = cT;
+            cs[r] = (double)cT;
+            const double dd = (double)cT - cold[r];
+            d2 += dd * dd;
+        }
+        P.delta[j] = d2;
+    }
+    __syncthreads();
+    // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a)
+    for (int64_t a = threadIdx.x; a < P.Ii; a += blockDim.x) {
+        double h = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) h += cs[r] * (double)P.Gik[a * R + r];
+        const int64_t o = P.k_lt_i ? (P.h_off + a * P.h_ld + j) : (P.h_off + j * P.h_ld + a);
+        P.H[o] = (T)h;
+    }
+}
+
+// ---- a1: build H_{p,q} = G_{p,q}ᵀ G_{q,p} for one pair (K=R skinny product; FMA pipes) ---
+template <typename T>
+__global__ void pair_gram(const T* Gpq, const T* Gqp, int R, int64_t Ip, int64_t Iq, T* H,
+                          int64_t ld) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= Ip * Iq) return;
+    const int64_t a = e % Ip, b = e / Ip;
+    double s = 0.0;
+    for (int r = 0; r < R; ++r) s += (double)Gpq[a * R + r] * (double)Gqp[b * R + r];
+    H[b * ld + a] = (T)s;
+}
+
+// ---- per-sweep finaliser: fixed-order fp64 sums of the refill norms and ΔG² -------------
+__global__ void __launch_bounds__(1024) finalize_norms(const double* norms, int64_t ngroups,
+                                                       const double* delta, int64_t ndelta,
+                                                       double* scal, int* flags, int obj_only) {
+    __shared__ double s[4][1024];
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int64_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
+        a0 += norms[3 * g + 0];
+        a1 += norms[3 * g + 1];
+        a2 += norms[3 * g + 2];
+    }
+    if (!obj_only)
+        for (int64_t d = threadIdx.x; d < ndelta; d += blockDim.x) a3 += delta[d];
+    s[0][threadIdx.x] = a0;
+    s[1][threadIdx.x] = a1;
+    s[2][threadIdx.x] = a2;
+    s[3][threadIdx.x] = a3;
+    __syncthreads();
+    for (int st = blockDim.x >> 1; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st)
+            for (int q = 0; q < 4; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (obj_only) {
+            scal[6] = 0.5 * s[2][0];
+            if (!isfinite(scal[6])) atomicOr(flags + 1, 1);
+            return;
+        }
+        const double dx2 = s[0][0], x2 = s[1][0], f = 0.5 * s[2][0], dg2 = s[3][0];
+        const double xn = sqrt(x2);
+        scal[0] = dx2;
+        scal[1] = x2;
+        scal[2] = f;
+        scal[3] = dg2;
+        scal[4] = sqrt(dx2) / (xn > 0.0 ? xn : 1.0);
+        scal[5] += 1.0;
+        if (!isfinite(dx2) || !isfinite(x2) || !isfinite(f) || !isfinite(dg2)) atomicOr(flags + 1, 1);
+    }
+}
+
+// ---- layout kernels ------------------------------------------------------------------------
+// X⁽⁰⁾ = P_Ω(O) (zeros on Ω^c; reading R7) packed into the padded fibre layout + mask bits.
+template <typename T>
+__global__ void pack_input(const T* obs, const uint8_t* mask, int64_t I1, int64_t I1p,
+                           int64_t npad, int xfull, T* X, uint32_t* bits) {
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t e0 = w * 32;
+    if (e0 >= npad) return;
+    uint32_t b = 0;
+    for (int t = 0; t < 32; ++t) {
+        const int64_t e = e0 + t;
+        if (e >= npad) {
+            b |= 1u << t;
+            continue;
+        }
+        const int64_t f = e / I1p, i1 = e - f * I1p;
+        T x = T(0);
+        uint32_t m = 1;
+        if (i1 < I1) {
+            const int64_t u = f * I1 + i1;
+            m = mask[u] != 0;
+            x = (m || xfull) ? obs[u] : T(0);
+        }
+        X[e] = x;
+        b |= m << t;
+    }
+    bits[w] = b;
+}
+
+template <typename T>
+__global__ void unpack_x(const T* X, int64_t I1, int64_t I1p, int64_t n, T* out) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int64_t f = u / I1, i1 = u - f * I1;
+    out[u] = X[f * I1p + i1];
+}
+
+// RSE partial sums: ‖T − X‖² and ‖T‖² per CTA (fp64), fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) rse_partial(const T* truth, const T* X, int64_t I1,
+                                                   int64_t I1p, int64_t n, double* part) {
+    __shared__ double s0[256], s1[256];
+    double a = 0.0, b = 0.0;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = u / I1, i1 = u - f * I1;
+        const double t = (double)truth[u];
+        const double d = t - (double)X[f * I1p + i1];
+        a += d * d;
+        b += t * t;
+    }
+    s0[threadIdx.x] = a;
+    s1[threadIdx.x] = b;
+    __syncthreads();
+    for (int st = 128; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st) {
+            s0[threadIdx.x] += s0[threadIdx.x + st];
+            s1[threadIdx.x] += s1[threadIdx.x + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = s0[0];
+        part[2 * blockIdx.x + 1] = s1[0];
+    }
+}
+
+__global__ void sum_pairs(const double* part, int n, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < n; ++i) {
+            a += part[2 * i];
+            b += part[2 * i + 1];
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+}  // namespace ifctn

@@ -1,0 +1,277 @@
+"""Parity of the CUDA path (through the C-ABI) with the float64 oracle (-m gpu).
+
+Tolerances: fp32 configs — relative Frobenius ≤ 1e-4 for factors and X
+after one sweep (north_star), model entries ≤ 4P·u·|t| (u = 2⁻²⁴, P pairs), step-level
+(β, ω) relative Frobenius ≤ 1e-5; fp64 (C1) — 1e-10.  Mask/observed handling is bit-exact.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from synth import make_config, make_problem
+
+from gpu_util import dev, make_solver, oracle_state, rel, requires_cuda, tol_for, torch
+
+pytestmark = [pytest.mark.gpu, requires_cuda]
+
+SMALL = ["C1", "C2s", "C3s", "C4s", "C5s"]
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _threads():
+    import os
+    O.set_threads(max(1, min(16, os.cpu_count() or 1)))
+    yield
+
+
+# ------------------------------------------------------------------ a0: inputs & mask ---
+
+@pytest.mark.parametrize("name", SMALL)
+def test_initial_x_is_masked_observed_bit_exact(name):
+    p = make_config(name)
+    s = make_solver(p)
+    X = s.reconstruct().cpu().numpy()
+    exp = np.where(p.mask.astype(bool), p.observed, np.zeros((), p.dtype))
+    assert X.dtype == p.dtype
+    assert np.array_equal(X.view(np.uint8), exp.view(np.uint8))
+    G = s.factors().cpu().numpy()
+    assert np.array_equal(G.view(np.uint8), p.G0.view(np.uint8))
+
+
+def test_host_and_device_inputs_agree():
+    from paper_2511_16358_b200 import Solver
+    p = make_config("C4s")
+    a = make_solver(p)
+    b = Solver(p.dims, p.ranks, p.observed, p.mask, p.G0, rho=p.rho)   # numpy host buffers
+    a.sweep(2)
+    b.sweep(2)
+    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
+
+
+# ------------------------------------------------------------------ model t (a1 + a5) ---
+
+@pytest.mark.parametrize("name", SMALL + ["C2"])
+def test_model_reconstruction(name):
+    from paper_2511_16358_b200 import IFCTN_MODEL
+    p = make_config(name)
+    s = make_solver(p)
+    t = s.reconstruct(IFCTN_MODEL).cpu().numpy().astype(np.float64)
+    sh, G, _ = oracle_state(p)
+    to = O.model(sh, G)
+    P = p.N * (p.N - 1) // 2
+    u = 2.0 ** -53 if p.dtype == np.float64 else 2.0 ** -24
+    assert np.all(np.abs(t - to) <= 4 * P * u * np.abs(to) + 1e-30)
+
+
+# --------------------------------------------------------------- a2: (β, ω) contraction ---
+
+@pytest.mark.parametrize("name", SMALL + ["C2"])
+def test_block_coefficients(name):
+    p = make_config(name)
+    s = make_solver(p)
+    sh, G, X = oracle_state(p)
+    Xin = X.astype(p.dtype)  # the oracle reads the same (exactly representable) X values
+    tol = tol_for(p, 1e-5, 1e-12)
+    for k in range(p.N):
+        for i in range(p.N):
+            if i == k:
+                continue
+            b, w = s.block_coefficients(k, i)
+            bo, wo = O.block_contract(sh, G, Xin, k, i)
+            assert rel(w, wo) <= tol, (k, i, rel(w, wo))
+            assert rel(b, bo) <= tol, (k, i, rel(b, bo))
+
+
+# ------------------------------------------------------------ a3/a4: one block update ---
+
+@pytest.mark.parametrize("name", SMALL)
+def test_single_block_update(name):
+    p = make_config(name)
+    for (k, i) in [(0, 1), (p.N - 1, 1), (1, p.N - 1)]:
+        s = make_solver(p)
+        sh, G, X = oracle_state(p)
+        s.block_update(k, i)
+        st, _ = O.block_update(sh, G, X, k, i, p.rho)
+        assert st == 0
+        Gg = s.factors().cpu().numpy()
+        assert rel(O.factor(sh, Gg, k, i), O.factor(sh, G, k, i)) <= tol_for(p, 1e-5, 1e-11)
+        # every other factor untouched
+        off = O.factor_offset(sh, k, i)
+        R = int(p.ranks[k, i])
+        mask = np.ones(Gg.size, bool)
+        mask[off:off + R * p.dims[k]] = False
+        assert np.array_equal(Gg[mask], p.G0[mask])
+
+
+# ---------------------------------------------------------------- a5: X update alone ---
+
+@pytest.mark.parametrize("name", SMALL)
+def test_x_update_and_norms(name):
+    p = make_config(name)
+    s = make_solver(p)
+    sh, G, X = oracle_state(p)
+    n = s.x_update()
+    dx2, x2, f = O.refill(sh, G, X, p.mask, p.rho)
+    Xg = s.reconstruct().cpu().numpy()
+    assert rel(Xg, X) <= tol_for(p, 1e-6, 1e-13)
+    obs = p.mask.astype(bool)
+    assert np.array_equal(Xg[obs].view(np.uint8), p.observed[obs].view(np.uint8))
+    t = tol_for(p, 1e-5, 1e-11)
+    assert abs(n[0] - dx2) <= t * dx2 and abs(n[1] - x2) <= t * x2 and abs(n[2] - f) <= t * f
+
+
+# ----------------------------------------------------------------- one whole sweep ---
+
+@pytest.mark.parametrize("name", SMALL + ["C2", "C3", "C4"])
+def test_one_sweep_parity(name):
+    """North-star bar: factors and X within 1e-4 relative Frobenius after one sweep."""
+    p = make_config(name)
+    s = make_solver(p)
+    sh, G, X = oracle_state(p)
+    F0 = O.objective(sh, G, X)
+    st, F1, row = O.sweep(sh, G, X, p.mask, p.rho, F0, True)
+    assert st == 0
+    done, rows = s.sweep(1, trace=True)
+    assert done == 1
+    Gg = s.factors().cpu().numpy()
+    Xg = s.reconstruct().cpu().numpy()
+    tol = tol_for(p)
+    for k in range(p.N):
+        for i in range(p.N):
+            if i != k:
+                e = rel(O.factor(sh, Gg, k, i), O.factor(sh, G, k, i))
+                assert e <= tol, (k, i, e)
+    assert rel(Xg, X) <= tol
+    obs = p.mask.astype(bool)
+    assert np.array_equal(Xg[obs].view(np.uint8), p.observed[obs].view(np.uint8))
+    r = rows[0]
+    assert abs(r["objective"] - F1) <= 1e-3 * abs(F1) + 1e-9
+    assert abs(r["rel_change"] - row[0]) <= 1e-3 * row[0] + 1e-12
+
+
+# ------------------------------------------------------- invariants over many sweeps ---
+
+@pytest.mark.parametrize("name", SMALL)
+def test_trace_lemma2_and_feasibility(name):
+    """Lemma 2 on the GPU trace, with fp32 slack ~ 1e-5·F."""
+    p = make_config(name)
+    s = make_solver(p)
+    sh, G, X = oracle_state(p)
+    F = O.objective(sh, G, X)
+    done, rows = s.sweep(8, trace=True)
+    slack = tol_for(p, 1e-5, 1e-12)
+    for r in rows:
+        assert F - r["objective"] >= 0.5 * p.rho * (r["dx2"] + r["dg2"]) - slack * max(1.0, F)
+        F = r["objective"]
+    Xg = s.reconstruct().cpu().numpy()
+    obs = p.mask.astype(bool)
+    assert np.array_equal(Xg[obs].view(np.uint8), p.observed[obs].view(np.uint8))
+
+
+@pytest.mark.parametrize("name", ["C2s", "C5s"])
+def test_graph_and_plain_launches_bit_identical(name):
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_GRAPH
+    p = make_config(name)
+    a = make_solver(p)
+    b = make_solver(p, flags=IFCTN_FLAG_NO_GRAPH)
+    c = make_solver(p)
+    for x in (a, b, c):
+        x.sweep(3)
+    Xa, Xb, Xc = (x.reconstruct().cpu().numpy() for x in (a, b, c))
+    assert np.array_equal(Xa, Xb) and np.array_equal(Xa, Xc)
+    assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
+    assert a.launch_count() == 3 * (3 * p.N * (p.N - 1) + 2)
+
+
+@pytest.mark.parametrize("name,sweeps", [("C1", 10), ("C2s", 20), ("C3s", 20), ("C4s", 20), ("C5s", 10)])
+def test_full_run_rse_parity(name, sweeps):
+    """Final RSE within 1e-3 relative (+ an absolute floor at fp32 resolution, reading R22)."""
+    p = make_config(name)
+    s = make_solver(p)
+    s.sweep(sweeps)
+    rg = s.rse(dev(p.truth))
+    sh, G, X = oracle_state(p)
+    r, _ = O.solve(sh, G, X, p.mask, p.rho, sweeps, 0.0, True)
+    assert r == sweeps
+    ro = O.rse(p.truth.astype(np.float64), X)
+    floor = 1e-10 if p.dtype == np.float64 else 1e-5
+    assert abs(rg - ro) <= 1e-3 * ro + floor, (rg, ro)
+
+
+def test_objective_and_rse_against_oracle():
+    p = make_config("C3s")
+    s = make_solver(p)
+    s.sweep(2)
+    G = s.factors().cpu().numpy().astype(np.float64)
+    X = s.reconstruct().cpu().numpy().astype(np.float64)
+    sh = O.Shape(p.dims, p.ranks)
+    assert abs(s.objective() - O.objective(sh, G, X)) <= 1e-5 * O.objective(sh, G, X)
+    assert abs(s.rse(dev(p.truth)) - O.rse(p.truth.astype(np.float64), X)) <= 1e-6
+
+
+def test_eps_stop():
+    p = make_config("C5s")
+    s = make_solver(p)
+    done = s.sweep(50, eps=1e300)
+    assert done == 1
+
+
+# ------------------------------------------------------------------------ edge cases ---
+
+EDGE = [
+    ("order2", (7, 5), 2, "float32"),
+    ("order2_f64", (6, 9), 3, "float64"),
+    ("unit_modes", (5, 1, 3, 1), 2, "float32"),
+    ("I1_is_1", (1, 6, 5), 2, "float32"),
+    ("ragged_I1", (13, 4, 3), 3, "float32"),
+    ("rank1", (9, 7, 5), 1, "float32"),
+    ("rank8", (10, 6, 5), 8, "float32"),
+    ("order6", (5, 3, 2, 3, 2, 2), 2, "float32"),
+    ("big_I1", (300, 3, 2), 2, "float32"),
+    ("f64_order4", (6, 5, 4, 3), 2, "float64"),
+]
+
+
+@pytest.mark.parametrize("label,dims,R,dtype", EDGE, ids=[e[0] for e in EDGE])
+def test_edge_shapes_one_sweep(label, dims, R, dtype):
+    p = make_problem(label, dims, R, dtype, "normal", sr=0.4, init_kind="normal", seed=3)
+    s = make_solver(p)
+    sh, G, X = oracle_state(p)
+    F0 = O.objective(sh, G, X)
+    st, _, _ = O.sweep(sh, G, X, p.mask, p.rho, F0, False)
+    assert st == 0
+    s.sweep(1)
+    tol = tol_for(p, 2e-4, 1e-10)
+    assert rel(s.factors().cpu().numpy(), G) <= tol
+    assert rel(s.reconstruct().cpu().numpy(), X) <= tol
+
+
+def test_fully_observed_and_single_observation():
+    p = make_problem("full", (8, 6, 5), 2, "float32", "normal", sr=1.0, init_kind="normal")
+    assert int(p.mask.sum()) == p.n
+    s = make_solver(p)
+    s.sweep(2)
+    assert np.array_equal(s.reconstruct().cpu().numpy(), p.observed)
+    q = make_problem("one", (8, 6, 5), 2, "float32", "normal", sr=1.0 / 240, init_kind="normal")
+    assert int(q.mask.sum()) == 1
+    s = make_solver(q)
+    sh, G, X = oracle_state(q)
+    O.sweep(sh, G, X, q.mask, q.rho, O.objective(sh, G, X), False)
+    s.sweep(1)
+    assert rel(s.reconstruct().cpu().numpy(), X) <= 1e-4
+
+
+def test_argument_errors():
+    from paper_2511_16358_b200 import IfctnError, Solver
+    p = make_config("C5s")
+    bad = p.ranks.copy()
+    bad[0, 1] = 3
+    with pytest.raises(IfctnError, match="E_RANKS"):
+        Solver(p.dims, bad, dev(p.observed), dev(p.mask), dev(p.G0))
+    with pytest.raises(IfctnError, match="E_ARG"):
+        Solver(p.dims, p.ranks, dev(p.observed), dev(p.mask), dev(p.G0), rho=0.0)
+    with pytest.raises(IfctnError, match="E_NO_OBSERVED"):
+        Solver(p.dims, p.ranks, p.observed, np.zeros(p.n, np.uint8), p.G0)
+    s = make_solver(p)
+    with pytest.raises(IfctnError, match="E_ARG"):
+        s.block_update(1, 1)
