@@ -163,6 +163,14 @@ ifctn_status ifctn_destroy(ifctn_ctx* ctx);
 const char* ifctn_status_string(ifctn_status s);
 const char* ifctn_last_error(const ifctn_ctx* ctx);
 
+/* Run ONE sweep as plain launches with a CUDA event before every kernel, on the context's
+ * stream, and return each launch's device time in ms, in launch order:
+ *   for every block (k asc, i asc, i≠k): [a2 fibre pass, a2 partial reduce, a3/a4 solve],
+ *   then [a5 refill pass, norm finaliser].
+ * *count = 3·N(N−1) + 2 (entries beyond `capacity` are dropped).  Advances the state by
+ * one sweep exactly like ifctn_sweep(ctx, 1, 0, …).                                    */
+ifctn_status ifctn_profile_sweep(ifctn_ctx* ctx, float* ms, int capacity, int* count);
+
 /* Kernel launches the last ifctn_sweep enqueued (graph nodes count as launches).         */
 int64_t ifctn_launch_count(const ifctn_ctx* ctx);
 

@@ -123,6 +123,10 @@ class Solver:
     def sync(self):
         _abi.ifctn_sync(self.ctx)
 
+    def profile_sweep(self):
+        """One sweep with per-launch CUDA-event timings (ms), see ifctn_profile_sweep."""
+        return _abi.ifctn_profile_sweep(self.ctx)
+
     def reconstruct(self, what=IFCTN_X, out=None):
         import torch
         if out is None:

@@ -53,6 +53,7 @@ SIGNATURES = {
                           ctypes.c_size_t, ctypes.POINTER(ifctn_dist), _VP, _U]),
     "ifctn_sweep": (_I, [_VP, _I, _D, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ifctn_trace_row)]),
     "ifctn_sync": (_I, [_VP]),
+    "ifctn_profile_sweep": (_I, [_VP, ctypes.POINTER(ctypes.c_float), _I, ctypes.POINTER(ctypes.c_int)]),
     "ifctn_reconstruct": (_I, [_VP, _I, _VP]),
     "ifctn_get_factors": (_I, [_VP, _VP]),
     "ifctn_rse": (_I, [_VP, _VP, ctypes.POINTER(ctypes.c_double)]),
@@ -135,6 +136,13 @@ def ifctn_sweep(ctx, t_max, eps=0.0, trace=None):
 
 def ifctn_sync(ctx):
     check(lib().ifctn_sync(ctx), ctx)
+
+
+def ifctn_profile_sweep(ctx, capacity=4096):
+    ms = (ctypes.c_float * capacity)()
+    cnt = ctypes.c_int(0)
+    check(lib().ifctn_profile_sweep(ctx, ms, capacity, ctypes.byref(cnt)), ctx)
+    return [ms[t] for t in range(min(cnt.value, capacity))]
 
 
 def ifctn_reconstruct(ctx, what, out_ptr):

@@ -258,6 +258,7 @@ struct SolverBase {
     virtual ~SolverBase() {}
     virtual void sweep(int t_max, double eps, int* done, ifctn_trace_row* trace) = 0;
     virtual void sync_check() = 0;
+    virtual int profile_sweep(float* ms, int cap) = 0;
     virtual void reconstruct(int what, void* out) = 0;
     virtual void get_factors(void* out) = 0;
     virtual double rse(const void* truth) = 0;
@@ -375,8 +376,20 @@ struct Solver : SolverBase {
         CU(cudaStreamWaitEvent(user_stream, ev_out, 0));
     }
 
+    // profiling (ifctn_profile_sweep): one event before every launch + one at the end
+    std::vector<cudaEvent_t> prof_ev;
+    bool profiling = false;
+    void prof_mark() {
+        if (!profiling) return;
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        CU(cudaEventRecord(e, st));
+        prof_ev.push_back(e);
+    }
+
     template <typename P>
     void launch(const void* fn, dim3 g, dim3 b, size_t smem, const P& p) {
+        prof_mark();
         void* args[] = {(void*)&p};
         CU(cudaLaunchKernel(fn, g, b, args, smem, st));
     }
@@ -556,6 +569,7 @@ struct Solver : SolverBase {
 
     void enqueue_xupdate() {
         launch(refill.fn, refill.grid, dim3(kPassThreads), refill.smem, refill.p);
+        prof_mark();
         finalize_norms<<<1, 1024, 0, st>>>(norms, refill.p.ngroups, delta, s.ndelta, scal, dflags, 0);
         CU(cudaGetLastError());
     }
@@ -684,6 +698,28 @@ struct Solver : SolverBase {
         }
         if (done) *done = s_done;
         end();
+    }
+
+    int profile_sweep(float* ms, int cap) override {
+        begin();
+        profiling = true;
+        prof_ev.clear();
+        try {
+            enqueue_sweep();
+            prof_mark();
+        } catch (...) {
+            profiling = false;
+            throw;
+        }
+        profiling = false;
+        CU(cudaStreamSynchronize(st));
+        const int n = (int)prof_ev.size() - 1;
+        for (int t = 0; t < n && t < cap; ++t) CU(cudaEventElapsedTime(ms + t, prof_ev[t], prof_ev[t + 1]));
+        for (auto e : prof_ev) cudaEventDestroy(e);
+        prof_ev.clear();
+        check_flags_sync();
+        end();
+        return n;
     }
 
     void sync_check() override {
@@ -920,6 +956,13 @@ ifctn_status ifctn_sweep(ifctn_ctx* ctx, int t_max, double eps, int* sweeps_done
 }
 
 ifctn_status ifctn_sync(ifctn_ctx* ctx) { CTX_CALL(ctx, ctx->s->sync_check()); }
+
+ifctn_status ifctn_profile_sweep(ifctn_ctx* ctx, float* ms, int capacity, int* count) {
+    CTX_CALL(ctx, {
+        if (!ms || !count || capacity < 1) ifctn::fail(IFCTN_E_ARG, "ms/count must not be NULL");
+        *count = ctx->s->profile_sweep(ms, capacity);
+    });
+}
 
 ifctn_status ifctn_reconstruct(ifctn_ctx* ctx, int what, void* out) {
     CTX_CALL(ctx, ctx->s->reconstruct(what, out));
