@@ -273,6 +273,8 @@ def run_ours(args):
                          "launches_per_step": B},
             "refill": {"achieved": refill_gbs, "frac": refill_gbs / hbm, "ms": refill_ms,
                        "bytes": refill_bytes},
+            "a2_ms_by_block": {f"{k},{i}": round(k2[b], 4) for b, (k, i) in enumerate(
+                [(k, i) for k in range(N) for i in range(N) if i != k])},
             "kernels_ms_per_sweep": {"a2_pass": sum(k2), "a2_reduce": sum(red),
                                      "a3a4_solve": sum(sol), "a5_refill": refill_ms,
                                      "finalize": fin_ms},

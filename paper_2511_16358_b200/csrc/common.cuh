@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace ifctn {
 
 constexpr int MAXN = 6;                        // IFCTN_MAX_ORDER
@@ -12,6 +14,7 @@ constexpr int MAXSF = MAXN - 2;                // pairs involving the fast mode 
 constexpr int MAXR = 8;                        // IFCTN_MAX_RANK
 constexpr int kPassThreads = 256;              // fiber-pass CTA size
 constexpr int kUnroll = 4;                     // fibers in flight per lane
+constexpr int kPassMinBlocks = 3;              // ≤ 85 registers: ≥ 24 warps per SM
 
 enum PassMode : int {
     PASS_KEPT1 = 0,   // a2, mode 1 (code mode 0) is one of the kept modes {k,i}
@@ -97,6 +100,8 @@ struct PassParams {
     int sf_fixmode[MAXSF];
     int64_t sf_fixmul[MAXSF];
     int64_t sf_inc[MAXSF];
+    int64_t ones_off;        // a column of I1p ones in H (the "fast factor" when nred == 0)
+    int sf_cap;              // per-group shared-memory slots for the fast scalar factors
 };
 
 template <typename T>

@@ -7,14 +7,16 @@
 //     β(a,j) = Σ_{i: i_i=a, i_k=j} M(i) X(i),   ω(a,j) = Σ_{i: i_i=a, i_k=j} M(i)²,
 //     M(i) = Π_{{p,q}≠{k,i}} H_{p,q}(i_p,i_q),   H_{p,q} = G_{p,q}ᵀ G_{q,p},
 // and Eq. 9 needs t(i) = Π_{p<q} H_{p,q}(i_p,i_q) per entry.  Z_k is never
-// materialised: the weight of an entry is rebuilt from the (small, on-chip) H matrices.
+// materialised: the weight of an entry is rebuilt from the (small, cache-resident) H.
 //
 // B200 mapping: one pass streams X once with 16-B loads; a "group" of
 // `lanes` threads owns whole mode-1 fibres, each lane fixed mode-1 positions (CPL chunks of
-// VW elements), so the mode-1 part of the weight is a per-lane vector that changes only with
-// the fast reduced mode r0 (one 16-B LDS per fibre) and everything slower is cached in
-// registers.  Reductions are deterministic: lane-local accumulation, one partial slot per
-// (group, v) pair, and a fixed-order fp64 second stage (reduce_partials).
+// VW elements).  Within a "run" only the fast reduced index i_{r0} changes, so
+//     M(i_1, fibre) = ws(i_1) · H_{0,r0}(i_1, i_{r0}) · sf(i_{r0})
+// with ws (every slower factor, per lane, registers), one 16-B H column chunk per fibre and
+// sf = Π_m H_{r0,m}(i_{r0}, i_m) precomputed per run into a per-group shared-memory vector
+// by the group's lanes.  Reductions are deterministic: lane-local accumulation, one partial
+// slot per (group, v) pair, and a fixed-order fp64 second stage (reduce_partials).
 #pragma once
 
 #include "common.cuh"
@@ -22,90 +24,95 @@
 namespace ifctn {
 
 template <typename T, int MODE, int CPL, bool SMEM>
-__global__ void __launch_bounds__(kPassThreads) fiber_pass(const __grid_constant__ PassParams<T> P) {
+__global__ void __launch_bounds__(kPassThreads, (CPL == 1 ? kPassMinBlocks : (CPL == 2 ? 2 : 1))) fiber_pass(const __grid_constant__ PassParams<T> P) {
     using VTr = VecT<T>;
     using V = typename VTr::V;
     constexpr int VW = VTr::W;
     constexpr int U = (CPL >= 4) ? 1 : (kUnroll / CPL);
+    constexpr bool kContract = (MODE == PASS_KEPT1 || MODE == PASS_RED1);
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const T* __restrict__ Hb = P.H;
+    size_t sm_off = 0;
     if constexpr (SMEM) {
         V* s = reinterpret_cast<V*>(smem_raw);
         const V* g = reinterpret_cast<const V*>(P.H);
         for (int64_t e = threadIdx.x; e < P.hsize / VW; e += blockDim.x) s[e] = g[e];
         __syncthreads();
         Hb = reinterpret_cast<const T*>(smem_raw);
+        sm_off = (size_t)P.hsize * sizeof(T);
     }
+    const int lanes = P.lanes;
+    const int lane = threadIdx.x & (lanes - 1);
+    const int gin = threadIdx.x >> P.lane_shift;  // group index inside the CTA
+    T* sfv = reinterpret_cast<T*>(smem_raw + sm_off) + (size_t)gin * P.sf_cap;
 
-    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t group = gt >> P.lane_shift;
-    const int lane = threadIdx.x & (P.lanes - 1);
+    const int group = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> P.lane_shift);
     if (group >= P.ngroups) return;
-    const unsigned gmask = (P.lanes == 32) ? 0xffffffffu
-                                           : (((1u << P.lanes) - 1u) << ((threadIdx.x & 31) & ~(P.lanes - 1)));
+    const unsigned gmask = (lanes == 32) ? 0xffffffffu
+                                         : (((1u << lanes) - 1u) << ((threadIdx.x & 31) & ~(lanes - 1)));
 
-    int chunk[CPL];
+    // lane → chunk offsets (clamped so every load is in bounds; invalid chunks weigh 0)
+    int cofs[CPL];
     bool cval[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-        chunk[c] = lane + c * P.lanes;
-        cval[c] = chunk[c] < P.nchunk;
+        const int ch = lane + c * lanes;
+        cval[c] = ch < P.nchunk;
+        cofs[c] = (cval[c] ? ch : P.nchunk - 1) * VW;
     }
 
-    const int64_t f0 = group * P.L;
-    const int64_t f1 = min(f0 + P.L, P.nfib);
+    // All fibre/index arithmetic is 32-bit (nfib < 2^31 is checked on the host); only
+    // element offsets into X are 64-bit.
+    const int f0 = group * (int)P.L;
+    const int f1 = min(f0 + (int)P.L, (int)P.nfib);
+    const int FR = (int)P.FR;
     const bool has_fast = P.nred > 0;
-    const int64_t fstep = has_fast ? P.fstride[P.rmode[0]] : 0;
+    const int fstep = has_fast ? (int)P.fstride[P.rmode[0]] : 0;
+    const int64_t xstep = (int64_t)fstep * P.I1p;      // elements between consecutive fibres
+    const int hstep = has_fast ? P.I1p : 0;            // H_{0,r0} column step (0: ones column)
+    const int rdim0 = has_fast ? (int)P.rdim[0] : 1;
 
-    // pass-level accumulators
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;  // REFILL: ‖ΔX‖², ‖X‖², ‖X_new − t‖²; OBJ: n2
 
-    int64_t pos = f0;
-    int64_t v = pos / P.FR;
-    int64_t r = pos - v * P.FR;
+    int pos = f0;
+    int v = pos / FR;
+    int r = pos - v * FR;
     while (pos < f1) {
-        const int64_t seg_end = min(f1, (v + 1) * P.FR);
-        int64_t kidx0 = 0, kidx1 = 0;
-        if (P.nkept >= 1) {
-            kidx0 = v % P.kdim[0];
-            kidx1 = v / P.kdim[0];
-        }
-        int64_t ridx[MAXN];
+        const int seg_end = min(f1, (v + 1) * FR);
+        int ridx[MAXN];
         {
-            int64_t rr = r;
+            int rr = r;
 #pragma unroll
             for (int j = 0; j < MAXN; ++j) {
                 ridx[j] = 0;
                 if (j < P.nred) {
-                    ridx[j] = rr % P.rdim[j];
-                    rr /= P.rdim[j];
+                    ridx[j] = rr % (int)P.rdim[j];
+                    rr /= (int)P.rdim[j];
                 }
             }
         }
-        // segment accumulators (one kept value v)
-        T sb[CPL][VW], sw[CPL][VW];
+        T sb[CPL][VW], sw[CPL][VW];  // segment accumulators (one kept value v)
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
 #pragma unroll
             for (int e = 0; e < VW; ++e) sb[c][e] = sw[c][e] = T(0);
 
-        int64_t remaining = seg_end - pos;
-        while (remaining > 0) {
-            const int64_t run = has_fast ? min(remaining, P.rdim[0] - ridx[0]) : 1;
+        while (pos < seg_end) {
+            const int run = has_fast ? min(seg_end - pos, rdim0 - ridx[0]) : 1;
             // ---- run setup (rare path): indices of every outer mode, slow factors --------
-            int64_t idx[MAXN];
+            int idx[MAXN];
 #pragma unroll
             for (int m = 0; m < MAXN; ++m) idx[m] = 0;
-            if (P.nkept >= 1) idx[P.kmode[0]] = kidx0;
-            if (P.nkept >= 2) idx[P.kmode[1]] = kidx1;
+            if (P.nkept >= 1) idx[P.kmode[0]] = v % (int)P.kdim[0];
+            if (P.nkept >= 2) idx[P.kmode[1]] = v / (int)P.kdim[0];
 #pragma unroll
             for (int j = 0; j < MAXN; ++j)
                 if (j < P.nred) idx[P.rmode[j]] = ridx[j];
-            int64_t fib = 0;
+            int fib = 0;
 #pragma unroll
             for (int m = 1; m < MAXN; ++m)
-                if (m <= P.nouter) fib += idx[m] * P.fstride[m];
+                if (m <= P.nouter) fib += idx[m] * (int)P.fstride[m];
 
             T ws[CPL][VW];
 #pragma unroll
@@ -113,95 +120,83 @@ __global__ void __launch_bounds__(kPassThreads) fiber_pass(const __grid_constant
 #pragma unroll
                 for (int e = 0; e < VW; ++e) ws[c][e] = T(1);
             for (int t = 0; t < P.nvs; ++t) {
-                const T* base = Hb + P.vs_off[t] + idx[P.vs_mode[t]] * P.I1p;
+                const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * P.I1p;
 #pragma unroll
                 for (int c = 0; c < CPL; ++c) {
-                    if (cval[c]) {
-                        T h[VW];
-                        VTr::get(*reinterpret_cast<const V*>(base + chunk[c] * VW), h);
+                    T h[VW];
+                    VTr::get(*reinterpret_cast<const V*>(base + cofs[c]), h);
 #pragma unroll
-                        for (int e = 0; e < VW; ++e) ws[c][e] *= h[e];
-                    }
+                    for (int e = 0; e < VW; ++e) ws[c][e] *= h[e];
                 }
             }
             T ss = T(1);
-            for (int t = 0; t < P.nss; ++t) ss *= Hb[P.ss_off[t] + idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
+            for (int t = 0; t < P.nss; ++t)
+                ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
 #pragma unroll
             for (int c = 0; c < CPL; ++c)
 #pragma unroll
                 for (int e = 0; e < VW; ++e) ws[c][e] = cval[c] ? ws[c][e] * ss : T(0);
-            int64_t sfo[MAXSF], sfi[MAXSF];
-#pragma unroll
-            for (int t = 0; t < MAXSF; ++t) {
-                sfo[t] = 0;
-                sfi[t] = 0;
-                if (t < P.nsf) {
-                    sfo[t] = P.sf_off[t] + idx[P.sf_fixmode[t]] * P.sf_fixmul[t];
-                    sfi[t] = P.sf_inc[t];
-                }
-            }
-            const T* vfb = Hb + (has_fast ? P.vf_off : 0);
-            const int64_t ri0 = ridx[0];
+            const int ri0 = ridx[0];
+            const T* hcol0 = Hb + (has_fast ? P.vf_off + (int64_t)ri0 * P.I1p : P.ones_off);
 
-            // ---- hot loop: `run` fibres with only the fast index i_{r0} changing ----------
-            // Phase 1 issues U·CPL independent 16-B loads of X (and mask words); phase 2
-            // rebuilds each entry's weight from cached slow factors × one fast H column.
+            // ---- the run, in sub-runs of ≤ sf_cap fibres --------------------------------
             T q0 = T(0), q1 = T(0), q2 = T(0);
-            for (int64_t t0 = 0; t0 < run; t0 += U) {
-                V xv[U][CPL];
-                uint32_t mb[U][CPL];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const bool uv = (t0 + u) < run;
-                    const int64_t fb = fib + (t0 + u) * fstep;
-#pragma unroll
-                    for (int c = 0; c < CPL; ++c) {
-                        const bool ok = uv && cval[c];
-                        const int64_t xo = fb * P.I1p + chunk[c] * VW;
-                        if constexpr (MODE == PASS_KEPT1 || MODE == PASS_RED1) {
-                            xv[u][c] = ok ? ld_stream(reinterpret_cast<const V*>(P.X + xo)) : zero_v<T>();
-                        } else if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
-                            xv[u][c] = ok ? *reinterpret_cast<const V*>(P.X + xo) : zero_v<T>();
-                        }
-                        if constexpr (MODE == PASS_REFILL) {
-                            mb[u][c] = ok ? (__ldg(P.mask + (xo >> 5)) >> (xo & 31)) : 0xffffffffu;
-                        }
-                    }
+            for (int sub = 0; sub < run; sub += P.sf_cap) {
+                const int len = min(run - sub, P.sf_cap);
+                __syncwarp(gmask);
+                for (int q = lane; q < len; q += lanes) {
+                    T f = T(1);
+                    for (int t = 0; t < P.nsf; ++t)
+                        f *= Hb[P.sf_off[t] + (int64_t)idx[P.sf_fixmode[t]] * P.sf_fixmul[t] +
+                                (int64_t)(ri0 + sub + q) * P.sf_inc[t]];
+                    sfv[q] = f;
                 }
+                __syncwarp(gmask);
+                const int64_t ebase = (int64_t)(fib + sub * fstep) * P.I1p;
+                const T* xp = P.X + ebase;
+                T* xw = P.Xw + ebase;
+                const T* hp = hcol0 + sub * hstep;
+
+                auto body = [&](auto uu, int q) {
+                    constexpr int UU = decltype(uu)::value;
+                    V xv[UU][CPL];
+                    uint32_t mb[UU][CPL];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const bool uv = (t0 + u) < run;
-                    const int64_t ri = ri0 + t0 + u;
-                    const int64_t fb = fib + (t0 + u) * fstep;
-                    T sf = T(1);
-                    if (has_fast) {
+                    for (int u = 0; u < UU; ++u) {
 #pragma unroll
-                        for (int t = 0; t < MAXSF; ++t)
-                            if (t < P.nsf) sf *= Hb[sfo[t] + ri * sfi[t]];
+                        for (int c = 0; c < CPL; ++c) {
+                            const int64_t eo = (int64_t)(q + u) * xstep + cofs[c];
+                            if constexpr (kContract) xv[u][c] = ld_stream(reinterpret_cast<const V*>(xp + eo));
+                            else if constexpr (MODE != PASS_MODEL) xv[u][c] = *reinterpret_cast<const V*>(xp + eo);
+                            if constexpr (MODE == PASS_REFILL) {
+                                const int64_t ge = ebase + eo;
+                                mb[u][c] = __ldg(P.mask + (ge >> 5)) >> (ge & 31);
+                            }
+                        }
                     }
 #pragma unroll
-                    for (int c = 0; c < CPL; ++c) {
-                        const bool ok = uv && cval[c];
-                        T hf[VW];
-                        if (has_fast) {
-                            VTr::get(*reinterpret_cast<const V*>(vfb + ri * P.I1p + chunk[c] * VW), hf);
-                        } else {
+                    for (int u = 0; u < UU; ++u) {
+                        const T sf = sfv[q + u];
+                        const T* hq = hp + (q + u) * hstep;
 #pragma unroll
-                            for (int e = 0; e < VW; ++e) hf[e] = T(1);
-                        }
-                        T w[VW], x[VW];
+                        for (int c = 0; c < CPL; ++c) {
+                            T hf[VW], w[VW];
+                            VTr::get(*reinterpret_cast<const V*>(hq + cofs[c]), hf);
 #pragma unroll
-                        for (int e = 0; e < VW; ++e) w[e] = ok ? ws[c][e] * (hf[e] * sf) : T(0);
-                        if constexpr (MODE != PASS_MODEL) VTr::get(xv[u][c], x);
-                        if constexpr (MODE == PASS_KEPT1 || MODE == PASS_RED1) {
+                            for (int e = 0; e < VW; ++e) w[e] = ws[c][e] * (hf[e] * sf);
+                            if constexpr (kContract) {
+                                T x[VW];
+                                VTr::get(xv[u][c], x);
 #pragma unroll
-                            for (int e = 0; e < VW; ++e) {
-                                sb[c][e] = fma(w[e], x[e], sb[c][e]);
-                                sw[c][e] = fma(w[e], w[e], sw[c][e]);
-                            }
-                        } else if constexpr (MODE == PASS_REFILL) {
-                            if (ok) {
-                                T xn[VW];
+                                for (int e = 0; e < VW; ++e) {
+                                    sb[c][e] = fma(w[e], x[e], sb[c][e]);
+                                    sw[c][e] = fma(w[e], w[e], sw[c][e]);
+                                }
+                            } else if constexpr (MODE == PASS_REFILL) {
+                                T x[VW], xn[VW];
+                                VTr::get(xv[u][c], x);
+#pragma unroll
+                                for (int e = 0; e < VW; ++e) x[e] = cval[c] ? x[e] : T(0);  // clamped lane
 #pragma unroll
                                 for (int e = 0; e < VW; ++e) {
                                     const bool obs = (mb[u][c] >> e) & 1u;
@@ -212,38 +207,44 @@ __global__ void __launch_bounds__(kPassThreads) fiber_pass(const __grid_constant
                                     q1 = fma(x[e], x[e], q1);
                                     q2 = fma(g, g, q2);
                                 }
-                                *reinterpret_cast<V*>(P.Xw + fb * P.I1p + chunk[c] * VW) = VTr::make(xn);
-                            }
-                        } else if constexpr (MODE == PASS_OBJ) {
-#pragma unroll
-                            for (int e = 0; e < VW; ++e) {
-                                const T g = x[e] - w[e];
-                                q2 = fma(g, g, q2);
-                            }
-                        } else {  // PASS_MODEL
-                            if (ok) {
+                                if (cval[c])
+                                    *reinterpret_cast<V*>(xw + (int64_t)(q + u) * xstep + cofs[c]) = VTr::make(xn);
+                            } else if constexpr (MODE == PASS_OBJ) {
+                                T x[VW];
+                                VTr::get(xv[u][c], x);
 #pragma unroll
                                 for (int e = 0; e < VW; ++e) {
-                                    const int i1 = chunk[c] * VW + e;
-                                    if (i1 < P.I1) P.out[fb * P.I1 + i1] = w[e];
+                                    const T g = (cval[c] ? x[e] : T(0)) - w[e];
+                                    q2 = fma(g, g, q2);
+                                }
+                            } else {  // PASS_MODEL: dense user layout, scalar stores
+                                if (cval[c]) {
+                                    const int64_t fb = (ebase + (int64_t)(q + u) * xstep) / P.I1p;
+#pragma unroll
+                                    for (int e = 0; e < VW; ++e) {
+                                        const int i1 = cofs[c] + e;
+                                        if (i1 < P.I1) P.out[fb * P.I1 + i1] = w[e];
+                                    }
                                 }
                             }
                         }
                     }
-                }
+                };
+                int q = 0;
+                for (; q + U <= len; q += U) body(std::integral_constant<int, U>{}, q);
+                for (; q < len; ++q) body(std::integral_constant<int, 1>{}, q);
             }
             if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
                 n0 += (double)q0;
                 n1 += (double)q1;
                 n2 += (double)q2;
             }
-            remaining -= run;
             pos += run;
             if (has_fast) {  // odometer advance by `run`
                 ridx[0] += run;
 #pragma unroll
                 for (int j = 0; j < MAXN - 1; ++j) {
-                    if (j + 1 < P.nred && ridx[j] >= P.rdim[j]) {
+                    if (j + 1 < P.nred && ridx[j] >= (int)P.rdim[j]) {
                         ridx[j] = 0;
                         ridx[j + 1] += 1;
                     }
@@ -252,11 +253,11 @@ __global__ void __launch_bounds__(kPassThreads) fiber_pass(const __grid_constant
         }
         // ---- flush the segment's partials into slot group + v ---------------------------
         if constexpr (MODE == PASS_KEPT1) {
-            const int64_t slot = group + v;
+            const int64_t slot = (int64_t)group + v;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 if (cval[c]) {
-                    const int64_t o = slot * P.Lv + chunk[c] * VW;
+                    const int64_t o = slot * P.Lv + cofs[c];
                     *reinterpret_cast<V*>(P.part_b + o) = VTr::make(sb[c]);
                     *reinterpret_cast<V*>(P.part_w + o) = VTr::make(sw[c]);
                 }
@@ -270,12 +271,12 @@ __global__ void __launch_bounds__(kPassThreads) fiber_pass(const __grid_constant
                     tb += sb[c][e];
                     tw += sw[c][e];
                 }
-            for (int off = P.lanes >> 1; off > 0; off >>= 1) {
+            for (int off = lanes >> 1; off > 0; off >>= 1) {
                 tb += __shfl_xor_sync(gmask, tb, off);
                 tw += __shfl_xor_sync(gmask, tw, off);
             }
             if (lane == 0) {
-                const int64_t slot = group + v;
+                const int64_t slot = (int64_t)group + v;
                 P.part_b[slot] = tb;
                 P.part_w[slot] = tw;
             }
@@ -284,15 +285,15 @@ __global__ void __launch_bounds__(kPassThreads) fiber_pass(const __grid_constant
         r = 0;
     }
     if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
-        for (int off = P.lanes >> 1; off > 0; off >>= 1) {
+        for (int off = lanes >> 1; off > 0; off >>= 1) {
             n0 += __shfl_xor_sync(gmask, n0, off);
             n1 += __shfl_xor_sync(gmask, n1, off);
             n2 += __shfl_xor_sync(gmask, n2, off);
         }
         if (lane == 0) {
-            P.norms[group * 3 + 0] = n0;
-            P.norms[group * 3 + 1] = n1;
-            P.norms[group * 3 + 2] = n2;
+            P.norms[(int64_t)group * 3 + 0] = n0;
+            P.norms[(int64_t)group * 3 + 1] = n1;
+            P.norms[(int64_t)group * 3 + 2] = n2;
         }
     }
 }

@@ -72,7 +72,7 @@ struct Shape {
     int64_t gtotal = 0;
     int64_t hoff[MAXN][MAXN] = {};  // p<q
     int64_t hld[MAXN] = {};
-    int64_t htotal = 0;
+    int64_t htotal = 0, ones_off = 0;
     int nchunk = 0, lanes = 0, lane_shift = 0, cpl = 0;
     int64_t part_elems = 0, max_bw = 0, ndelta = 0, groups_bound = 0;
     int64_t delta_off[MAXN][MAXN] = {};
@@ -144,6 +144,7 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
     s.I1p = align_up(s.I1, s.vw);
     s.nfib = 1;
     for (int m = 1; m < order; ++m) s.nfib *= s.ld[m];
+    if (s.nfib >= (1LL << 31)) fail(IFCTN_E_UNSUPPORTED, "more than 2^31 mode-1 fibres per shard");
     s.npad = s.nfib * s.I1p;
     s.nloc = s.nfib * s.I1;
     s.nglob = (int64_t)prodd;
@@ -170,7 +171,9 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
             s.hoff[p][q] = off;
             off += align_up(s.hld[p] * s.ld[q], s.vw);
         }
-    s.htotal = std::max<int64_t>(off, s.vw);
+    s.ones_off = off;  // a column of I1p ones (see PassParams::ones_off)
+    off += s.I1p;
+    s.htotal = off;
     // lane mapping
     s.nchunk = (int)(s.I1p / s.vw);
     s.lanes = std::min(32, pow2ceil(s.nchunk));
@@ -478,8 +481,11 @@ struct Solver : SolverBase {
                     ++p.nss;
                 }
             }
+        p.ones_off = s.ones_off;
+        const int gpc = kPassThreads / s.lanes;  // groups per CTA
+        p.sf_cap = std::max<int>(8, (int)((16384 / s.esize) / gpc));
         // grid: one wave of groups, equal fibre counts
-        const size_t smem = use_smem ? (size_t)(s.htotal * s.esize) : 0;
+        const size_t smem = (use_smem ? (size_t)(s.htotal * s.esize) : 0) + (size_t)gpc * p.sf_cap * s.esize;
         pp.fn = pick_pass_mode<T>(mode, s.cpl, use_smem);
         if (smem > 48 * 1024) CU(cudaFuncSetAttribute(pp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int nb = 0;
@@ -643,6 +649,11 @@ struct Solver : SolverBase {
                            is_device_ptr(G0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
         if (tmp_o) CU(cudaFreeAsync(tmp_o, st));
         if (tmp_m) CU(cudaFreeAsync(tmp_m, st));
+        {
+            std::vector<T> ones((size_t)s.I1p, T(1));
+            CU(cudaMemcpyAsync(H + s.ones_off, ones.data(), ones.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+            CU(cudaStreamSynchronize(st));
+        }
         plan();
         build_all_H();
         CU(cudaStreamSynchronize(st));
