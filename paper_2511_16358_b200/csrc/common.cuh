@@ -13,8 +13,22 @@ constexpr int MAXP = MAXN * (MAXN - 1) / 2;    // pairs p<q
 constexpr int MAXSF = MAXN - 2;                // pairs involving the fast mode r0 (outer)
 constexpr int MAXR = 8;                        // IFCTN_MAX_RANK
 constexpr int kPassThreads = 256;              // fiber-pass CTA size
-constexpr int kUnroll = 4;                     // fibers in flight per lane
-constexpr int kPassMinBlocks = 3;              // ≤ 85 registers: ≥ 24 warps per SM
+constexpr int kPassMinBlocks = 2;              // ≤ 128 registers: ≥ 16 warps per SM
+
+// Compile-time shape of one fibre-pass instance (fiber_pass.cuh): EPL mode-1 positions per
+// lane, LPF lanes per fibre (FP = 32/LPF fibres per warp step), ring rows per fibre (X and,
+// without a resident H block, the H column), F fibres per TMA stage (≈ 2 KB), D stages.
+template <typename T, int EPL, int LPF, bool HRES, bool LOADX>
+struct PassCfg {
+    static constexpr int FP = 32 / LPF;
+    static constexpr int SR = LPF * EPL;  // shared-memory row stride (elements)
+    static constexpr int NROW = (LOADX ? 1 : 0) + (HRES ? 0 : 1);
+    static constexpr int ROWB = SR * (int)sizeof(T);
+    static constexpr int FK = (2048 / (NROW > 0 ? NROW : 1) / ROWB) / FP;
+    static constexpr int F = FP * (FK > 1 ? FK : 1);
+    static constexpr int D = 4;
+    static constexpr int RING = D * NROW * F * SR;  // ring elements per warp
+};
 
 enum PassMode : int {
     PASS_KEPT1 = 0,   // a2, mode 1 (code mode 0) is one of the kept modes {k,i}
@@ -60,6 +74,69 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
     return r;
 }
 
+// ---- TMA bulk copies + mbarriers (sm_90+ PTX; UBLKCP / SYNCS in sm_100a SASS) -------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// global → shared bulk copy (TMA engine), completion counted on `bar` in bytes
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Blocking wait for phase `parity` of `bar`; the suspend-time hint lets the hardware park the
+// warp until the phase completes instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!done);
+}
+
+// 32-bit shared-address variants (no generic→shared conversion in the hot loop)
+__device__ __forceinline__ void mbar_arrive_expect_tx_a(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_g2s_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!done);
+}
+
 // One fiber pass = one streaming sweep over the (local) X in fibre order.  A "fibre" is a
 // mode-1 line X(:, i_2, …, i_N) stored contiguously with I1p ≥ I1 padded entries (pad = 0).
 // Fibres are enumerated as pos = v·FR + r, v over the kept outer modes, r over the reduced
@@ -76,7 +153,7 @@ struct PassParams {
     double* norms;       // PASS_REFILL/OBJ: 3 doubles per group
     T* out;              // PASS_MODEL: dense user layout
     T rho, inv1p;        // ρ and 1/(1+ρ)
-    int I1, I1p, nchunk, lanes, lane_shift;
+    int I1, I1p;
     int64_t nfib, L, ngroups, NV, FR, Lv;
     int nkept;
     int kmode[2];
@@ -101,7 +178,9 @@ struct PassParams {
     int64_t sf_fixmul[MAXSF];
     int64_t sf_inc[MAXSF];
     int64_t ones_off;        // a column of I1p ones in H (the "fast factor" when nred == 0)
-    int sf_cap;              // per-group shared-memory slots for the fast scalar factors
+    int sf_cap;              // per-warp shared-memory slots for the fast scalar factors
+    int64_t sfv_off, hres_off, stage_off;  // byte offsets in dynamic shared memory
+    int64_t hres_src, hres_elems;          // resident H block (HRES): offset in H, elements
 };
 
 template <typename T>

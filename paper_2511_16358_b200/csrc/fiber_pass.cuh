@@ -9,286 +9,431 @@
 // and Eq. 9 needs t(i) = Π_{p<q} H_{p,q}(i_p,i_q) per entry.  Z_k is never
 // materialised: the weight of an entry is rebuilt from the (small, cache-resident) H.
 //
-// B200 mapping: one pass streams X once with 16-B loads; a "group" of
-// `lanes` threads owns whole mode-1 fibres, each lane fixed mode-1 positions (CPL chunks of
-// VW elements).  Within a "run" only the fast reduced index i_{r0} changes, so
+// B200 mapping.  One warp owns a contiguous range of mode-1 fibres
+// (a fibre = the I1p-padded line X(:, i_2..i_N)), walked as "runs" in which only the fast
+// reduced index i_{r0} changes, so
 //     M(i_1, fibre) = ws(i_1) · H_{0,r0}(i_1, i_{r0}) · sf(i_{r0})
-// with ws (every slower factor, per lane, registers), one 16-B H column chunk per fibre and
-// sf = Π_m H_{r0,m}(i_{r0}, i_m) precomputed per run into a per-group shared-memory vector
-// by the group's lanes.  Reductions are deterministic: lane-local accumulation, one partial
-// slot per (group, v) pair, and a fixed-order fp64 second stage (reduce_partials).
+// with ws (all slower factors, registers), the H_{0,r0} column of the fibre (resident in
+// shared memory for the whole pass when it fits: HRES) and sf = Π_m H_{r0,m}(i_{r0}, i_m),
+// precomputed per run into a per-warp shared-memory vector.  The warp works on FP = 32/LPF
+// fibres per step: lane l serves step fibre l/LPF at mode-1 positions [(l mod LPF)·EPL, +EPL)
+// (16-B shared-memory vectors; fp32 math in packed FMUL2/FFMA2 pairs).
+// Data movement is a TMA pipeline that runs ahead across run and segment boundaries: lane 0
+// (the producer, with its own copy of the fibre walker) issues cp.async.bulk copies of F
+// fibres of X (and their H columns when !HRES) per stage into a D-stage shared-memory ring
+// guarded by mbarriers; all 32 lanes consume.  Reductions are deterministic: lane-local
+// accumulation, one partial slot per (warp, v) pair, and a fixed-order fp64 second stage
+// (reduce_partials).
 #pragma once
 
 #include "common.cuh"
 
 namespace ifctn {
 
-template <typename T, int MODE, int CPL, bool SMEM>
-__global__ void __launch_bounds__(kPassThreads, (CPL == 1 ? kPassMinBlocks : (CPL == 2 ? 2 : 1))) fiber_pass(const __grid_constant__ PassParams<T> P) {
-    using VTr = VecT<T>;
-    using V = typename VTr::V;
-    constexpr int VW = VTr::W;
-    constexpr int U = (CPL >= 4) ? 1 : (kUnroll / CPL);
-    constexpr bool kContract = (MODE == PASS_KEPT1 || MODE == PASS_RED1);
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const T* __restrict__ Hb = P.H;
-    size_t sm_off = 0;
-    if constexpr (SMEM) {
-        V* s = reinterpret_cast<V*>(smem_raw);
-        const V* g = reinterpret_cast<const V*>(P.H);
-        for (int64_t e = threadIdx.x; e < P.hsize / VW; e += blockDim.x) s[e] = g[e];
-        __syncthreads();
-        Hb = reinterpret_cast<const T*>(smem_raw);
-        sm_off = (size_t)P.hsize * sizeof(T);
-    }
-    const int lanes = P.lanes;
-    const int lane = threadIdx.x & (lanes - 1);
-    const int gin = threadIdx.x >> P.lane_shift;  // group index inside the CTA
-    T* sfv = reinterpret_cast<T*>(smem_raw + sm_off) + (size_t)gin * P.sf_cap;
-
-    const int group = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> P.lane_shift);
-    if (group >= P.ngroups) return;
-    const unsigned gmask = (lanes == 32) ? 0xffffffffu
-                                         : (((1u << lanes) - 1u) << ((threadIdx.x & 31) & ~(lanes - 1)));
-
-    // lane → chunk offsets (clamped so every load is in bounds; invalid chunks weigh 0)
-    int cofs[CPL];
-    bool cval[CPL];
+template <typename T, int N>
+__device__ __forceinline__ void lds_vec(const T* p, T (&o)[N]) {
+    static_assert(N * sizeof(T) % 16 == 0, "16-B vectors only");
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-        const int ch = lane + c * lanes;
-        cval[c] = ch < P.nchunk;
-        cofs[c] = (cval[c] ? ch : P.nchunk - 1) * VW;
+    for (int v = 0; v < N * (int)sizeof(T) / 16; ++v) {
+        const float4 q = reinterpret_cast<const float4*>(p)[v];
+        const T* t = reinterpret_cast<const T*>(&q);
+#pragma unroll
+        for (int e = 0; e < 16 / (int)sizeof(T); ++e) o[v * (16 / sizeof(T)) + e] = t[e];
     }
+}
 
-    // All fibre/index arithmetic is 32-bit (nfib < 2^31 is checked on the host); only
-    // element offsets into X are 64-bit.
+template <typename T, int N>
+__device__ __forceinline__ void stg_vec(T* p, const T (&o)[N]) {
+    static_assert(N * sizeof(T) % 16 == 0, "16-B vectors only");
+#pragma unroll
+    for (int v = 0; v < N * (int)sizeof(T) / 16; ++v) {
+        float4 q;
+        T* t = reinterpret_cast<T*>(&q);
+#pragma unroll
+        for (int e = 0; e < 16 / (int)sizeof(T); ++e) t[e] = o[v * (16 / sizeof(T)) + e];
+        reinterpret_cast<float4*>(p)[v] = q;
+    }
+}
+
+// w = ws ⊙ h · sf   (fp32: packed FMUL2 pairs)
+template <typename T, int N>
+__device__ __forceinline__ void weight(const T (&ws)[N], const T (&h)[N], T sf, T (&w)[N]) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+        const float2 s2 = make_float2(sf, sf);
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 hs = __fmul2_rn(make_float2(h[e], h[e + 1]), s2);
+            const float2 r = __fmul2_rn(make_float2(ws[e], ws[e + 1]), hs);
+            w[e] = r.x;
+            w[e + 1] = r.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) w[e] = ws[e] * (h[e] * sf);
+    }
+}
+
+// sb += w ⊙ x, sw += w ⊙ w   (fp32: packed FFMA2 pairs)
+template <typename T, int N>
+__device__ __forceinline__ void accumulate(const T (&w)[N], const T (&x)[N], T (&sb)[N], T (&sw)[N]) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 w2 = make_float2(w[e], w[e + 1]);
+            const float2 b = __ffma2_rn(w2, make_float2(x[e], x[e + 1]), make_float2(sb[e], sb[e + 1]));
+            const float2 q = __ffma2_rn(w2, w2, make_float2(sw[e], sw[e + 1]));
+            sb[e] = b.x;
+            sb[e + 1] = b.y;
+            sw[e] = q.x;
+            sw[e + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            sb[e] = fma(w[e], x[e], sb[e]);
+            sw[e] = fma(w[e], w[e], sw[e]);
+        }
+    }
+}
+
+// Fibre walker: positions pos = v·FR + r of one warp's range, cut into runs (consecutive
+// fibres differing only in i_{r0}, at most sf_cap long).  32-bit index arithmetic
+// (nfib < 2^31 is checked on the host).
+struct Walker {
+    int pos, f1, v, seg_end;
+    int ridx[MAXN];
+    int run_len, fib, ri0;
+    bool new_seg, seg_last;
+};
+
+template <typename T>
+__device__ __forceinline__ void walker_init(Walker& w, const PassParams<T>& P, int f0, int f1) {
+    const int FR = (int)P.FR;
+    w.pos = f0;
+    w.f1 = f1;
+    w.v = f0 / FR;
+    int rr = f0 - w.v * FR;
+#pragma unroll
+    for (int j = 0; j < MAXN; ++j) {
+        w.ridx[j] = 0;
+        if (j < P.nred) {
+            w.ridx[j] = rr % (int)P.rdim[j];
+            rr /= (int)P.rdim[j];
+        }
+    }
+    w.seg_end = min(f1, (w.v + 1) * FR);
+    w.run_len = 0;
+    w.fib = 0;
+    w.ri0 = 0;
+    w.new_seg = true;
+    w.seg_last = false;
+}
+
+// Move past the current run and describe the next one; false when the range is exhausted.
+template <typename T>
+__device__ __forceinline__ bool walker_next(Walker& w, const PassParams<T>& P) {
+    const bool has_fast = P.nred > 0;
+    if (w.run_len > 0) {
+        w.pos += w.run_len;
+        if (w.pos >= w.seg_end) {
+            w.v += 1;
+#pragma unroll
+            for (int j = 0; j < MAXN; ++j) w.ridx[j] = 0;
+            w.seg_end = min(w.f1, (w.v + 1) * (int)P.FR);
+            w.new_seg = true;
+        } else {
+            w.new_seg = false;
+            w.ridx[0] += w.run_len;
+#pragma unroll
+            for (int j = 0; j < MAXN - 1; ++j) {
+                if (j + 1 < P.nred && w.ridx[j] >= (int)P.rdim[j]) {
+                    w.ridx[j] = 0;
+                    w.ridx[j + 1] += 1;
+                }
+            }
+        }
+    }
+    if (w.pos >= w.f1) return false;
+    w.run_len = has_fast ? min(min(w.seg_end - w.pos, (int)P.rdim[0] - w.ridx[0]), P.sf_cap) : 1;
+    w.seg_last = w.pos + w.run_len >= w.seg_end;
+    int fib = 0;
+    if (P.nkept >= 1) fib += (w.v % (int)P.kdim[0]) * (int)P.fstride[P.kmode[0]];
+    if (P.nkept >= 2) fib += (w.v / (int)P.kdim[0]) * (int)P.fstride[P.kmode[1]];
+#pragma unroll
+    for (int j = 0; j < MAXN; ++j)
+        if (j < P.nred) fib += w.ridx[j] * (int)P.fstride[P.rmode[j]];
+    w.fib = fib;
+    w.ri0 = w.ridx[0];
+    return true;
+}
+
+template <typename T, int MODE, int EPL, int LPF, bool HRES>
+__global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
+    constexpr bool kContract = (MODE == PASS_KEPT1 || MODE == PASS_RED1);
+    constexpr bool kLoadX = (MODE != PASS_MODEL);
+    using Cfg = PassCfg<T, EPL, LPF, HRES, kLoadX>;
+    constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR, NROW = Cfg::NROW;
+    constexpr int STAGE = NROW * F * SR;  // elements per ring stage
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int fsub = lane / LPF;                 // fibre of the step served by this lane
+    const int eb = (lane % LPF) * EPL;           // first mode-1 position of this lane
+    const int I1p = P.I1p;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * D;
+    T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sf_cap;
+    T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);
+    T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
+
+    // CTA setup: the resident H_{0,r0} block (HRES), then per warp: zero the ring (row
+    // tails past I1p must read as 0), init the stage barriers.
+    if constexpr (HRES) {
+        const float4* src = reinterpret_cast<const float4*>(P.H + P.hres_src);
+        float4* dst = reinterpret_cast<float4*>(hres);
+        for (int e = threadIdx.x; e < (int)(P.hres_elems * sizeof(T) / 16); e += blockDim.x) dst[e] = src[e];
+    }
+    for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
+    if (lane == 0)
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    const int group = blockIdx.x * nwarps + warp;
+    if (group >= P.ngroups) return;
+
+    const uint32_t bar0 = smem_u32(bars);
+    const uint32_t stg0 = smem_u32(stg);
+    const T* __restrict__ Hb = P.H;
+    bool ev[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) ev[e] = eb + e < I1p;
+    const bool lane_full = eb + EPL <= I1p;
+    const int ebc = eb < I1p ? eb : 0;               // clamped (HRES reads stay in bounds)
+
     const int f0 = group * (int)P.L;
     const int f1 = min(f0 + (int)P.L, (int)P.nfib);
-    const int FR = (int)P.FR;
     const bool has_fast = P.nred > 0;
     const int fstep = has_fast ? (int)P.fstride[P.rmode[0]] : 0;
-    const int64_t xstep = (int64_t)fstep * P.I1p;      // elements between consecutive fibres
-    const int hstep = has_fast ? P.I1p : 0;            // H_{0,r0} column step (0: ones column)
-    const int rdim0 = has_fast ? (int)P.rdim[0] : 1;
+    const int64_t xstep = (int64_t)fstep * I1p;      // elements between consecutive fibres
+    const int hstep = has_fast ? I1p : 0;            // H_{0,r0} column step (0: ones column)
+    const uint32_t rowbytes = (uint32_t)(I1p * sizeof(T));
+    const bool xmerge = (SR == I1p) && (fstep == 1);  // F fibres = one contiguous copy
+    const bool hmerge = (SR == I1p) && has_fast;
 
+    // ---- producer (lane 0): its own walker, D stages ahead of the consumers --------------
+    Walker Pw;
+    walker_init(Pw, P, f0, f1);
+    int p_left = 0;          // fibres of the producer's current run not yet issued
+    uint32_t p_n = 0;        // next stage sequence number
+    const T* p_x = P.X;      // next X fibre of the producer's run
+    const T* p_h = Hb;       // next H column of the producer's run (!HRES)
+    auto produce = [&]() {
+        if (p_left == 0) {
+            if (!walker_next(Pw, P)) return;
+            p_left = Pw.run_len;
+            p_x = P.X + (int64_t)Pw.fib * I1p;
+            p_h = Hb + (has_fast ? P.vf_off + (int64_t)Pw.ri0 * I1p : P.ones_off);
+        }
+        const int nf = min(F, p_left);
+        const int s = (int)(p_n & (uint32_t)(D - 1));
+        const uint32_t bar = bar0 + 8u * (uint32_t)s;
+        const uint32_t sx = stg0 + (uint32_t)(s * STAGE * (int)sizeof(T));
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx_a(bar, (uint32_t)nf * rowbytes * (uint32_t)NROW);
+        if constexpr (kLoadX) {
+            if (xmerge) {
+                tma_g2s_a(sx, p_x, (uint32_t)nf * rowbytes, bar);
+            } else {
+                for (int f = 0; f < nf; ++f)
+                    tma_g2s_a(sx + (uint32_t)(f * SR * (int)sizeof(T)), p_x + (int64_t)f * xstep, rowbytes, bar);
+            }
+            p_x += (int64_t)nf * xstep;
+        }
+        if constexpr (!HRES) {
+            const uint32_t sh = sx + (uint32_t)((kLoadX ? F * SR : 0) * (int)sizeof(T));
+            if (hmerge) {
+                tma_g2s_a(sh, p_h, (uint32_t)nf * rowbytes, bar);
+            } else {
+                for (int f = 0; f < nf; ++f)
+                    tma_g2s_a(sh + (uint32_t)(f * SR * (int)sizeof(T)), p_h + (int64_t)f * hstep, rowbytes, bar);
+            }
+            p_h += (int64_t)nf * hstep;
+        }
+        p_left -= nf;
+        ++p_n;
+    };
+    if (lane == 0)
+        for (int d = 0; d < D; ++d) produce();
+
+    // ---- consumers (all lanes) ---------------------------------------------------------
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;  // REFILL: ‖ΔX‖², ‖X‖², ‖X_new − t‖²; OBJ: n2
-
-    int pos = f0;
-    int v = pos / FR;
-    int r = pos - v * FR;
-    while (pos < f1) {
-        const int seg_end = min(f1, (v + 1) * FR);
-        int ridx[MAXN];
-        {
-            int rr = r;
+    T sb[EPL], sw[EPL];                     // segment accumulators (one kept value v)
+    uint32_t cn = 0;                        // next stage to consume
+    Walker C;
+    walker_init(C, P, f0, f1);
+    while (walker_next(C, P)) {
+        if (C.new_seg) {
 #pragma unroll
-            for (int j = 0; j < MAXN; ++j) {
-                ridx[j] = 0;
-                if (j < P.nred) {
-                    ridx[j] = rr % (int)P.rdim[j];
-                    rr /= (int)P.rdim[j];
-                }
-            }
+            for (int e = 0; e < EPL; ++e) sb[e] = sw[e] = T(0);
         }
-        T sb[CPL][VW], sw[CPL][VW];  // segment accumulators (one kept value v)
+        // run setup (rare path): indices of every outer mode, slow factors, sf vector
+        int idx[MAXN];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
+        for (int m = 0; m < MAXN; ++m) idx[m] = 0;
+        if (P.nkept >= 1) idx[P.kmode[0]] = C.v % (int)P.kdim[0];
+        if (P.nkept >= 2) idx[P.kmode[1]] = C.v / (int)P.kdim[0];
 #pragma unroll
-            for (int e = 0; e < VW; ++e) sb[c][e] = sw[c][e] = T(0);
-
-        while (pos < seg_end) {
-            const int run = has_fast ? min(seg_end - pos, rdim0 - ridx[0]) : 1;
-            // ---- run setup (rare path): indices of every outer mode, slow factors --------
-            int idx[MAXN];
+        for (int j = 0; j < MAXN; ++j)
+            if (j < P.nred) idx[P.rmode[j]] = C.ridx[j];
+        T ws[EPL];
 #pragma unroll
-            for (int m = 0; m < MAXN; ++m) idx[m] = 0;
-            if (P.nkept >= 1) idx[P.kmode[0]] = v % (int)P.kdim[0];
-            if (P.nkept >= 2) idx[P.kmode[1]] = v / (int)P.kdim[0];
+        for (int e = 0; e < EPL; ++e) ws[e] = ev[e] ? T(1) : T(0);
+        for (int t = 0; t < P.nvs; ++t) {
+            const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * I1p + eb;
 #pragma unroll
-            for (int j = 0; j < MAXN; ++j)
-                if (j < P.nred) idx[P.rmode[j]] = ridx[j];
-            int fib = 0;
-#pragma unroll
-            for (int m = 1; m < MAXN; ++m)
-                if (m <= P.nouter) fib += idx[m] * (int)P.fstride[m];
-
-            T ws[CPL][VW];
-#pragma unroll
-            for (int c = 0; c < CPL; ++c)
-#pragma unroll
-                for (int e = 0; e < VW; ++e) ws[c][e] = T(1);
-            for (int t = 0; t < P.nvs; ++t) {
-                const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * P.I1p;
-#pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    T h[VW];
-                    VTr::get(*reinterpret_cast<const V*>(base + cofs[c]), h);
-#pragma unroll
-                    for (int e = 0; e < VW; ++e) ws[c][e] *= h[e];
-                }
-            }
-            T ss = T(1);
-            for (int t = 0; t < P.nss; ++t)
-                ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
-#pragma unroll
-            for (int c = 0; c < CPL; ++c)
-#pragma unroll
-                for (int e = 0; e < VW; ++e) ws[c][e] = cval[c] ? ws[c][e] * ss : T(0);
-            const int ri0 = ridx[0];
-            const T* hcol0 = Hb + (has_fast ? P.vf_off + (int64_t)ri0 * P.I1p : P.ones_off);
-
-            // ---- the run, in sub-runs of ≤ sf_cap fibres --------------------------------
-            T q0 = T(0), q1 = T(0), q2 = T(0);
-            for (int sub = 0; sub < run; sub += P.sf_cap) {
-                const int len = min(run - sub, P.sf_cap);
-                __syncwarp(gmask);
-                for (int q = lane; q < len; q += lanes) {
-                    T f = T(1);
-                    for (int t = 0; t < P.nsf; ++t)
-                        f *= Hb[P.sf_off[t] + (int64_t)idx[P.sf_fixmode[t]] * P.sf_fixmul[t] +
-                                (int64_t)(ri0 + sub + q) * P.sf_inc[t]];
-                    sfv[q] = f;
-                }
-                __syncwarp(gmask);
-                const int64_t ebase = (int64_t)(fib + sub * fstep) * P.I1p;
-                const T* xp = P.X + ebase;
-                T* xw = P.Xw + ebase;
-                const T* hp = hcol0 + sub * hstep;
-
-                auto body = [&](auto uu, int q) {
-                    constexpr int UU = decltype(uu)::value;
-                    V xv[UU][CPL];
-                    uint32_t mb[UU][CPL];
-#pragma unroll
-                    for (int u = 0; u < UU; ++u) {
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) {
-                            const int64_t eo = (int64_t)(q + u) * xstep + cofs[c];
-                            if constexpr (kContract) xv[u][c] = ld_stream(reinterpret_cast<const V*>(xp + eo));
-                            else if constexpr (MODE != PASS_MODEL) xv[u][c] = *reinterpret_cast<const V*>(xp + eo);
-                            if constexpr (MODE == PASS_REFILL) {
-                                const int64_t ge = ebase + eo;
-                                mb[u][c] = __ldg(P.mask + (ge >> 5)) >> (ge & 31);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < UU; ++u) {
-                        const T sf = sfv[q + u];
-                        const T* hq = hp + (q + u) * hstep;
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) {
-                            T hf[VW], w[VW];
-                            VTr::get(*reinterpret_cast<const V*>(hq + cofs[c]), hf);
-#pragma unroll
-                            for (int e = 0; e < VW; ++e) w[e] = ws[c][e] * (hf[e] * sf);
-                            if constexpr (kContract) {
-                                T x[VW];
-                                VTr::get(xv[u][c], x);
-#pragma unroll
-                                for (int e = 0; e < VW; ++e) {
-                                    sb[c][e] = fma(w[e], x[e], sb[c][e]);
-                                    sw[c][e] = fma(w[e], w[e], sw[c][e]);
-                                }
-                            } else if constexpr (MODE == PASS_REFILL) {
-                                T x[VW], xn[VW];
-                                VTr::get(xv[u][c], x);
-#pragma unroll
-                                for (int e = 0; e < VW; ++e) x[e] = cval[c] ? x[e] : T(0);  // clamped lane
-#pragma unroll
-                                for (int e = 0; e < VW; ++e) {
-                                    const bool obs = (mb[u][c] >> e) & 1u;
-                                    xn[e] = obs ? x[e] : (w[e] + P.rho * x[e]) * P.inv1p;
-                                    const T d = xn[e] - x[e];
-                                    const T g = xn[e] - w[e];
-                                    q0 = fma(d, d, q0);
-                                    q1 = fma(x[e], x[e], q1);
-                                    q2 = fma(g, g, q2);
-                                }
-                                if (cval[c])
-                                    *reinterpret_cast<V*>(xw + (int64_t)(q + u) * xstep + cofs[c]) = VTr::make(xn);
-                            } else if constexpr (MODE == PASS_OBJ) {
-                                T x[VW];
-                                VTr::get(xv[u][c], x);
-#pragma unroll
-                                for (int e = 0; e < VW; ++e) {
-                                    const T g = (cval[c] ? x[e] : T(0)) - w[e];
-                                    q2 = fma(g, g, q2);
-                                }
-                            } else {  // PASS_MODEL: dense user layout, scalar stores
-                                if (cval[c]) {
-                                    const int64_t fb = (ebase + (int64_t)(q + u) * xstep) / P.I1p;
-#pragma unroll
-                                    for (int e = 0; e < VW; ++e) {
-                                        const int i1 = cofs[c] + e;
-                                        if (i1 < P.I1) P.out[fb * P.I1 + i1] = w[e];
-                                    }
-                                }
-                            }
-                        }
-                    }
-                };
-                int q = 0;
-                for (; q + U <= len; q += U) body(std::integral_constant<int, U>{}, q);
-                for (; q < len; ++q) body(std::integral_constant<int, 1>{}, q);
-            }
-            if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
-                n0 += (double)q0;
-                n1 += (double)q1;
-                n2 += (double)q2;
-            }
-            pos += run;
-            if (has_fast) {  // odometer advance by `run`
-                ridx[0] += run;
-#pragma unroll
-                for (int j = 0; j < MAXN - 1; ++j) {
-                    if (j + 1 < P.nred && ridx[j] >= (int)P.rdim[j]) {
-                        ridx[j] = 0;
-                        ridx[j + 1] += 1;
-                    }
-                }
-            }
+            for (int e = 0; e < EPL; ++e)
+                if (ev[e]) ws[e] *= base[e];
         }
+        T ss = T(1);
+        for (int t = 0; t < P.nss; ++t)
+            ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) ws[e] *= ss;
+        const int len = C.run_len, ri0 = C.ri0;
+        for (int q = lane; q < len; q += 32) {
+            T f = T(1);
+            for (int t = 0; t < P.nsf; ++t)
+                f *= Hb[P.sf_off[t] + (int64_t)idx[P.sf_fixmode[t]] * P.sf_fixmul[t] + (int64_t)(ri0 + q) * P.sf_inc[t]];
+            sfv[q] = f;
+        }
+        __syncwarp();
+        const int64_t ebase = (int64_t)C.fib * I1p;
+        const T* hrun = hres + (HRES && has_fast ? ri0 * I1p : 0) + ebc;
+
+        T q0 = T(0), q1 = T(0), q2 = T(0);
+        for (int off = 0; off < len; off += F) {
+            const int nf = min(F, len - off);
+            const int s = (int)(cn & (uint32_t)(D - 1));
+            mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
+            const T* sx = stg + s * STAGE;
+            const T* sh = sx + (kLoadX ? F * SR : 0);
+#pragma unroll
+            for (int st = 0; st < F / FP; ++st) {
+                const int f = st * FP + fsub;
+                if (f < nf) {
+                    const T sf = sfv[off + f];
+                    T h[EPL], w[EPL];
+                    if constexpr (HRES) lds_vec<T, EPL>(hrun + (off + f) * hstep, h);
+                    else lds_vec<T, EPL>(sh + f * SR + eb, h);
+                    weight<T, EPL>(ws, h, sf, w);
+                    if constexpr (kContract) {
+                        T x[EPL];
+                        lds_vec<T, EPL>(sx + f * SR + eb, x);
+                        accumulate<T, EPL>(w, x, sb, sw);
+                    } else if constexpr (MODE == PASS_REFILL) {
+                        T x[EPL], xn[EPL];
+                        lds_vec<T, EPL>(sx + f * SR + eb, x);
+                        const int64_t ge = ebase + (int64_t)(off + f) * xstep + eb;
+                        const uint32_t* mw = P.mask + (ge >> 5);
+                        const uint32_t bits = __funnelshift_r(__ldg(mw), __ldg(mw + 1), (uint32_t)(ge & 31));
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) {
+                            const bool obs = (bits >> e) & 1u;
+                            xn[e] = obs ? x[e] : (w[e] + P.rho * x[e]) * P.inv1p;
+                            const T d = xn[e] - x[e];
+                            const T g = xn[e] - w[e];
+                            q0 = fma(d, d, q0);
+                            q1 = fma(x[e], x[e], q1);
+                            q2 = fma(g, g, q2);
+                        }
+                        T* dst = P.Xw + ge;
+                        if (lane_full) {
+                            stg_vec<T, EPL>(dst, xn);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e)
+                                if (ev[e]) dst[e] = xn[e];
+                        }
+                    } else if constexpr (MODE == PASS_OBJ) {
+                        T x[EPL];
+                        lds_vec<T, EPL>(sx + f * SR + eb, x);
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) {
+                            const T g = x[e] - w[e];
+                            q2 = fma(g, g, q2);
+                        }
+                    } else {  // PASS_MODEL: dense user layout, scalar stores
+                        const int64_t fb = C.fib + (int64_t)(off + f) * fstep;
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e)
+                            if (eb + e < P.I1) P.out[fb * P.I1 + eb + e] = w[e];
+                    }
+                }
+            }
+            __syncwarp();
+            ++cn;
+            if (lane == 0) produce();
+        }
+        if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
+            n0 += (double)q0;
+            n1 += (double)q1;
+            n2 += (double)q2;
+        }
+        __syncwarp();  // sfv is rewritten by the next run
         // ---- flush the segment's partials into slot group + v ---------------------------
-        if constexpr (MODE == PASS_KEPT1) {
-            const int64_t slot = (int64_t)group + v;
+        if (C.seg_last) {
+            if constexpr (MODE == PASS_KEPT1) {
+                // lanes serving the same mode-1 positions in different step fibres: sum them
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-                if (cval[c]) {
-                    const int64_t o = slot * P.Lv + cofs[c];
-                    *reinterpret_cast<V*>(P.part_b + o) = VTr::make(sb[c]);
-                    *reinterpret_cast<V*>(P.part_w + o) = VTr::make(sw[c]);
+                for (int o = 16; o >= LPF; o >>= 1)
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) {
+                        sb[e] += __shfl_xor_sync(0xffffffffu, sb[e], o);
+                        sw[e] += __shfl_xor_sync(0xffffffffu, sw[e], o);
+                    }
+                if (fsub == 0) {
+                    T* pbd = P.part_b + ((int64_t)group + C.v) * P.Lv + eb;
+                    T* pwd = P.part_w + ((int64_t)group + C.v) * P.Lv + eb;
+                    if (lane_full) {
+                        stg_vec<T, EPL>(pbd, sb);
+                        stg_vec<T, EPL>(pwd, sw);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e)
+                            if (ev[e]) {
+                                pbd[e] = sb[e];
+                                pwd[e] = sw[e];
+                            }
+                    }
                 }
-            }
-        } else if constexpr (MODE == PASS_RED1) {
-            T tb = T(0), tw = T(0);
+            } else if constexpr (MODE == PASS_RED1) {
+                T tb = T(0), tw = T(0);
 #pragma unroll
-            for (int c = 0; c < CPL; ++c)
-#pragma unroll
-                for (int e = 0; e < VW; ++e) {
-                    tb += sb[c][e];
-                    tw += sw[c][e];
+                for (int e = 0; e < EPL; ++e) {
+                    tb += sb[e];
+                    tw += sw[e];
                 }
-            for (int off = lanes >> 1; off > 0; off >>= 1) {
-                tb += __shfl_xor_sync(gmask, tb, off);
-                tw += __shfl_xor_sync(gmask, tw, off);
-            }
-            if (lane == 0) {
-                const int64_t slot = (int64_t)group + v;
-                P.part_b[slot] = tb;
-                P.part_w[slot] = tw;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    tb += __shfl_xor_sync(0xffffffffu, tb, o);
+                    tw += __shfl_xor_sync(0xffffffffu, tw, o);
+                }
+                if (lane == 0) {
+                    const int64_t slot = (int64_t)group + C.v;
+                    P.part_b[slot] = tb;
+                    P.part_w[slot] = tw;
+                }
             }
         }
-        v += 1;
-        r = 0;
     }
     if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
-        for (int off = lanes >> 1; off > 0; off >>= 1) {
-            n0 += __shfl_xor_sync(gmask, n0, off);
-            n1 += __shfl_xor_sync(gmask, n1, off);
-            n2 += __shfl_xor_sync(gmask, n2, off);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+            n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         }
         if (lane == 0) {
             P.norms[(int64_t)group * 3 + 0] = n0;

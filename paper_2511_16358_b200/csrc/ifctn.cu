@@ -73,7 +73,7 @@ struct Shape {
     int64_t hoff[MAXN][MAXN] = {};  // p<q
     int64_t hld[MAXN] = {};
     int64_t htotal = 0, ones_off = 0;
-    int nchunk = 0, lanes = 0, lane_shift = 0, cpl = 0;
+    int epl = 0, lpf = 0, sf_cap = 0;  // see fiber_pass.cuh / PassCfg
     int64_t part_elems = 0, max_bw = 0, ndelta = 0, groups_bound = 0;
     int64_t delta_off[MAXN][MAXN] = {};
     int64_t proj_elems = 0;  // multi-GPU projected Gram/RHS buffer (doubles)
@@ -175,14 +175,27 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
     off += s.I1p;
     s.htotal = off;
     // lane mapping
-    s.nchunk = (int)(s.I1p / s.vw);
-    s.lanes = std::min(32, pow2ceil(s.nchunk));
-    s.lane_shift = 0;
-    while ((1 << s.lane_shift) < s.lanes) ++s.lane_shift;
-    int cpl = (s.nchunk + s.lanes - 1) / s.lanes;
-    s.cpl = pow2ceil(cpl);
-    if (s.cpl > 8) fail(IFCTN_E_UNSUPPORTED, "mode-1 size above 1024 (f32) / 512 (f64) per shard is not supported by this build");
-    s.groups_bound = std::min<int64_t>(s.nfib, kGroupBoundThreads / s.lanes);
+    // one warp per fibre stream: FP = 32/LPF fibres per step, lane serves EPL positions
+    // (the instantiated (EPL, LPF) pairs of fiber_pass.cuh)
+    if (s.esize == 4) {
+        if (s.I1p <= 64) { s.epl = 4; s.lpf = 16; }
+        else if (s.I1p <= 128) { s.epl = 4; s.lpf = 32; }
+        else if (s.I1p <= 256) { s.epl = 8; s.lpf = 32; }
+        else if (s.I1p <= 512) { s.epl = 16; s.lpf = 32; }
+        else fail(IFCTN_E_UNSUPPORTED, "mode-1 size above 512 (f32) per shard is not supported by this build");
+    } else {
+        if (s.I1p <= 32) { s.epl = 2; s.lpf = 16; }
+        else if (s.I1p <= 64) { s.epl = 2; s.lpf = 32; }
+        else if (s.I1p <= 128) { s.epl = 4; s.lpf = 32; }
+        else if (s.I1p <= 256) { s.epl = 8; s.lpf = 32; }
+        else fail(IFCTN_E_UNSUPPORTED, "mode-1 size above 256 (f64) per shard is not supported by this build");
+    }
+    s.groups_bound = std::min<int64_t>(s.nfib, kGroupBoundThreads / 32);
+    {
+        int64_t mx = 1;
+        for (int m = 1; m < order; ++m) mx = std::max(mx, s.ld[m]);
+        s.sf_cap = (int)std::max<int64_t>(8, std::min<int64_t>(256, mx));
+    }
     // partial slots: max over contract passes of (groups + NV) * Lv
     int64_t pmax = 0, bw = 0, nd = 0;
     for (int k = 0; k < order; ++k)
@@ -226,7 +239,7 @@ static Layout make_layout(const Shape& s) {
         return r;
     };
     L.x = take(s.npad * s.esize);
-    L.bits = take(align_up((s.npad + 31) / 32, 8) * 4);
+    L.bits = take((align_up((s.npad + 31) / 32, 8) + 8) * 4);  // +8 words: 2-word funnel reads
     L.g = take(s.gtotal * s.esize);
     L.h = take(s.htotal * s.esize);
     L.pb = take(s.part_elems * s.esize);
@@ -291,24 +304,43 @@ struct BlockPlan {
     const void* sol_fn = nullptr;
 };
 
-template <typename T, int MODE>
-static const void* pick_pass(int cpl, bool smem) {
-    switch (cpl) {
-        case 1: return smem ? (const void*)fiber_pass<T, MODE, 1, true> : (const void*)fiber_pass<T, MODE, 1, false>;
-        case 2: return smem ? (const void*)fiber_pass<T, MODE, 2, true> : (const void*)fiber_pass<T, MODE, 2, false>;
-        case 4: return smem ? (const void*)fiber_pass<T, MODE, 4, true> : (const void*)fiber_pass<T, MODE, 4, false>;
-        default: return smem ? (const void*)fiber_pass<T, MODE, 8, true> : (const void*)fiber_pass<T, MODE, 8, false>;
+// (kernel, ring elements per warp) of one instantiated (T, MODE, EPL, LPF, HRES)
+struct PassKernel {
+    const void* fn;
+    int64_t ring;
+};
+
+template <typename T, int MODE, int EPL, int LPF, bool HRES>
+static PassKernel pk() {
+    return {(const void*)fiber_pass<T, MODE, EPL, LPF, HRES>, PassCfg<T, EPL, LPF, HRES, MODE != PASS_MODEL>::RING};
+}
+
+template <typename T, int MODE, bool HRES>
+static PassKernel pick_pass_cfg(int epl, int lpf) {
+    if constexpr (sizeof(T) == 4) {
+        if (epl == 4) return lpf == 16 ? pk<T, MODE, 4, 16, HRES>() : pk<T, MODE, 4, 32, HRES>();
+        if (epl == 8) return pk<T, MODE, 8, 32, HRES>();
+        return pk<T, MODE, 16, 32, HRES>();
+    } else {
+        if (epl == 2) return lpf == 16 ? pk<T, MODE, 2, 16, HRES>() : pk<T, MODE, 2, 32, HRES>();
+        if (epl == 4) return pk<T, MODE, 4, 32, HRES>();
+        return pk<T, MODE, 8, 32, HRES>();
     }
 }
 
+template <typename T, int MODE>
+static PassKernel pick_pass(int epl, int lpf, bool hres) {
+    return hres ? pick_pass_cfg<T, MODE, true>(epl, lpf) : pick_pass_cfg<T, MODE, false>(epl, lpf);
+}
+
 template <typename T>
-static const void* pick_pass_mode(int mode, int cpl, bool smem) {
+static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
     switch (mode) {
-        case PASS_KEPT1: return pick_pass<T, PASS_KEPT1>(cpl, smem);
-        case PASS_RED1: return pick_pass<T, PASS_RED1>(cpl, smem);
-        case PASS_REFILL: return pick_pass<T, PASS_REFILL>(cpl, smem);
-        case PASS_OBJ: return pick_pass<T, PASS_OBJ>(cpl, smem);
-        default: return pick_pass<T, PASS_MODEL>(cpl, smem);
+        case PASS_KEPT1: return pick_pass<T, PASS_KEPT1>(epl, lpf, hres);
+        case PASS_RED1: return pick_pass<T, PASS_RED1>(epl, lpf, hres);
+        case PASS_REFILL: return pick_pass<T, PASS_REFILL>(epl, lpf, hres);
+        case PASS_OBJ: return pick_pass<T, PASS_OBJ>(epl, lpf, hres);
+        default: return pick_pass<T, PASS_MODEL>(epl, lpf, hres);
     }
 }
 
@@ -338,7 +370,6 @@ struct Solver : SolverBase {
     unsigned char* ws = nullptr;
     bool own_ws = false;
     int nsm = 0;
-    bool use_smem = false;
     size_t smem_limit = 0;
     // device views
     T *X, *G, *H, *pb, *pw;
@@ -414,9 +445,6 @@ struct Solver : SolverBase {
         p.inv1p = (T)(1.0 / (1.0 + rho));
         p.I1 = (int)s.I1;
         p.I1p = (int)s.I1p;
-        p.nchunk = s.nchunk;
-        p.lanes = s.lanes;
-        p.lane_shift = s.lane_shift;
         p.nouter = N - 1;
         for (int m = 0; m < N; ++m) p.fstride[m] = s.fstride[m];
         const bool contract = (mode == PASS_KEPT1 || mode == PASS_RED1);
@@ -482,21 +510,34 @@ struct Solver : SolverBase {
                 }
             }
         p.ones_off = s.ones_off;
-        const int gpc = kPassThreads / s.lanes;  // groups per CTA
-        p.sf_cap = std::max<int>(8, (int)((16384 / s.esize) / gpc));
-        // grid: one wave of groups, equal fibre counts
-        const size_t smem = (use_smem ? (size_t)(s.htotal * s.esize) : 0) + (size_t)gpc * p.sf_cap * s.esize;
-        pp.fn = pick_pass_mode<T>(mode, s.cpl, use_smem);
-        if (smem > 48 * 1024) CU(cudaFuncSetAttribute(pp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        p.sf_cap = s.sf_cap;
+        // H_{0,r0} (the per-fibre factor) resident in shared memory when it fits
+        const int64_t rdim0 = red.empty() ? 1 : s.ld[red[0]];
+        const int64_t hres_elems = red.empty() ? s.I1p : s.I1p * rdim0;
+        const bool hres = hres_elems * s.esize <= 32 * 1024;
+        p.hres_src = red.empty() ? s.ones_off : p.vf_off;
+        p.hres_elems = hres ? hres_elems : 0;
+        // shared memory per CTA: [mbarriers][sf vectors][resident H][TMA ring per warp]
+        const int nwarps = kPassThreads / 32;
+        const PassKernel kern = pick_pass_mode<T>(mode, s.epl, s.lpf, hres);
+        p.sfv_off = align_up((int64_t)nwarps * 8 * 8, 128);  // ≤ 8 stage barriers per warp
+        p.hres_off = align_up(p.sfv_off + (int64_t)nwarps * p.sf_cap * s.esize, 128);
+        p.stage_off = align_up(p.hres_off + p.hres_elems * s.esize, 128);
+        const size_t smem = (size_t)(p.stage_off + (int64_t)nwarps * kern.ring * s.esize);
+        pp.fn = kern.fn;
+        if (smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "fibre-pass shared memory exceeds the device limit");
+        // one kernel serves several passes with different sizes: allow the device maximum
+        CU(cudaFuncSetAttribute(pp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit));
         int nb = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pp.fn, kPassThreads, smem));
         if (nb < 1) nb = 1;
-        int64_t gmax = (int64_t)nsm * nb * (kPassThreads / s.lanes);
+        // grid: one wave of warps ("groups"), equal fibre counts
+        int64_t gmax = (int64_t)nsm * nb * nwarps;
         gmax = std::min(gmax, s.groups_bound);
         const int64_t L = std::max<int64_t>(1, (s.nfib + gmax - 1) / gmax);
         p.L = L;
         p.ngroups = (s.nfib + L - 1) / L;
-        pp.grid = dim3((unsigned)((p.ngroups * s.lanes + kPassThreads - 1) / kPassThreads));
+        pp.grid = dim3((unsigned)((p.ngroups + nwarps - 1) / nwarps));
         pp.smem = smem;
         return pp;
     }
@@ -594,7 +635,6 @@ struct Solver : SolverBase {
         int smo = 0;
         CU(cudaDeviceGetAttribute(&smo, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         smem_limit = (size_t)smo;
-        use_smem = (flags & 4u) && (size_t)(s.htotal * s.esize) <= smem_limit;
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
