@@ -67,6 +67,7 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NONE 0u
 #define IFCTN_FLAG_NO_GRAPH 1u /* run sweeps as plain launches instead of a CUDA graph     */
 #define IFCTN_FLAG_X_FULL 2u   /* `observed` is a full X (values off Ω kept), for resume  */
+#define IFCTN_FLAG_NO_VBLOCK 8u /* diagnostic: plain fibre walk for every block (no v-blocking) */
 
 /* Multi-GPU description (one process per GPU).  NULL or world == 1: single GPU. */
 typedef struct {

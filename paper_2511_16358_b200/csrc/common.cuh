@@ -181,6 +181,14 @@ struct PassParams {
     int sf_cap;              // per-warp shared-memory slots for the fast scalar factors
     int64_t sfv_off, hres_off, stage_off;  // byte offsets in dynamic shared memory
     int64_t hres_src, hres_elems;          // resident H block (HRES): offset in H, elements
+    // v-blocking (fiber_pass_vb only): mode 1 (code mode 1, fibre stride 1) is kept; runs are
+    // F consecutive fibres i_1 ∈ [b·F, b·F+F) at one reduced position r; positions are
+    // ((vb·FR + r)·F + f), vb = b + nb0·kidx1.
+    int64_t nb0;
+    int64_t vf2_off, hres2_elems;  // tiled pass: resident H_{0,r0} block after H_{0,1}
+    int ntf;                       // tiled pass: scalar factors touching mode 1 or r0
+    int64_t tf_off[MAXP], tf_ld[MAXP];
+    int tf_p[MAXP], tf_q[MAXP];
 };
 
 template <typename T>
@@ -196,6 +204,7 @@ struct ReduceParams {
     int kIsMode0;        // KEPT1: k == 0 (j = i_1, a = v) else (a = i_1, j = v)
     int kmode0IsK;       // RED1: kmode[0] == k
     int64_t kdim0;
+    int64_t VB, nb0;     // v-blocking: block width (1 = off), blocks along kmode[0]
 };
 
 template <typename T>

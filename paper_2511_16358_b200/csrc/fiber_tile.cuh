@@ -1,0 +1,264 @@
+// fiber_tile.cuh — v-blocked (tiled) contraction pass for the blocks that KEEP mode 2
+// (code mode 1, fibre stride 1).
+//
+// Same arithmetic as fiber_walk.cuh (β/ω of Eq. 8 from the leave-one-pair-out weights of
+// Prop. 1).  Only the fibre order differs: in the plain walk the kept
+// index is fixed inside a segment, so consecutive fibres of a run are I_1 fibres apart (one
+// 256-B piece per 16 KB for C5) and DRAM locality suffers.  Here a warp walks TILES of
+// F consecutive kept values v = i_1 (one contiguous TMA copy per stage) × a run of the fast
+// reduced index i_{r0}; every lane keeps F/FP accumulator sets, one per kept value, and
+//     M = ws(i_0 | slow) · H_{0,1}(i_0, v) · H_{0,r0}(i_0, i_{r0}) · sf(v, i_{r0})
+// with both H column blocks resident in shared memory, ws in registers and the scalar
+// factors touching mode 1 or r0 tabulated per tile in shared memory (sfv[f][t]).
+// Partial slot of (warp g, v) = (g + vb)·F + f (reduce_partials with VB = F).
+#pragma once
+
+#include "fiber_walk.cuh"
+
+namespace ifctn {
+
+template <typename T, int MODE, int EPL, int LPF, bool HRES>
+__global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
+    fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
+    static_assert(MODE == PASS_KEPT1 || MODE == PASS_RED1, "contraction passes only");
+    static_assert(HRES, "the tiled pass keeps its H blocks resident");
+    using Cfg = PassCfg<T, EPL, LPF, true, true>;
+    constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR;
+    constexpr int STAGE = F * SR;
+    constexpr int NS = F / FP;  // accumulator sets per lane
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int fsub = lane / LPF;
+    const int eb = (lane % LPF) * EPL;
+    const int I1p = P.I1p;
+    const int RL = P.sf_cap / F;  // tile run capacity (stages per tile)
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * D;
+    T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sf_cap;
+    T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);  // [H_{0,1} | H_{0,r0}]
+    T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
+    {
+        const float4* s1 = reinterpret_cast<const float4*>(P.H + P.hres_src);
+        const float4* s2 = reinterpret_cast<const float4*>(P.H + P.vf2_off);
+        float4* dst = reinterpret_cast<float4*>(hres);
+        const int n1 = (int)(P.hres_elems * sizeof(T) / 16), n2 = (int)(P.hres2_elems * sizeof(T) / 16);
+        for (int e = threadIdx.x; e < n1 + n2; e += blockDim.x) dst[e] = e < n1 ? s1[e] : s2[e - n1];
+    }
+    for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
+    if (lane == 0)
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    const int group = blockIdx.x * nwarps + warp;
+    if (group >= P.ngroups) return;
+
+    const uint32_t bar0 = smem_u32(bars);
+    const uint32_t stg0 = smem_u32(stg);
+    const T* __restrict__ Hb = P.H;
+    bool ev[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) ev[e] = eb + e < I1p;
+    const bool lane_full = eb + EPL <= I1p;
+    const int ebc = eb < I1p ? eb : 0;
+    const int FR = (int)P.FR;
+    const int kdim0 = (int)P.kdim[0];
+    const int nb0 = (int)P.nb0;
+    const int rdim0 = (int)P.rdim[0];
+    const int fstep = (int)P.fstride[P.rmode[0]];
+    const int h1step = P.vf_off >= 0 ? I1p : 0;      // H_{0,1} is a factor (not the kept pair)
+    const T* h1 = hres + ebc;                         // H_{0,1} block or the ones column
+    const T* h2 = hres + P.hres_elems + ebc;          // H_{0,r0} block
+    const uint32_t rowbytes = (uint32_t)(I1p * sizeof(T));
+
+    // stages = positions q = vb·FR + r (r in odometer order, r0 fastest); warp range [q0, q1)
+    const int q0 = group * (int)(P.L / F);
+    const int q1 = min(q0 + (int)(P.L / F), (int)(P.nfib / F));
+    auto decode = [&](int q, int& vb, int& b0, int& nvalid, int (&ridx)[MAXN]) {
+        vb = q / FR;
+        int r = q - vb * FR;
+        b0 = (vb % nb0) * F;
+        nvalid = min(F, kdim0 - b0);
+        int fib = b0;  // fstride[1] == 1
+        if (P.nkept >= 2) fib += (vb / nb0) * (int)P.fstride[P.kmode[1]];
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j) {
+            ridx[j] = 0;
+            if (j < P.nred) {
+                ridx[j] = r % (int)P.rdim[j];
+                r /= (int)P.rdim[j];
+                fib += ridx[j] * (int)P.fstride[P.rmode[j]];
+            }
+        }
+        return fib;
+    };
+
+    // ---- producer (lane 0): one stage (F contiguous fibres) per position, D ahead --------
+    // incremental odometer over r (rmode[0] fastest); full decode only when vb changes
+    int pq = q0;
+    uint32_t p_n = 0;
+    int p_vb, p_b0, p_nvalid, p_ridx[MAXN];
+    int p_fib = decode(q0, p_vb, p_b0, p_nvalid, p_ridx);
+    auto produce = [&]() {
+        if (pq >= q1) return;
+        const int fib = p_fib;
+        const int nvalid = p_nvalid;
+        const int s = (int)(p_n & (uint32_t)(D - 1));
+        const uint32_t bar = bar0 + 8u * (uint32_t)s;
+        const uint32_t sx = stg0 + (uint32_t)(s * STAGE * (int)sizeof(T));
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx_a(bar, (uint32_t)nvalid * rowbytes);
+        const T* xs = P.X + (int64_t)fib * I1p;
+        if (SR == I1p) {
+            tma_g2s_a(sx, xs, (uint32_t)nvalid * rowbytes, bar);
+        } else {
+            for (int f = 0; f < nvalid; ++f)
+                tma_g2s_a(sx + (uint32_t)(f * SR * (int)sizeof(T)), xs + (int64_t)f * I1p, rowbytes, bar);
+        }
+        ++pq;
+        ++p_n;
+        if (pq >= q1) return;
+        // advance the odometer
+        bool wrapped = true;
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j) {
+            if (wrapped && j < P.nred) {
+                p_ridx[j] += 1;
+                p_fib += (int)P.fstride[P.rmode[j]];
+                if (p_ridx[j] < (int)P.rdim[j]) {
+                    wrapped = false;
+                } else {
+                    p_fib -= p_ridx[j] * (int)P.fstride[P.rmode[j]];
+                    p_ridx[j] = 0;
+                }
+            }
+        }
+        if (wrapped) p_fib = decode(pq, p_vb, p_b0, p_nvalid, p_ridx);  // next kept block
+    };
+    if (lane == 0)
+        for (int d = 0; d < D; ++d) produce();
+
+    T sb[NS][EPL], sw[NS][EPL];
+#pragma unroll
+    for (int t = 0; t < NS; ++t)
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) sb[t][e] = sw[t][e] = T(0);
+    uint32_t cn = 0;
+    int q = q0;
+    while (q < q1) {
+        int vb, b0, nvalid, ridx[MAXN];
+        decode(q, vb, b0, nvalid, ridx);
+        const int seg_end = min(q1, (vb + 1) * FR);           // end of this kept block
+        const int rl = min(min(seg_end - q, rdim0 - ridx[0]), RL);  // tile: r0 run
+        // ---- tile setup: slow factors and the (v, i_{r0}) scalar table --------------------
+        int idx[MAXN];
+#pragma unroll
+        for (int m = 0; m < MAXN; ++m) idx[m] = 0;
+        if (P.nkept >= 2) idx[P.kmode[1]] = vb / nb0;
+#pragma unroll
+        for (int j = 0; j < MAXN; ++j)
+            if (j < P.nred) idx[P.rmode[j]] = ridx[j];
+        T ws[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) ws[e] = ev[e] ? T(1) : T(0);
+        for (int t = 0; t < P.nvs; ++t) {
+            const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * I1p + eb;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e)
+                if (ev[e]) ws[e] *= base[e];
+        }
+        T ss = T(1);
+        for (int t = 0; t < P.nss; ++t)
+            ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) ws[e] *= ss;
+        const int r0m = P.rmode[0];
+        for (int e = lane; e < F * rl; e += 32) {
+            const int f = e / rl, t = e - f * rl;
+            int ix[MAXN];
+#pragma unroll
+            for (int m = 0; m < MAXN; ++m) ix[m] = idx[m];
+            ix[1] = b0 + min(f, nvalid - 1);
+            ix[r0m] = ridx[0] + t;
+            T val = T(1);
+            for (int u = 0; u < P.ntf; ++u)
+                val *= Hb[P.tf_off[u] + (int64_t)ix[P.tf_q[u]] * P.tf_ld[u] + ix[P.tf_p[u]]];
+            sfv[f * RL + t] = val;
+        }
+        __syncwarp();
+        const T* h2run = h2 + (int64_t)ridx[0] * I1p;
+        for (int t = 0; t < rl; ++t) {
+            const int s = (int)(cn & (uint32_t)(D - 1));
+            mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
+            const T* sx = stg + s * STAGE;
+            T hr[EPL];
+            lds_vec<T, EPL>(h2run + t * I1p, hr);
+            T wr[EPL];
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) wr[e] = ws[e] * hr[e];
+#pragma unroll
+            for (int st = 0; st < NS; ++st) {
+                const int f = st * FP + fsub;
+                if (f < nvalid) {
+                    T h[EPL], w[EPL], x[EPL];
+                    lds_vec<T, EPL>(h1 + (b0 + f) * h1step, h);
+                    weight<T, EPL>(wr, h, sfv[f * RL + t], w);
+                    lds_vec<T, EPL>(sx + f * SR + eb, x);
+                    accumulate<T, EPL>(w, x, sb[st], sw[st]);
+                }
+            }
+            __syncwarp();
+            ++cn;
+            if (lane == 0) produce();
+        }
+        __syncwarp();  // sfv is rewritten by the next tile
+        q += rl;
+        (void)fstep;
+        if (q >= seg_end) {  // kept block finished (or range end): flush its F values
+#pragma unroll
+            for (int st = 0; st < NS; ++st) {
+                const int f = st * FP + fsub;
+                const int64_t slot = ((int64_t)group + vb) * F + f;
+                if constexpr (MODE == PASS_KEPT1) {
+                    if (f < nvalid) {
+                        T* pbd = P.part_b + slot * P.Lv + eb;
+                        T* pwd = P.part_w + slot * P.Lv + eb;
+                        if (lane_full) {
+                            stg_vec<T, EPL>(pbd, sb[st]);
+                            stg_vec<T, EPL>(pwd, sw[st]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e)
+                                if (ev[e]) {
+                                    pbd[e] = sb[st][e];
+                                    pwd[e] = sw[st][e];
+                                }
+                        }
+                    }
+                } else {
+                    T tb = T(0), tw = T(0);
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) {
+                        tb += sb[st][e];
+                        tw += sw[st][e];
+                    }
+#pragma unroll
+                    for (int o = LPF / 2; o > 0; o >>= 1) {  // the fibre's LPF lanes
+                        tb += __shfl_xor_sync(0xffffffffu, tb, o);
+                        tw += __shfl_xor_sync(0xffffffffu, tw, o);
+                    }
+                    if ((lane % LPF) == 0 && f < nvalid) {
+                        P.part_b[slot] = tb;
+                        P.part_w[slot] = tw;
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) sb[st][e] = sw[st][e] = T(0);
+            }
+        }
+    }
+}
+
+}  // namespace ifctn

@@ -444,3 +444,4 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
 }
 
 }  // namespace ifctn
+

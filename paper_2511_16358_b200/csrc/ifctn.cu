@@ -17,7 +17,8 @@
 
 #include "../../include/ifctn.h"
 #include "common.cuh"
-#include "fiber_pass.cuh"
+#include "fiber_walk.cuh"
+#include "fiber_tile.cuh"
 #include "solve.cuh"
 #include "nccl_lite.h"
 
@@ -50,6 +51,7 @@ static int pow2ceil(int x) {
 }
 
 constexpr int64_t kGroupBoundThreads = 160LL * 2048;  // ≥ resident threads of any B200 part
+constexpr unsigned kFlagNoVBlock = IFCTN_FLAG_NO_VBLOCK;
 
 // ------------------------------------------------------------------------------------------
 // Shape: everything derivable from the arguments alone (no device needed).
@@ -206,7 +208,12 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
                 if (m == k || m == i) NV *= s.ld[m];
             const bool kept1 = (k == 0 || i == 0);
             const int64_t Lv = kept1 ? s.I1p : 1;
-            pmax = std::max(pmax, (s.groups_bound + NV) * Lv);
+            int64_t slots = s.groups_bound + NV;
+            if (order >= 2 && (k == 1 || i == 1)) {  // v-blocked pass: (groups + NVB)·F, F ≤ 8
+                const int64_t kdim1 = NV / s.ld[1];
+                slots = s.groups_bound * 8 + NV + 8 * kdim1;
+            }
+            pmax = std::max(pmax, slots * Lv);
             bw = std::max(bw, s.ld[i] * s.ld[k]);
             s.delta_off[k][i] = nd;
             nd += s.ld[k];
@@ -308,11 +315,21 @@ struct BlockPlan {
 struct PassKernel {
     const void* fn;
     int64_t ring;
+    int F;
 };
 
+// MODE >= 100: the v-blocked contraction kernel for MODE - 100
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 static PassKernel pk() {
-    return {(const void*)fiber_pass<T, MODE, EPL, LPF, HRES>, PassCfg<T, EPL, LPF, HRES, MODE != PASS_MODEL>::RING};
+    using Cfg = PassCfg<T, EPL, LPF, HRES, (MODE % 100) != PASS_MODEL>;
+    if constexpr (MODE >= 100) {
+        constexpr int M = MODE - 100;
+        if constexpr ((M == PASS_KEPT1 || M == PASS_RED1) && HRES)
+            return {(const void*)fiber_pass_vb<T, M, EPL, LPF, HRES>, Cfg::RING, Cfg::F};
+        return {nullptr, 0, 0};
+    } else {
+        return {(const void*)fiber_pass<T, MODE, EPL, LPF, HRES>, Cfg::RING, Cfg::F};
+    }
 }
 
 template <typename T, int MODE, bool HRES>
@@ -336,6 +353,8 @@ static PassKernel pick_pass(int epl, int lpf, bool hres) {
 template <typename T>
 static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
     switch (mode) {
+        case 100 + PASS_KEPT1: return pick_pass<T, 100 + PASS_KEPT1>(epl, lpf, hres);
+        case 100 + PASS_RED1: return pick_pass<T, 100 + PASS_RED1>(epl, lpf, hres);
         case PASS_KEPT1: return pick_pass<T, PASS_KEPT1>(epl, lpf, hres);
         case PASS_RED1: return pick_pass<T, PASS_RED1>(epl, lpf, hres);
         case PASS_REFILL: return pick_pass<T, PASS_REFILL>(epl, lpf, hres);
@@ -428,7 +447,8 @@ struct Solver : SolverBase {
         CU(cudaLaunchKernel(fn, g, b, args, smem, st));
     }
 
-    PassPlan<T> make_pass(int mode, int k, int i) {
+    // vblk: v-blocked contraction (mode 1 kept; fiber_pass_vb), else the plain walk
+    PassPlan<T> make_pass(int mode, int k, int i, bool vblk = false) {
         const int N = s.N;
         PassPlan<T> pp;
         PassParams<T>& p = pp.p;
@@ -455,7 +475,8 @@ struct Solver : SolverBase {
             else red.push_back(m);
         }
         // odometer order: r0 = the largest reduced mode (ties: lowest), then ascending
-        if (!red.empty()) {
+        // (v-blocked: ascending; the fast index is the kept mode 1)
+        if (!red.empty() && !vblk) {
             int best = 0;
             for (size_t t = 1; t < red.size(); ++t)
                 if (s.ld[red[t]] > s.ld[red[best]]) best = (int)t;
@@ -481,8 +502,37 @@ struct Solver : SolverBase {
         p.Lv = (mode == PASS_KEPT1) ? s.I1p : 1;
         const int r0 = red.empty() ? -1 : red[0];
         // weight factors: every pair p<q except {k,i} when contracting
-        p.vf_off = 0;
-        for (int a = 0; a < N; ++a)
+        p.vf_off = -1;
+        p.vf2_off = -1;
+        if (vblk) {  // tiled pass (fiber_tile.cuh): fast indices are mode 1 and r0
+            for (int a = 0; a < N; ++a)
+                for (int b = a + 1; b < N; ++b) {
+                    if ((a == k && b == i) || (a == i && b == k)) continue;
+                    const int64_t off = s.hoff[a][b];
+                    if (a == 0) {
+                        if (b == 1) p.vf_off = off;
+                        else if (b == r0) p.vf2_off = off;
+                        else {
+                            p.vs_off[p.nvs] = off;
+                            p.vs_mode[p.nvs] = b;
+                            ++p.nvs;
+                        }
+                    } else if (a == 1 || b == 1 || a == r0 || b == r0) {
+                        p.tf_off[p.ntf] = off;
+                        p.tf_ld[p.ntf] = s.hld[a];
+                        p.tf_p[p.ntf] = a;
+                        p.tf_q[p.ntf] = b;
+                        ++p.ntf;
+                    } else {
+                        p.ss_off[p.nss] = off;
+                        p.ss_ld[p.nss] = s.hld[a];
+                        p.ss_p[p.nss] = a;
+                        p.ss_q[p.nss] = b;
+                        ++p.nss;
+                    }
+                }
+        }
+        for (int a = 0; a < N && !vblk; ++a)
             for (int b = a + 1; b < N; ++b) {
                 if (contract && ((a == k && b == i) || (a == i && b == k))) continue;
                 const int64_t off = s.hoff[a][b];
@@ -511,18 +561,32 @@ struct Solver : SolverBase {
             }
         p.ones_off = s.ones_off;
         p.sf_cap = s.sf_cap;
-        // H_{0,r0} (the per-fibre factor) resident in shared memory when it fits
-        const int64_t rdim0 = red.empty() ? 1 : s.ld[red[0]];
-        const int64_t hres_elems = red.empty() ? s.I1p : s.I1p * rdim0;
+        if (vblk) p.sf_cap = 8 * (int)std::min<int64_t>(s.ld[r0], 32);  // F ≤ 8 rows × run ≤ 32
+        // H_{0,r0} (the per-fibre factor) resident in shared memory when it fits; without
+        // that factor (no fast mode, or the kept pair itself) a column of ones stands in
+        const bool hfac = p.vf_off >= 0;
+        const int64_t rdim0 = hfac ? s.ld[vblk ? 1 : r0] : 1;
+        const int64_t hres_elems = hfac ? s.I1p * rdim0 : s.I1p;
         const bool hres = hres_elems * s.esize <= 32 * 1024;
-        p.hres_src = red.empty() ? s.ones_off : p.vf_off;
+        p.hres_src = hfac ? p.vf_off : s.ones_off;
         p.hres_elems = hres ? hres_elems : 0;
+        if (vblk) {  // second resident block: H_{0,r0}
+            p.hres2_elems = s.I1p * s.ld[r0];
+            if (!hres || p.hres2_elems * s.esize > 32 * 1024) fail(IFCTN_E_STATE, "tiled pass needs resident H blocks");
+        }
         // shared memory per CTA: [mbarriers][sf vectors][resident H][TMA ring per warp]
         const int nwarps = kPassThreads / 32;
-        const PassKernel kern = pick_pass_mode<T>(mode, s.epl, s.lpf, hres);
+        const PassKernel kern = pick_pass_mode<T>(vblk ? 100 + mode : mode, s.epl, s.lpf, hres);
+        if (!kern.fn) fail(IFCTN_E_STATE, "no kernel for this pass");
+        if (vblk) {  // positions (vb·FR + r)·F + f over NVB = nb0·kdim1 kept blocks
+            const int64_t F = kern.F;
+            if (F > p.sf_cap) fail(IFCTN_E_STATE, "v-block wider than the sf vector");
+            p.nb0 = (p.kdim[0] + F - 1) / F;
+            p.nfib = p.nb0 * p.kdim[1] * p.FR * F;
+        }
         p.sfv_off = align_up((int64_t)nwarps * 8 * 8, 128);  // ≤ 8 stage barriers per warp
         p.hres_off = align_up(p.sfv_off + (int64_t)nwarps * p.sf_cap * s.esize, 128);
-        p.stage_off = align_up(p.hres_off + p.hres_elems * s.esize, 128);
+        p.stage_off = align_up(p.hres_off + (p.hres_elems + p.hres2_elems) * s.esize, 128);
         const size_t smem = (size_t)(p.stage_off + (int64_t)nwarps * kern.ring * s.esize);
         pp.fn = kern.fn;
         if (smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "fibre-pass shared memory exceeds the device limit");
@@ -534,12 +598,26 @@ struct Solver : SolverBase {
         // grid: one wave of warps ("groups"), equal fibre counts
         int64_t gmax = (int64_t)nsm * nb * nwarps;
         gmax = std::min(gmax, s.groups_bound);
-        const int64_t L = std::max<int64_t>(1, (s.nfib + gmax - 1) / gmax);
+        const int64_t unit = vblk ? kern.F : 1;  // v-blocked ranges hold whole runs
+        const int64_t nunits = p.nfib / unit;
+        const int64_t L = std::max<int64_t>(1, (nunits + gmax - 1) / gmax) * unit;
         p.L = L;
-        p.ngroups = (s.nfib + L - 1) / L;
+        p.ngroups = (p.nfib + L - 1) / L;
         pp.grid = dim3((unsigned)((p.ngroups + nwarps - 1) / nwarps));
         pp.smem = smem;
         return pp;
+    }
+
+    // the tiled pass applies when a reduced outer mode exists and both resident H blocks fit
+    bool tile_ok(int k, int i) const {
+        int r0 = -1;
+        for (int m = 1; m < s.N; ++m)
+            if (m != k && m != i && (r0 < 0 || s.ld[m] > s.ld[r0])) r0 = m;
+        if (r0 < 0) return false;
+        const bool pair01_kept = (k == 0 || i == 0);
+        const int64_t b1 = (pair01_kept ? s.I1p : s.I1p * s.ld[1]) * s.esize;
+        const int64_t b2 = s.I1p * s.ld[r0] * s.esize;
+        return b1 <= 32 * 1024 && b2 <= 32 * 1024;
     }
 
     void plan() {
@@ -552,7 +630,8 @@ struct Solver : SolverBase {
                 b.k = k;
                 b.i = i;
                 const int mode = (k == 0 || i == 0) ? PASS_KEPT1 : PASS_RED1;
-                b.pass = make_pass(mode, k, i);
+                const bool vblk = (k == 1 || i == 1) && !(flags & kFlagNoVBlock) && tile_ok(k, i);
+                b.pass = make_pass(mode, k, i, vblk);
                 ReduceParams<T>& r = b.red;
                 r.part_b = pb;
                 r.part_w = pw;
@@ -568,6 +647,8 @@ struct Solver : SolverBase {
                 r.kIsMode0 = (k == 0);
                 r.kmode0IsK = (b.pass.p.nkept >= 1 && b.pass.p.kmode[0] == k);
                 r.kdim0 = b.pass.p.kdim[0];
+                r.VB = vblk ? b.pass.p.nfib / (b.pass.p.nb0 * b.pass.p.kdim[1] * b.pass.p.FR) : 1;
+                r.nb0 = vblk ? b.pass.p.nb0 : r.kdim0;
                 b.red_grid = dim3((unsigned)r.NV);
                 SolveParams<T>& q = b.sol;
                 q.beta = beta;

@@ -12,8 +12,13 @@ template <typename T>
 __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
     __shared__ double sb[256], sw[256];
     const int64_t v = blockIdx.x;
-    const int64_t g0 = (v * P.FR) / P.L;
-    const int64_t g1 = ((v + 1) * P.FR - 1) / P.L;
+    // v-blocking (fiber_pass_vb): v = (kidx0, kidx1) lies in block vb at offset vv; the warps
+    // that covered block vb are g0..g1 and their slot of v is (g + vb)·VB + vv.  VB = 1 is the
+    // plain layout (vb = v).
+    const int64_t kx0 = v % P.kdim0, kx1 = v / P.kdim0;
+    const int64_t vb = kx0 / P.VB + P.nb0 * kx1, vv = kx0 % P.VB;
+    const int64_t g0 = (vb * P.FR * P.VB) / P.L;
+    const int64_t g1 = ((vb + 1) * P.FR * P.VB - 1) / P.L;
     const int64_t nslots = g1 - g0 + 1;
     const int ex = (int)(P.Lv < 256 ? P.Lv : 256);
     // round ex up to a power of two so the y-split is a clean tree
@@ -27,7 +32,7 @@ __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) 
         double b = 0.0, w = 0.0;
         if (e < P.Lv) {
             for (int64_t s = ty; s < nslots; s += ny) {
-                const int64_t o = (g0 + s + v) * P.Lv + e;
+                const int64_t o = ((g0 + s + vb) * P.VB + vv) * P.Lv + e;
                 b += (double)P.part_b[o];
                 w += (double)P.part_w[o];
             }

@@ -70,10 +70,13 @@ def test_model_reconstruction(name):
 
 # --------------------------------------------------------------- a2: (β, ω) contraction ---
 
+@pytest.mark.parametrize("vblock", [True, False], ids=["vblock", "plain"])
 @pytest.mark.parametrize("name", SMALL + ["C2"])
-def test_block_coefficients(name):
+def test_block_coefficients(name, vblock):
+    """Both fibre walks (v-blocked for blocks keeping mode 2, and the plain walk)."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_VBLOCK
     p = make_config(name)
-    s = make_solver(p)
+    s = make_solver(p, flags=0 if vblock else IFCTN_FLAG_NO_VBLOCK)
     sh, G, X = oracle_state(p)
     Xin = X.astype(p.dtype)  # the oracle reads the same (exactly representable) X values
     tol = tol_for(p, 1e-5, 1e-12)
