@@ -68,6 +68,8 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NO_GRAPH 1u /* run sweeps as plain launches instead of a CUDA graph     */
 #define IFCTN_FLAG_X_FULL 2u   /* `observed` is a full X (values off Ω kept), for resume  */
 #define IFCTN_FLAG_NO_VBLOCK 8u /* diagnostic: plain fibre walk for every block (no v-blocking) */
+#define IFCTN_FLAG_NO_FUSE 16u  /* diagnostic: never fuse a sweep's X update into the next
+                                   sweep's first block (see ifctn_sweep)                      */
 
 /* Multi-GPU description (one process per GPU).  NULL or world == 1: single GPU. */
 typedef struct {
@@ -122,7 +124,10 @@ ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims,
 /* Run up to t_max PAM sweeps (Algorithm 1 while-loop).  eps ≤ 0 runs exactly
  * t_max sweeps and, with trace == NULL, returns without synchronising (device errors are
  * then reported by ifctn_sync).  eps > 0 stops after the first sweep with rel_change < eps.
- * trace (host, t_max rows) is filled when non-NULL.  *sweeps_done (may be NULL).         */
+ * trace (host, t_max rows) is filled when non-NULL.  *sweeps_done (may be NULL).
+ * With eps ≤ 0, no trace and t_max ≥ 2 the X update of sweep s and the first block of
+ * sweep s+1 run as one pass over X (they use the same factors); results are the same
+ * sweeps up to floating-point summation order.                                           */
 ifctn_status ifctn_sweep(ifctn_ctx* ctx, int t_max, double eps, int* sweeps_done,
                          ifctn_trace_row* trace);
 

@@ -36,6 +36,7 @@ enum PassMode : int {
     PASS_REFILL = 2,  // a5: X update + norms
     PASS_OBJ = 3,     // f = ½‖X − t‖² only
     PASS_MODEL = 4,   // write t = iFCTN(G) in the user layout
+    PASS_FUSED = 5,   // a5 of sweep s fused with a2 of block (0,1) of sweep s+1 (KEPT1 layout)
 };
 
 template <typename T> struct VecT;
@@ -186,6 +187,7 @@ struct PassParams {
     // ((vb·FR + r)·F + f), vb = b + nb0·kidx1.
     int64_t nb0;
     int64_t vf2_off, hres2_elems;  // tiled pass: resident H_{0,r0} block after H_{0,1}
+    int64_t h01_off, hres3_elems;  // fused pass: H_{0,1} (global offset; resident when tiled)
     int ntf;                       // tiled pass: scalar factors touching mode 1 or r0
     int64_t tf_off[MAXP], tf_ld[MAXP];
     int tf_p[MAXP], tf_q[MAXP];

@@ -20,8 +20,11 @@ namespace ifctn {
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
-    static_assert(MODE == PASS_KEPT1 || MODE == PASS_RED1, "contraction passes only");
+    static_assert(MODE == PASS_KEPT1 || MODE == PASS_RED1 || MODE == PASS_FUSED, "contraction passes only");
     static_assert(HRES, "the tiled pass keeps its H blocks resident");
+    // PASS_FUSED: a5 refill of sweep s fused with block (0,1)'s a2 of sweep s+1 (K = {0,1}):
+    // t = M·H_{0,1}(i_0, v), X_new written back and used for β.
+    constexpr bool kFused = (MODE == PASS_FUSED);
     using Cfg = PassCfg<T, EPL, LPF, true, true>;
     constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR;
     constexpr int STAGE = F * SR;
@@ -41,9 +44,12 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     {
         const float4* s1 = reinterpret_cast<const float4*>(P.H + P.hres_src);
         const float4* s2 = reinterpret_cast<const float4*>(P.H + P.vf2_off);
+        const float4* s3 = reinterpret_cast<const float4*>(P.H + P.h01_off);
         float4* dst = reinterpret_cast<float4*>(hres);
         const int n1 = (int)(P.hres_elems * sizeof(T) / 16), n2 = (int)(P.hres2_elems * sizeof(T) / 16);
-        for (int e = threadIdx.x; e < n1 + n2; e += blockDim.x) dst[e] = e < n1 ? s1[e] : s2[e - n1];
+        const int n3 = (int)(P.hres3_elems * sizeof(T) / 16);
+        for (int e = threadIdx.x; e < n1 + n2 + n3; e += blockDim.x)
+            dst[e] = e < n1 ? s1[e] : (e < n1 + n2 ? s2[e - n1] : s3[e - n1 - n2]);
     }
     for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
     if (lane == 0)
@@ -71,7 +77,9 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     const int h1step = P.vf_off >= 0 ? I1p : 0;      // H_{0,1} is a factor (not the kept pair)
     const T* h1 = hres + ebc;                         // H_{0,1} block or the ones column
     const T* h2 = hres + P.hres_elems + ebc;          // H_{0,r0} block
+    const T* h3 = hres + P.hres_elems + P.hres2_elems + ebc;  // fused: H_{0,1} block
     const uint32_t rowbytes = (uint32_t)(I1p * sizeof(T));
+    double n0 = 0.0, n1 = 0.0, n2 = 0.0;  // fused: ‖ΔX‖², ‖X‖², ‖X_new − t‖²
 
     // stages = positions q = vb·FR + r (r in odometer order, r0 fastest); warp range [q0, q1)
     const int q0 = group * (int)(P.L / F);
@@ -189,6 +197,9 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
         }
         __syncwarp();
         const T* h2run = h2 + (int64_t)ridx[0] * I1p;
+        const int64_t fib0 = kFused ? decode(q, vb, b0, nvalid, ridx) : 0;  // fused: X address
+        const int fstep = (int)P.fstride[P.rmode[0]];
+        T q0 = T(0), q1 = T(0), q2 = T(0);
         for (int t = 0; t < rl; ++t) {
             const int s = (int)(cn & (uint32_t)(D - 1));
             mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
@@ -206,7 +217,18 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
                     lds_vec<T, EPL>(h1 + (b0 + f) * h1step, h);
                     weight<T, EPL>(wr, h, sfv[f * RL + t], w);
                     lds_vec<T, EPL>(sx + f * SR + eb, x);
-                    accumulate<T, EPL>(w, x, sb[st], sw[st]);
+                    if constexpr (kFused) {
+                        T h01[EPL], tt[EPL], xn[EPL];
+                        lds_vec<T, EPL>(h3 + (b0 + f) * I1p, h01);
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) tt[e] = w[e] * h01[e];
+                        const int64_t ge = (fib0 + (int64_t)t * fstep + f) * I1p + eb;
+                        refill_chunk<T, EPL>(x, tt, mask_bits(P.mask, ge), P.rho, P.inv1p, xn, q0, q1, q2);
+                        store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
+                        accumulate<T, EPL>(w, xn, sb[st], sw[st]);
+                    } else {
+                        accumulate<T, EPL>(w, x, sb[st], sw[st]);
+                    }
                 }
             }
             __syncwarp();
@@ -214,14 +236,18 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
             if (lane == 0) produce();
         }
         __syncwarp();  // sfv is rewritten by the next tile
+        if constexpr (kFused) {
+            n0 += (double)q0;
+            n1 += (double)q1;
+            n2 += (double)q2;
+        }
         q += rl;
-        (void)fstep;
         if (q >= seg_end) {  // kept block finished (or range end): flush its F values
 #pragma unroll
             for (int st = 0; st < NS; ++st) {
                 const int f = st * FP + fsub;
                 const int64_t slot = ((int64_t)group + vb) * F + f;
-                if constexpr (MODE == PASS_KEPT1) {
+                if constexpr (MODE == PASS_KEPT1 || kFused) {
                     if (f < nvalid) {
                         T* pbd = P.part_b + slot * P.Lv + eb;
                         T* pwd = P.part_w + slot * P.Lv + eb;
@@ -257,6 +283,19 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
 #pragma unroll
                 for (int e = 0; e < EPL; ++e) sb[st][e] = sw[st][e] = T(0);
             }
+        }
+    }
+    if constexpr (kFused) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+            n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        }
+        if (lane == 0) {
+            P.norms[(int64_t)group * 3 + 0] = n0;
+            P.norms[(int64_t)group * 3 + 1] = n1;
+            P.norms[(int64_t)group * 3 + 2] = n2;
         }
     }
 }

@@ -96,6 +96,39 @@ __device__ __forceinline__ void accumulate(const T (&w)[N], const T (&x)[N], T (
     }
 }
 
+// Eq. 9 on EPL entries (reading R1: per-entry prox minimiser), with the norm accumulators of
+// the stop test and the objective: q0 += (x_new − x)², q1 += x², q2 += (x_new − t)².
+template <typename T, int N>
+__device__ __forceinline__ void refill_chunk(const T (&x)[N], const T (&t)[N], uint32_t bits, T rho,
+                                             T inv1p, T (&xn)[N], T& q0, T& q1, T& q2) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+        const bool obs = (bits >> e) & 1u;
+        xn[e] = obs ? x[e] : (t[e] + rho * x[e]) * inv1p;
+        const T d = xn[e] - x[e];
+        const T g = xn[e] - t[e];
+        q0 = fma(d, d, q0);
+        q1 = fma(x[e], x[e], q1);
+        q2 = fma(g, g, q2);
+    }
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void store_chunk(T* dst, const T (&v)[N], bool full, const bool (&ev)[N]) {
+    if (full) {
+        stg_vec<T, N>(dst, v);
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e)
+            if (ev[e]) dst[e] = v[e];
+    }
+}
+
+__device__ __forceinline__ uint32_t mask_bits(const uint32_t* mask, int64_t ge) {
+    const uint32_t* mw = mask + (ge >> 5);
+    return __funnelshift_r(__ldg(mw), __ldg(mw + 1), (uint32_t)(ge & 31));
+}
+
 // Fibre walker: positions pos = v·FR + r of one warp's range, cut into runs (consecutive
 // fibres differing only in i_{r0}, at most sf_cap long).  32-bit index arithmetic
 // (nfib < 2^31 is checked on the host).
@@ -169,7 +202,11 @@ __device__ __forceinline__ bool walker_next(Walker& w, const PassParams<T>& P) {
 
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
-    constexpr bool kContract = (MODE == PASS_KEPT1 || MODE == PASS_RED1);
+    // PASS_FUSED = the a5 refill of sweep s fused with the a2 contraction of block (0,1) of
+    // sweep s+1 (same G): X is read once and written once for both.
+    constexpr bool kFused = (MODE == PASS_FUSED);
+    constexpr bool kContract = (MODE == PASS_KEPT1 || MODE == PASS_RED1 || kFused);
+    constexpr bool kNorms = (MODE == PASS_REFILL || MODE == PASS_OBJ || kFused);
     constexpr bool kLoadX = (MODE != PASS_MODEL);
     using Cfg = PassCfg<T, EPL, LPF, HRES, kLoadX>;
     constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR, NROW = Cfg::NROW;
@@ -311,6 +348,12 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
         __syncwarp();
         const int64_t ebase = (int64_t)C.fib * I1p;
         const T* hrun = hres + (HRES && has_fast ? ri0 * I1p : 0) + ebc;
+        T h01v[EPL];  // fused: the excluded pair's column H_{0,1}(·, i_1) completes t = M·H_{0,1}
+        if constexpr (kFused) {
+            const T* hb = Hb + P.h01_off + (int64_t)idx[1] * I1p + eb;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) h01v[e] = ev[e] ? hb[e] : T(0);
+        }
 
         T q0 = T(0), q1 = T(0), q2 = T(0);
         for (int off = 0; off < len; off += F) {
@@ -328,7 +371,16 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                     if constexpr (HRES) lds_vec<T, EPL>(hrun + (off + f) * hstep, h);
                     else lds_vec<T, EPL>(sh + f * SR + eb, h);
                     weight<T, EPL>(ws, h, sf, w);
-                    if constexpr (kContract) {
+                    if constexpr (kFused) {
+                        T x[EPL], t[EPL], xn[EPL];
+                        lds_vec<T, EPL>(sx + f * SR + eb, x);
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) t[e] = w[e] * h01v[e];
+                        const int64_t ge = ebase + (int64_t)(off + f) * xstep + eb;
+                        refill_chunk<T, EPL>(x, t, mask_bits(P.mask, ge), P.rho, P.inv1p, xn, q0, q1, q2);
+                        store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
+                        accumulate<T, EPL>(w, xn, sb, sw);
+                    } else if constexpr (kContract) {
                         T x[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
                         accumulate<T, EPL>(w, x, sb, sw);
@@ -336,26 +388,8 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                         T x[EPL], xn[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
                         const int64_t ge = ebase + (int64_t)(off + f) * xstep + eb;
-                        const uint32_t* mw = P.mask + (ge >> 5);
-                        const uint32_t bits = __funnelshift_r(__ldg(mw), __ldg(mw + 1), (uint32_t)(ge & 31));
-#pragma unroll
-                        for (int e = 0; e < EPL; ++e) {
-                            const bool obs = (bits >> e) & 1u;
-                            xn[e] = obs ? x[e] : (w[e] + P.rho * x[e]) * P.inv1p;
-                            const T d = xn[e] - x[e];
-                            const T g = xn[e] - w[e];
-                            q0 = fma(d, d, q0);
-                            q1 = fma(x[e], x[e], q1);
-                            q2 = fma(g, g, q2);
-                        }
-                        T* dst = P.Xw + ge;
-                        if (lane_full) {
-                            stg_vec<T, EPL>(dst, xn);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < EPL; ++e)
-                                if (ev[e]) dst[e] = xn[e];
-                        }
+                        refill_chunk<T, EPL>(x, w, mask_bits(P.mask, ge), P.rho, P.inv1p, xn, q0, q1, q2);
+                        store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
                     } else if constexpr (MODE == PASS_OBJ) {
                         T x[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
@@ -376,7 +410,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
             ++cn;
             if (lane == 0) produce();
         }
-        if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
+        if constexpr (kNorms) {
             n0 += (double)q0;
             n1 += (double)q1;
             n2 += (double)q2;
@@ -384,7 +418,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
         __syncwarp();  // sfv is rewritten by the next run
         // ---- flush the segment's partials into slot group + v ---------------------------
         if (C.seg_last) {
-            if constexpr (MODE == PASS_KEPT1) {
+            if constexpr (MODE == PASS_KEPT1 || kFused) {
                 // lanes serving the same mode-1 positions in different step fibres: sum them
 #pragma unroll
                 for (int o = 16; o >= LPF; o >>= 1)
@@ -428,7 +462,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
             }
         }
     }
-    if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ) {
+    if constexpr (kNorms) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             n0 += __shfl_xor_sync(0xffffffffu, n0, o);

@@ -52,6 +52,7 @@ static int pow2ceil(int x) {
 
 constexpr int64_t kGroupBoundThreads = 160LL * 2048;  // ≥ resident threads of any B200 part
 constexpr unsigned kFlagNoVBlock = IFCTN_FLAG_NO_VBLOCK;
+constexpr unsigned kFlagNoFuse = IFCTN_FLAG_NO_FUSE;
 
 // ------------------------------------------------------------------------------------------
 // Shape: everything derivable from the arguments alone (no device needed).
@@ -303,6 +304,7 @@ struct PassPlan {
 template <typename T>
 struct BlockPlan {
     int k = 0, i = 0;
+    bool vblk = false;
     PassPlan<T> pass;
     ReduceParams<T> red;
     dim3 red_grid;
@@ -324,7 +326,7 @@ static PassKernel pk() {
     using Cfg = PassCfg<T, EPL, LPF, HRES, (MODE % 100) != PASS_MODEL>;
     if constexpr (MODE >= 100) {
         constexpr int M = MODE - 100;
-        if constexpr ((M == PASS_KEPT1 || M == PASS_RED1) && HRES)
+        if constexpr ((M == PASS_KEPT1 || M == PASS_RED1 || M == PASS_FUSED) && HRES)
             return {(const void*)fiber_pass_vb<T, M, EPL, LPF, HRES>, Cfg::RING, Cfg::F};
         return {nullptr, 0, 0};
     } else {
@@ -355,6 +357,8 @@ static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
     switch (mode) {
         case 100 + PASS_KEPT1: return pick_pass<T, 100 + PASS_KEPT1>(epl, lpf, hres);
         case 100 + PASS_RED1: return pick_pass<T, 100 + PASS_RED1>(epl, lpf, hres);
+        case 100 + PASS_FUSED: return pick_pass<T, 100 + PASS_FUSED>(epl, lpf, hres);
+        case PASS_FUSED: return pick_pass<T, PASS_FUSED>(epl, lpf, hres);
         case PASS_KEPT1: return pick_pass<T, PASS_KEPT1>(epl, lpf, hres);
         case PASS_RED1: return pick_pass<T, PASS_RED1>(epl, lpf, hres);
         case PASS_REFILL: return pick_pass<T, PASS_REFILL>(epl, lpf, hres);
@@ -399,16 +403,19 @@ struct Solver : SolverBase {
     int* hflags = nullptr;    // pinned
     std::vector<BlockPlan<T>> blocks;
     PassPlan<T> refill, obj, model;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t gexec = nullptr;
+    PassPlan<T> fused;          // a5 ⊕ a2(0,1), see enqueue_mid()
+    ReduceParams<T> fused_red;
+    bool has_fused = false;
+    cudaGraphExec_t gexec = nullptr;                                    // one plain sweep
+    cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
     int64_t nlaunch_sweep = 0, last_launches = 0;
     // multi-GPU (see dist.cuh notes in DESIGN.md)
     NcclLite* nccl = nullptr;
     void* comm = nullptr;
 
     ~Solver() override {
-        if (gexec) cudaGraphExecDestroy(gexec);
-        if (graph) cudaGraphDestroy(graph);
+        for (cudaGraphExec_t e : {gexec, gexec_first, gexec_mid, gexec_last})
+            if (e) cudaGraphExecDestroy(e);
         if (comm && nccl) nccl->commDestroy(comm);
         if (st) cudaStreamSynchronize(st);
         if (own_ws && ws) cudaFree(ws);
@@ -467,7 +474,8 @@ struct Solver : SolverBase {
         p.I1p = (int)s.I1p;
         p.nouter = N - 1;
         for (int m = 0; m < N; ++m) p.fstride[m] = s.fstride[m];
-        const bool contract = (mode == PASS_KEPT1 || mode == PASS_RED1);
+        const bool contract = (mode == PASS_KEPT1 || mode == PASS_RED1 || mode == PASS_FUSED);
+        if (mode == PASS_FUSED) p.h01_off = s.hoff[0][1];
         // kept outer modes (ascending), reduced outer modes
         std::vector<int> kept, red;
         for (int m = 1; m < N; ++m) {
@@ -499,7 +507,7 @@ struct Solver : SolverBase {
         p.FR = 1;
         for (int m : red) p.FR *= s.ld[m];
         p.nfib = s.nfib;
-        p.Lv = (mode == PASS_KEPT1) ? s.I1p : 1;
+        p.Lv = (mode == PASS_KEPT1 || mode == PASS_FUSED) ? s.I1p : 1;
         const int r0 = red.empty() ? -1 : red[0];
         // weight factors: every pair p<q except {k,i} when contracting
         p.vf_off = -1;
@@ -570,8 +578,9 @@ struct Solver : SolverBase {
         const bool hres = hres_elems * s.esize <= 32 * 1024;
         p.hres_src = hfac ? p.vf_off : s.ones_off;
         p.hres_elems = hres ? hres_elems : 0;
-        if (vblk) {  // second resident block: H_{0,r0}
+        if (vblk) {  // second resident block: H_{0,r0}; fused: third, H_{0,1}
             p.hres2_elems = s.I1p * s.ld[r0];
+            if (mode == PASS_FUSED) p.hres3_elems = s.I1p * s.ld[1];
             if (!hres || p.hres2_elems * s.esize > 32 * 1024) fail(IFCTN_E_STATE, "tiled pass needs resident H blocks");
         }
         // shared memory per CTA: [mbarriers][sf vectors][resident H][TMA ring per warp]
@@ -586,7 +595,7 @@ struct Solver : SolverBase {
         }
         p.sfv_off = align_up((int64_t)nwarps * 8 * 8, 128);  // ≤ 8 stage barriers per warp
         p.hres_off = align_up(p.sfv_off + (int64_t)nwarps * p.sf_cap * s.esize, 128);
-        p.stage_off = align_up(p.hres_off + (p.hres_elems + p.hres2_elems) * s.esize, 128);
+        p.stage_off = align_up(p.hres_off + (p.hres_elems + p.hres2_elems + p.hres3_elems) * s.esize, 128);
         const size_t smem = (size_t)(p.stage_off + (int64_t)nwarps * kern.ring * s.esize);
         pp.fn = kern.fn;
         if (smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "fibre-pass shared memory exceeds the device limit");
@@ -631,6 +640,7 @@ struct Solver : SolverBase {
                 b.i = i;
                 const int mode = (k == 0 || i == 0) ? PASS_KEPT1 : PASS_RED1;
                 const bool vblk = (k == 1 || i == 1) && !(flags & kFlagNoVBlock) && tile_ok(k, i);
+                b.vblk = vblk;
                 b.pass = make_pass(mode, k, i, vblk);
                 ReduceParams<T>& r = b.red;
                 r.part_b = pb;
@@ -673,6 +683,19 @@ struct Solver : SolverBase {
         obj = make_pass(PASS_OBJ, -1, -1);
         model = make_pass(PASS_MODEL, -1, -1);
         nlaunch_sweep = 3 * (int64_t)blocks.size() + 2;
+        // fused a5(s) + a2 of block (0,1) of sweep s+1 (same G, X read and written once)
+        has_fused = false;
+        if (!(flags & kFlagNoFuse) && blocks[0].k == 0 && blocks[0].i == 1) {
+            const BlockPlan<T>& b0 = blocks[0];
+            const bool vb = b0.vblk && s.I1p * s.ld[1] * s.esize <= 32 * 1024;
+            fused = make_pass(PASS_FUSED, 0, 1, vb);
+            fused_red = b0.red;
+            fused_red.FR = fused.p.FR;
+            fused_red.L = fused.p.L;
+            fused_red.VB = vb ? fused.p.nfib / (fused.p.nb0 * fused.p.kdim[1] * fused.p.FR) : 1;
+            fused_red.nb0 = vb ? fused.p.nb0 : fused_red.kdim0;
+            has_fused = true;
+        }
     }
 
     void build_all_H() {
@@ -706,6 +729,24 @@ struct Solver : SolverBase {
         for (const auto& b : blocks) enqueue_block(b);
         enqueue_xupdate();
     }
+
+    // Fused sweep sequence for a fixed sweep count (eps ≤ 0, no trace):
+    //   first = blocks of sweep 1;  mid = [a5(s-1) ⊕ a2(0,1)(s)], finaliser, rest of sweep s;
+    //   last = a5 of the final sweep.  Same arithmetic as enqueue_sweep() repeated.
+    void enqueue_first() {
+        for (const auto& b : blocks) enqueue_block(b);
+    }
+    void enqueue_mid() {
+        const BlockPlan<T>& b0 = blocks[0];
+        launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fused.p);
+        prof_mark();
+        finalize_norms<<<1, 1024, 0, st>>>(norms, fused.p.ngroups, delta, s.ndelta, scal, dflags, 0);
+        CU(cudaGetLastError());
+        launch((const void*)reduce_partials<T>, b0.red_grid, dim3(256), 0, fused_red);
+        launch(b0.sol_fn, b0.sol_grid, dim3(128), 0, b0.sol);
+        for (size_t b = 1; b < blocks.size(); ++b) enqueue_block(blocks[b]);
+    }
+    void enqueue_last() { enqueue_xupdate(); }
 
     void init(const void* observed, const uint8_t* mask, const void* G0, void* workspace,
               size_t wbytes, cudaStream_t stream) {
@@ -781,18 +822,32 @@ struct Solver : SolverBase {
         end();
     }
 
-    void capture() {
+    template <typename F>
+    cudaGraphExec_t capture_one(F&& enqueue) {
         CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue_sweep();
+            enqueue();
         } catch (...) {
-            cudaGraph_t g;
+            cudaGraph_t g = nullptr;
             cudaStreamEndCapture(st, &g);
             if (g) cudaGraphDestroy(g);
             throw;
         }
-        CU(cudaStreamEndCapture(st, &graph));
-        CU(cudaGraphInstantiate(&gexec, graph, 0));
+        cudaGraph_t g = nullptr;
+        CU(cudaStreamEndCapture(st, &g));
+        cudaGraphExec_t e = nullptr;
+        const cudaError_t err = cudaGraphInstantiate(&e, g, 0);
+        cudaGraphDestroy(g);
+        CU(err);
+        return e;
+    }
+
+    void capture() { gexec = capture_one([&] { enqueue_sweep(); }); }
+
+    void capture_fused() {
+        gexec_first = capture_one([&] { enqueue_first(); });
+        gexec_mid = capture_one([&] { enqueue_mid(); });
+        gexec_last = capture_one([&] { enqueue_last(); });
     }
 
     void check_flags_sync() {
@@ -806,10 +861,26 @@ struct Solver : SolverBase {
         if (t_max < 0) fail(IFCTN_E_ARG, "t_max must be >= 0");
         begin();
         const bool use_graph = !(flags & IFCTN_FLAG_NO_GRAPH);
-        if (use_graph && !gexec) capture();
         const bool need_sync = trace || eps > 0.0;
         int s_done = 0;
         last_launches = 0;
+        if (has_fused && !need_sync && t_max >= 2) {  // fixed sweep count: fused sequence
+            if (use_graph && !gexec_mid) capture_fused();
+            const int64_t B = (int64_t)blocks.size();
+            if (use_graph) CU(cudaGraphLaunch(gexec_first, st));
+            else enqueue_first();
+            for (int sw = 1; sw < t_max; ++sw) {
+                if (use_graph) CU(cudaGraphLaunch(gexec_mid, st));
+                else enqueue_mid();
+            }
+            if (use_graph) CU(cudaGraphLaunch(gexec_last, st));
+            else enqueue_last();
+            last_launches = 3 * B + (int64_t)(t_max - 1) * (3 * B + 1) + 2;
+            if (done) *done = t_max;
+            end();
+            return;
+        }
+        if (use_graph && !gexec) capture();
         for (int sw = 0; sw < t_max; ++sw) {
             if (use_graph) CU(cudaGraphLaunch(gexec, st));
             else enqueue_sweep();
