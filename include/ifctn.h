@@ -71,12 +71,22 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NO_FUSE 16u  /* diagnostic: never fuse a sweep's X update into the next
                                    sweep's first block (see ifctn_sweep)                      */
 
-/* Multi-GPU description (one process per GPU).  NULL or world == 1: single GPU. */
+/* Multi-GPU description (one process per GPU).  NULL or world == 1: single GPU.
+ * Sharding: X and Ω are split along the shard mode s; the factor chains
+ * G_{s,·} hold this rank's columns; every other factor is replicated.  Per block (k,i) with
+ * k ≠ s each rank projects its partial (β, ω) onto the Gram/RHS of Eq. 8 (I_k·(R(R+1)/2+R)
+ * doubles) and the partials are summed across ranks; blocks with k = s need no exchange.  */
 typedef struct {
     const void* nccl_unique_id; /* ncclUniqueId (128 bytes), identical on all ranks       */
     int rank;
     int world;
     int shard_mode;             /* 0-based; -1 = the largest mode, first on ties           */
+    /* Optional: sum across ranks on the host instead of NCCL (several ranks driven from host
+     * threads on one device in tests, or a custom transport).  Called synchronously with a
+     * host buffer of `count` doubles that must be replaced by the element-wise sum over all
+     * ranks.  NULL = NCCL (nccl_unique_id required).  Disables CUDA-graph capture.          */
+    void (*host_allreduce)(double* buf, size_t count, void* user);
+    void* user;
 } ifctn_dist;
 
 /* One row of the per-sweep trace (Algorithm 1 stop test P:L341-344, Lemma 2). */

@@ -31,9 +31,13 @@ class IfctnError(RuntimeError):
         super().__init__(f"{name}: {msg}")
 
 
+HOST_ALLREDUCE = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, ctypes.c_void_p)
+
+
 class ifctn_dist(ctypes.Structure):
     _fields_ = [("nccl_unique_id", ctypes.c_void_p), ("rank", ctypes.c_int),
-                ("world", ctypes.c_int), ("shard_mode", ctypes.c_int)]
+                ("world", ctypes.c_int), ("shard_mode", ctypes.c_int),
+                ("host_allreduce", HOST_ALLREDUCE), ("user", ctypes.c_void_p)]
 
 
 class ifctn_trace_row(ctypes.Structure):

@@ -222,6 +222,7 @@ struct SolveParams {
     double rho;
     double* delta;       // per column ‖c_new − c_old‖²
     int* flags;          // flags[0] |= 1 on a non-positive pivot
+    double* proj;        // multi-GPU: per column [Gram upper triangle, rhs] partials
 };
 
 }  // namespace ifctn

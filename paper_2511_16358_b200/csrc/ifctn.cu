@@ -311,6 +311,10 @@ struct BlockPlan {
     SolveParams<T> sol;
     dim3 sol_grid;
     const void* sol_fn = nullptr;
+    // multi-GPU, k ≠ shard mode: project → all-reduce → solve
+    bool dist = false;
+    const void* proj_fn = nullptr;
+    int64_t proj_count = 0;  // doubles summed across ranks
 };
 
 // (kernel, ring elements per warp) of one instantiated (T, MODE, EPL, LPF, HRES)
@@ -367,18 +371,25 @@ static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
     }
 }
 
-template <typename T>
-static const void* pick_solve(int R) {
+template <typename T, int SM>
+static const void* pick_solve_sm(int R) {
     switch (R) {
-        case 1: return (const void*)block_solve<T, 1>;
-        case 2: return (const void*)block_solve<T, 2>;
-        case 3: return (const void*)block_solve<T, 3>;
-        case 4: return (const void*)block_solve<T, 4>;
-        case 5: return (const void*)block_solve<T, 5>;
-        case 6: return (const void*)block_solve<T, 6>;
-        case 7: return (const void*)block_solve<T, 7>;
-        default: return (const void*)block_solve<T, 8>;
+        case 1: return (const void*)block_solve<T, 1, SM>;
+        case 2: return (const void*)block_solve<T, 2, SM>;
+        case 3: return (const void*)block_solve<T, 3, SM>;
+        case 4: return (const void*)block_solve<T, 4, SM>;
+        case 5: return (const void*)block_solve<T, 5, SM>;
+        case 6: return (const void*)block_solve<T, 6, SM>;
+        case 7: return (const void*)block_solve<T, 7, SM>;
+        default: return (const void*)block_solve<T, 8, SM>;
     }
+}
+
+template <typename T>
+static const void* pick_solve(int R, int sm = SOLVE_FULL) {
+    if (sm == SOLVE_PROJECT) return pick_solve_sm<T, SOLVE_PROJECT>(R);
+    if (sm == SOLVE_FROM_PROJ) return pick_solve_sm<T, SOLVE_FROM_PROJ>(R);
+    return pick_solve_sm<T, SOLVE_FULL>(R);
 }
 
 template <typename T>
@@ -409,6 +420,13 @@ struct Solver : SolverBase {
     cudaGraphExec_t gexec = nullptr;                                    // one plain sweep
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
     int64_t nlaunch_sweep = 0, last_launches = 0;
+    int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
+    int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
+    int64_t sh_off = 0, sh_len = 0;        // ΔG² range of the shard-mode chains
+    double* p5 = nullptr;                  // norm partials (see finalize_norms)
+    double* hred = nullptr;                // pinned host buffer for host_allreduce
+    void (*host_allreduce)(double*, size_t, void*) = nullptr;
+    void* host_user = nullptr;
     // multi-GPU (see dist.cuh notes in DESIGN.md)
     NcclLite* nccl = nullptr;
     void* comm = nullptr;
@@ -421,6 +439,7 @@ struct Solver : SolverBase {
         if (own_ws && ws) cudaFree(ws);
         if (hscal) cudaFreeHost(hscal);
         if (hflags) cudaFreeHost(hflags);
+        if (hred) cudaFreeHost(hred);
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
         if (st) cudaStreamDestroy(st);
@@ -452,6 +471,7 @@ struct Solver : SolverBase {
         prof_mark();
         void* args[] = {(void*)&p};
         CU(cudaLaunchKernel(fn, g, b, args, smem, st));
+        ++ctr;
     }
 
     // vblk: v-blocked contraction (mode 1 kept; fiber_pass_vb), else the plain walk
@@ -675,14 +695,27 @@ struct Solver : SolverBase {
                 q.rho = rho;
                 q.delta = delta + s.delta_off[k][i];
                 q.flags = dflags;
+                q.proj = proj;
                 b.sol_grid = dim3((unsigned)s.ld[k]);
-                b.sol_fn = pick_solve<T>(s.R(k, i));
+                b.dist = s.world > 1 && k != s.shard;
+                if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
+                    const int R = s.R(k, i);
+                    b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT);
+                    b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ);
+                    b.proj_count = s.ld[k] * (R * (R + 1) / 2 + R);
+                } else {
+                    b.sol_fn = pick_solve<T>(s.R(k, i));
+                }
                 blocks.push_back(b);
             }
         refill = make_pass(PASS_REFILL, -1, -1);
         obj = make_pass(PASS_OBJ, -1, -1);
         model = make_pass(PASS_MODEL, -1, -1);
         nlaunch_sweep = 3 * (int64_t)blocks.size() + 2;
+        // ΔG² of the shard-mode chains (local columns) is summed across ranks; the rest is
+        // replicated: delta layout is block order, so blocks (s, ·) are one contiguous range
+        sh_off = s.world > 1 ? s.delta_off[s.shard][s.shard == 0 ? 1 : 0] : 0;
+        sh_len = s.world > 1 ? (int64_t)(s.N - 1) * s.ld[s.shard] : 0;
         // fused a5(s) + a2 of block (0,1) of sweep s+1 (same G, X read and written once)
         has_fused = false;
         if (!(flags & kFlagNoFuse) && blocks[0].k == 0 && blocks[0].i == 1) {
@@ -713,16 +746,39 @@ struct Solver : SolverBase {
         launch((const void*)reduce_partials<T>, b.red_grid, dim3(256), 0, b.red);
     }
 
+    void enqueue_solve(const BlockPlan<T>& b) {
+        if (b.dist) {
+            launch(b.proj_fn, b.sol_grid, dim3(128), 0, b.sol);
+            allreduce_dev(proj, (size_t)b.proj_count);
+        }
+        launch(b.sol_fn, b.sol_grid, dim3(128), 0, b.sol);
+    }
+
     void enqueue_block(const BlockPlan<T>& b) {
         enqueue_contract(b);
-        launch(b.sol_fn, b.sol_grid, dim3(128), 0, b.sol);
+        enqueue_solve(b);
+    }
+
+    // norms of the pass that just ran (ngroups partials) → scal (all-reduced across ranks)
+    void enqueue_finalize(int64_t ngroups, int obj_only) {
+        prof_mark();
+        const bool multi = s.world > 1;
+        finalize_norms<<<1, 1024, 0, st>>>(norms, ngroups, delta, obj_only ? 0 : s.ndelta, sh_off, sh_len, p5,
+                                            scal, dflags, obj_only, multi ? 0 : 1);
+        CU(cudaGetLastError());
+        ++ctr;
+        if (multi) {
+            allreduce_dev(p5, 4);
+            prof_mark();
+            combine_norms<<<1, 32, 0, st>>>(p5, scal, dflags, obj_only);
+            CU(cudaGetLastError());
+            ++ctr;
+        }
     }
 
     void enqueue_xupdate() {
         launch(refill.fn, refill.grid, dim3(kPassThreads), refill.smem, refill.p);
-        prof_mark();
-        finalize_norms<<<1, 1024, 0, st>>>(norms, refill.p.ngroups, delta, s.ndelta, scal, dflags, 0);
-        CU(cudaGetLastError());
+        enqueue_finalize(refill.p.ngroups, 0);
     }
 
     void enqueue_sweep() {
@@ -739,11 +795,9 @@ struct Solver : SolverBase {
     void enqueue_mid() {
         const BlockPlan<T>& b0 = blocks[0];
         launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fused.p);
-        prof_mark();
-        finalize_norms<<<1, 1024, 0, st>>>(norms, fused.p.ngroups, delta, s.ndelta, scal, dflags, 0);
-        CU(cudaGetLastError());
+        enqueue_finalize(fused.p.ngroups, 0);
         launch((const void*)reduce_partials<T>, b0.red_grid, dim3(256), 0, fused_red);
-        launch(b0.sol_fn, b0.sol_grid, dim3(128), 0, b0.sol);
+        enqueue_solve(b0);
         for (size_t b = 1; b < blocks.size(); ++b) enqueue_block(blocks[b]);
     }
     void enqueue_last() { enqueue_xupdate(); }
@@ -781,6 +835,7 @@ struct Solver : SolverBase {
         delta = (double*)(ws + lay.delta);
         norms = (double*)(ws + lay.norms);
         scal = (double*)(ws + lay.scal);
+        p5 = scal + 10;  // scal[10..14]
         dflags = (int*)(ws + lay.flags);
         rsep = (double*)(ws + lay.rse);
         proj = (double*)(ws + lay.proj);
@@ -842,12 +897,20 @@ struct Solver : SolverBase {
         return e;
     }
 
-    void capture() { gexec = capture_one([&] { enqueue_sweep(); }); }
+    template <typename F>
+    cudaGraphExec_t capture_counted(F&& enqueue, int64_t& n) {
+        const int64_t c0 = ctr;
+        cudaGraphExec_t e = capture_one(enqueue);
+        n = ctr - c0;
+        return e;
+    }
+
+    void capture() { gexec = capture_counted([&] { enqueue_sweep(); }, n_full); }
 
     void capture_fused() {
-        gexec_first = capture_one([&] { enqueue_first(); });
-        gexec_mid = capture_one([&] { enqueue_mid(); });
-        gexec_last = capture_one([&] { enqueue_last(); });
+        gexec_first = capture_counted([&] { enqueue_first(); }, n_first);
+        gexec_mid = capture_counted([&] { enqueue_mid(); }, n_mid);
+        gexec_last = capture_counted([&] { enqueue_last(); }, n_last);
     }
 
     void check_flags_sync() {
@@ -860,31 +923,35 @@ struct Solver : SolverBase {
     void sweep(int t_max, double eps, int* done, ifctn_trace_row* trace) override {
         if (t_max < 0) fail(IFCTN_E_ARG, "t_max must be >= 0");
         begin();
-        const bool use_graph = !(flags & IFCTN_FLAG_NO_GRAPH);
+        // host-side all-reduce callbacks cannot live in a graph
+        const bool use_graph = !(flags & IFCTN_FLAG_NO_GRAPH) && !host_allreduce;
         const bool need_sync = trace || eps > 0.0;
         int s_done = 0;
         last_launches = 0;
+        const int64_t c0 = ctr;
         if (has_fused && !need_sync && t_max >= 2) {  // fixed sweep count: fused sequence
             if (use_graph && !gexec_mid) capture_fused();
-            const int64_t B = (int64_t)blocks.size();
-            if (use_graph) CU(cudaGraphLaunch(gexec_first, st));
-            else enqueue_first();
-            for (int sw = 1; sw < t_max; ++sw) {
-                if (use_graph) CU(cudaGraphLaunch(gexec_mid, st));
-                else enqueue_mid();
+            if (use_graph) {
+                CU(cudaGraphLaunch(gexec_first, st));
+                for (int sw = 1; sw < t_max; ++sw) CU(cudaGraphLaunch(gexec_mid, st));
+                CU(cudaGraphLaunch(gexec_last, st));
+                last_launches = n_first + (int64_t)(t_max - 1) * n_mid + n_last;
+            } else {
+                enqueue_first();
+                for (int sw = 1; sw < t_max; ++sw) enqueue_mid();
+                enqueue_last();
+                last_launches = ctr - c0;
             }
-            if (use_graph) CU(cudaGraphLaunch(gexec_last, st));
-            else enqueue_last();
-            last_launches = 3 * B + (int64_t)(t_max - 1) * (3 * B + 1) + 2;
             if (done) *done = t_max;
             end();
             return;
         }
         if (use_graph && !gexec) capture();
         for (int sw = 0; sw < t_max; ++sw) {
+            const int64_t c1 = ctr;
             if (use_graph) CU(cudaGraphLaunch(gexec, st));
             else enqueue_sweep();
-            last_launches += nlaunch_sweep;
+            last_launches += use_graph ? n_full : ctr - c1;
             ++s_done;
             if (need_sync) {
                 CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -983,7 +1050,7 @@ struct Solver : SolverBase {
         rse_partial<T><<<nb, 256, 0, st>>>(dt, X, s.I1, s.I1p, s.nloc, rsep);
         sum_pairs<<<1, 32, 0, st>>>(rsep, nb, rsep + 2 * nb);
         CU(cudaGetLastError());
-        if (comm) allreduce_doubles(rsep + 2 * nb, 2);
+        allreduce_dev(rsep + 2 * nb, 2);
         CU(cudaMemcpyAsync(hscal + 8, rsep + 2 * nb, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         if (tmp) CU(cudaFreeAsync(tmp, st));
         CU(cudaStreamSynchronize(st));
@@ -996,8 +1063,7 @@ struct Solver : SolverBase {
     double objective() override {
         begin();
         launch(obj.fn, obj.grid, dim3(kPassThreads), obj.smem, obj.p);
-        finalize_norms<<<1, 1024, 0, st>>>(norms, obj.p.ngroups, delta, 0, scal, dflags, 1);
-        CU(cudaGetLastError());
+        enqueue_finalize(obj.p.ngroups, 1);
         CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         end();
@@ -1046,7 +1112,19 @@ struct Solver : SolverBase {
         end();
     }
 
-    void allreduce_doubles(double* buf, size_t count) {
+    // In-place sum across ranks of `count` device doubles, ordered on the context's stream:
+    // NCCL all-reduce (capturable into the sweep graph), or the caller's host_allreduce.
+    void allreduce_dev(double* buf, size_t count) {
+        if (s.world <= 1) return;
+        if (host_allreduce) {
+            if (count > (size_t)s.proj_elems) fail(IFCTN_E_STATE, "all-reduce larger than the staging buffer");
+            CU(cudaMemcpyAsync(hred, buf, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            host_allreduce(hred, count, host_user);
+            CU(cudaMemcpyAsync(buf, hred, count * sizeof(double), cudaMemcpyHostToDevice, st));
+            CU(cudaStreamSynchronize(st));
+            return;
+        }
         int r = nccl->allReduce(buf, buf, count, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm, st);
         if (r != 0) fail(IFCTN_E_NCCL, std::string("ncclAllReduce: ") + nccl->errorString(r));
     }
@@ -1133,12 +1211,18 @@ ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims, const
             sv->rho = rho;
             sv->flags = flags;
             if (s.world > 1) {
-                if (!dist->nccl_unique_id) ifctn::fail(IFCTN_E_ARG, "dist->nccl_unique_id must be set when world > 1");
-                sv->nccl = ifctn::NcclLite::get();
-                if (!sv->nccl) ifctn::fail(IFCTN_E_NCCL, "libnccl.so.2 could not be loaded");
-                int r = sv->nccl->commInitRank(&sv->comm, s.world, dist->nccl_unique_id, s.rank);
-                if (r != 0) ifctn::fail(IFCTN_E_NCCL, std::string("ncclCommInitRank: ") + sv->nccl->errorString(r));
-                ifctn::fail(IFCTN_E_UNSUPPORTED, "multi-GPU sweeps are not enabled in this build yet");
+                if (dist->host_allreduce) {
+                    sv->host_allreduce = dist->host_allreduce;
+                    sv->host_user = dist->user;
+                    CU(cudaMallocHost(&sv->hred, (size_t)s.proj_elems * sizeof(double)));
+                } else {
+                    if (!dist->nccl_unique_id)
+                        ifctn::fail(IFCTN_E_ARG, "dist->nccl_unique_id (or host_allreduce) must be set when world > 1");
+                    sv->nccl = ifctn::NcclLite::get();
+                    if (!sv->nccl) ifctn::fail(IFCTN_E_NCCL, "libnccl.so.2 could not be loaded");
+                    int r = sv->nccl->commInitRank(&sv->comm, s.world, dist->nccl_unique_id, s.rank);
+                    if (r != 0) ifctn::fail(IFCTN_E_NCCL, std::string("ncclCommInitRank: ") + sv->nccl->errorString(r));
+                }
             }
             sv->init(observed, mask, init_factors, workspace, workspace_bytes, (cudaStream_t)stream);
         };

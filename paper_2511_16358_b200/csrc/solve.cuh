@@ -77,7 +77,12 @@ __device__ __forceinline__ double warp_sum(double x) {
 // ---- a3 + a4: per column j of G_{k,i} (Eq. 8) -------------------------------
 //   Gram_j = Σ_a ω(a,j) g_a g_aᵀ + ρI,  rhs_j = Σ_a β(a,j) g_a + ρ c_old,  g_a = G_{i,k}(:,a)
 //   c = Gram_j⁻¹ rhs_j by Cholesky (fp64);  then row j of H_{k,i} = cᵀ G_{i,k} (refresh).
-template <typename T, int R>
+// SM = SOLVE_FULL: all of it.  Multi-GPU (k ≠ shard mode): SOLVE_PROJECT writes
+// this rank's projected partial (Gram upper triangle, rhs) = Σ_{a local} …, the partials are
+// summed across ranks (NCCL all-reduce), then SOLVE_FROM_PROJ adds ρI, ρc_old and solves.
+enum SolveMode : int { SOLVE_FULL = 0, SOLVE_PROJECT = 1, SOLVE_FROM_PROJ = 2 };
+
+template <typename T, int R, int SM>
 __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     double acc[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
-    for (int64_t a = threadIdx.x; a < P.Ii; a += blockDim.x) {
+    for (int64_t a = threadIdx.x; a < (SM == SOLVE_FROM_PROJ ? 0 : P.Ii); a += blockDim.x) {
         const double b = P.beta[j * P.Ii + a];
         const double w = P.omega[j * P.Ii + a];
         double g[R];
@@ -102,20 +107,33 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
         for (int r = 0; r < R; ++r) acc[NG + r] += b * g[r];
     }
     const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if constexpr (SM != SOLVE_FROM_PROJ) {
 #pragma unroll
-    for (int t = 0; t < NA; ++t) {
-        const double s = warp_sum(acc[t]);
-        if (ln == 0) red[wid][t] = s;
+        for (int t = 0; t < NA; ++t) {
+            const double s = warp_sum(acc[t]);
+            if (ln == 0) red[wid][t] = s;
+        }
+        __syncthreads();
+        if constexpr (SM == SOLVE_PROJECT) {
+            if (threadIdx.x < NA) {
+                const int t = threadIdx.x;
+                P.proj[j * NA + t] = red[0][t] + red[1][t] + red[2][t] + red[3][t];
+            }
+            return;
+        }
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
+        double sum[NA];
+#pragma unroll
+        for (int t = 0; t < NA; ++t)
+            sum[t] = (SM == SOLVE_FROM_PROJ) ? P.proj[j * NA + t] : red[0][t] + red[1][t] + red[2][t] + red[3][t];
         double A[R][R], L[R][R], y[R], c[R], cold[R];
         int t = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int s = r; s < R; ++s) {
-                const double v = red[0][t] + red[1][t] + red[2][t] + red[3][t];
+                const double v = sum[t];
                 A[r][s] = v;
                 A[s][r] = v;
                 ++t;
@@ -125,7 +143,7 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
         for (int r = 0; r < R; ++r) {
             cold[r] = (double)P.Gki[j * R + r];
             A[r][r] += P.rho;
-            rhs[r] = red[0][NG + r] + red[1][NG + r] + red[2][NG + r] + red[3][NG + r] + P.rho * cold[r];
+            rhs[r] = sum[NG + r] + P.rho * cold[r];
         }
         bool ok = true;
 #pragma unroll
@@ -198,44 +216,61 @@ __global__ void pair_gram(const T* Gpq, const T* Gqp, int R, int64_t Ip, int64_t
 }
 
 // ---- per-sweep finaliser: fixed-order fp64 sums of the refill norms and ΔG² -------------
+// part5 = [‖ΔX‖², ‖X‖², ‖X_new − t‖², ΣΔG² of this rank's sharded columns, ΣΔG² of the
+// replicated blocks].  Multi-GPU: the first four are summed across ranks before combining.
+__device__ __forceinline__ void combine_into(const double* p5, double* scal, int* flags, int obj_only) {
+    if (obj_only) {
+        scal[6] = 0.5 * p5[2];
+        if (!isfinite(scal[6])) atomicOr(flags + 1, 1);
+        return;
+    }
+    const double dx2 = p5[0], x2 = p5[1], f = 0.5 * p5[2], dg2 = p5[3] + p5[4];
+    const double xn = sqrt(x2);
+    scal[0] = dx2;
+    scal[1] = x2;
+    scal[2] = f;
+    scal[3] = dg2;
+    scal[4] = sqrt(dx2) / (xn > 0.0 ? xn : 1.0);
+    scal[5] += 1.0;
+    if (!isfinite(dx2) || !isfinite(x2) || !isfinite(f) || !isfinite(dg2)) atomicOr(flags + 1, 1);
+}
+
 __global__ void __launch_bounds__(1024) finalize_norms(const double* norms, int64_t ngroups,
                                                        const double* delta, int64_t ndelta,
-                                                       double* scal, int* flags, int obj_only) {
-    __shared__ double s[4][1024];
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                                                       int64_t sh_off, int64_t sh_len, double* p5,
+                                                       double* scal, int* flags, int obj_only,
+                                                       int combine) {
+    __shared__ double s[5][1024];
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
     for (int64_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
         a0 += norms[3 * g + 0];
         a1 += norms[3 * g + 1];
         a2 += norms[3 * g + 2];
     }
     if (!obj_only)
-        for (int64_t d = threadIdx.x; d < ndelta; d += blockDim.x) a3 += delta[d];
+        for (int64_t d = threadIdx.x; d < ndelta; d += blockDim.x) {
+            if (d >= sh_off && d < sh_off + sh_len) a3 += delta[d];
+            else a4 += delta[d];
+        }
     s[0][threadIdx.x] = a0;
     s[1][threadIdx.x] = a1;
     s[2][threadIdx.x] = a2;
     s[3][threadIdx.x] = a3;
+    s[4][threadIdx.x] = a4;
     __syncthreads();
     for (int st = blockDim.x >> 1; st > 0; st >>= 1) {
         if ((int)threadIdx.x < st)
-            for (int q = 0; q < 4; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + st];
+            for (int q = 0; q < 5; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + st];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        if (obj_only) {
-            scal[6] = 0.5 * s[2][0];
-            if (!isfinite(scal[6])) atomicOr(flags + 1, 1);
-            return;
-        }
-        const double dx2 = s[0][0], x2 = s[1][0], f = 0.5 * s[2][0], dg2 = s[3][0];
-        const double xn = sqrt(x2);
-        scal[0] = dx2;
-        scal[1] = x2;
-        scal[2] = f;
-        scal[3] = dg2;
-        scal[4] = sqrt(dx2) / (xn > 0.0 ? xn : 1.0);
-        scal[5] += 1.0;
-        if (!isfinite(dx2) || !isfinite(x2) || !isfinite(f) || !isfinite(dg2)) atomicOr(flags + 1, 1);
+        for (int q = 0; q < 5; ++q) p5[q] = s[q][0];
+        if (combine) combine_into(p5, scal, flags, obj_only);
     }
+}
+
+__global__ void combine_norms(const double* p5, double* scal, int* flags, int obj_only) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) combine_into(p5, scal, flags, obj_only);
 }
 
 // ---- layout kernels ------------------------------------------------------------------------
