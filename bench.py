@@ -206,48 +206,87 @@ def time_sweeps(torch, s, K):
     return e0.elapsed_time(e1)
 
 
+def split_profile(prof, N, world, sm):
+    """ifctn_profile_sweep's launch order: per block [a2 pass, reduce, (project), solve] with
+    the projection only on ranks' blocks k ≠ shard mode; then [refill, finaliser(s)]."""
+    k2, red, sol = [], [], []
+    t = 0
+    for k in range(N):
+        for i in range(N):
+            if i == k:
+                continue
+            k2.append(prof[t])
+            red.append(prof[t + 1])
+            t += 2
+            if world > 1 and k != sm:
+                sol.append(prof[t] + prof[t + 1])
+                t += 2
+            else:
+                sol.append(prof[t])
+                t += 1
+    return k2, red, sol, prof[t], sum(prof[t + 1:])
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
+    tdist = None
     if world > 1:
-        import torch.distributed as dist
+        import torch.distributed as tdist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2511_16358_b200 import Solver
     from synth import make_config
 
     p = make_config(args.config)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    if world > 1:
-        raise SystemExit("multi-GPU sweeps are not enabled in this build")
-    obs_d, mask_d, g0_d = dev(p.observed), dev(p.mask), dev(p.G0)
     N, s_bytes = p.N, p.dtype.itemsize
     R = int(p.ranks.max())
+    sm, sb, se = 0, 0, p.dims[0]
+    mk_dist = lambda: None
+    obs, msk, g0, truth = p.observed, p.mask, p.G0, p.truth
+    if world > 1:  # shard X/Ω along the shard mode, the shard-mode chains by column (§8(e))
+        from paper_2511_16358_b200 import dist as D
+        sm, sb, se = D.shard_range(p.dims, world, rank)
+        obs = D.shard_tensor(p.observed, p.dims, sm, sb, se)
+        msk = D.shard_tensor(p.mask, p.dims, sm, sb, se)
+        truth = D.shard_tensor(p.truth, p.dims, sm, sb, se)
+        g0 = D.shard_factors(p.G0, p.dims, p.ranks, sm, sb, se)
+        uid = D.nccl_unique_id_from_torch()
+        mk_dist = lambda: D.make_dist(rank, world, -1, nccl_id=uid)
+    obs_d, mask_d, g0_d = dev(obs), dev(msk), dev(g0)
+
+    def barrier():
+        if tdist is not None:
+            tdist.barrier()
+        torch.cuda.synchronize()
 
     # warm-up on a throwaway context (graph capture, clocks up), then a fresh context so the
     # timed sweeps are sweeps 1..K of the configured run
-    warm = Solver(p.dims, p.ranks, obs_d, mask_d, g0_d, rho=p.rho)
+    warm = Solver(p.dims, p.ranks, obs_d, mask_d, g0_d, rho=p.rho, dist=mk_dist())
     warm.sweep(args.warmup)
     warm.sync()
     prof = warm.profile_sweep()
     warm.close()
     del warm
-    s = Solver(p.dims, p.ranks, obs_d, mask_d, g0_d, rho=p.rho)
+    s = Solver(p.dims, p.ranks, obs_d, mask_d, g0_d, rho=p.rho, dist=mk_dist())
+    barrier()
     with ClockSampler(torch.cuda.current_device()) as clk:
         ms = time_sweeps(torch, s, args.steps)
+    barrier()
+    if tdist is not None:  # the job's time is the slowest rank's
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
     launches = s.launch_count()
-    rse = s.rse(dev(p.truth))
+    rse = s.rse(dev(truth))
     s.close()
     del s
     sweeps_per_s = args.steps / (ms / 1e3)
 
     # per-kernel split of one sweep (CUDA events on the launching stream)
-    B = N * (N - 1)
-    k2 = [prof[3 * b] for b in range(B)]
-    red = [prof[3 * b + 1] for b in range(B)]
-    sol = [prof[3 * b + 2] for b in range(B)]
-    refill_ms, fin_ms = prof[3 * B], prof[3 * B + 1]
-    n = p.n
+    k2, red, sol, refill_ms, fin_ms = split_profile(prof, N, world, sm)
+    n = int(np.prod(obs.shape)) if world > 1 else p.n  # this rank's entries
     k2_bytes = n * s_bytes                     # algorithmic: X read once per launch
     refill_bytes = n * (2 * s_bytes) + n / 8   # X read + write, 1 mask bit
     hbm, src = peaks()
@@ -279,31 +318,37 @@ def run_ours(args):
                                      "a3a4_solve": sum(sol), "a5_refill": refill_ms,
                                      "finalize": fin_ms},
             "gpu_launches": launches, "clocks": clk.summary(), "rse_after_steps": rse}
+    if world > 1:
+        line["config"]["shard"] = {"mode": sm, "rank0_slice": [sb, se],
+                                   "exchange": "NCCL all-reduce of projected Gram/RHS partials per block k != shard mode"}
+        line["roofline"]["note"] = "per-rank a2 pass over this rank's shard"
 
     if not args.no_e2e:
-        line["e2e"] = e2e(torch, p, args.steps)
-    if not args.no_cpu:
+        line["e2e"] = e2e(torch, p, args.steps, obs, msk, g0, mk_dist, barrier, tdist)
+    if not args.no_cpu and world == 1:
         line["cpu_baseline"] = oracle_cpu_baseline(p)
-    if not args.no_extras:
+    if not args.no_extras and world == 1:
         line["other_configs"] = other_configs(torch)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if tdist is not None:
+        tdist.destroy_process_group()
     return 0
 
 
-def e2e(torch, p, K):
+def e2e(torch, p, K, obs_h, mask_h, g0_h, mk_dist, barrier, tdist):
     """Same metric through the public API from pinned HOST buffers: ifctn_create copies O,
     Ω and G⁰ host→device, K sweeps each read back their trace row (device→host), and the final
-    X is copied back to pinned host memory."""
+    X is copied back to pinned host memory.  Multi-GPU: each rank its shard; max over ranks."""
     from paper_2511_16358_b200 import IFCTN_X, Solver
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-    obs, mask, g0 = pin(p.observed), pin(p.mask), pin(p.G0)
-    out = torch.empty(p.n, dtype=torch.float32 if p.dtype == np.float32 else torch.float64).pin_memory()
+    obs, mask, g0 = pin(obs_h), pin(mask_h), pin(g0_h)
+    out = torch.empty(obs.numel(), dtype=torch.float32 if p.dtype == np.float32 else torch.float64).pin_memory()
     res = []
     for it in range(2):
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
-        s = Solver(p.dims, p.ranks, obs, mask, g0, rho=p.rho)
+        s = Solver(p.dims, p.ranks, obs, mask, g0, rho=p.rho, dist=mk_dist())
         s.sweep(K, trace=True)
         s.reconstruct(IFCTN_X, out=out)
         torch.cuda.synchronize()
@@ -311,8 +356,12 @@ def e2e(torch, p, K):
         s.close()
         del s
     el = res[-1]
-    h2d = p.observed.nbytes + p.mask.nbytes + p.G0.nbytes
-    d2h = p.observed.nbytes + K * 40
+    if tdist is not None:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        el = float(t.item())
+    h2d = obs_h.nbytes + mask_h.nbytes + g0_h.nbytes
+    d2h = obs_h.nbytes + K * 40
     return {"value": K / el, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
             "d2h_bytes_per_step": d2h / K, "seconds": el,
             "note": f"one full solve of {K} sweeps per timed iteration (create from pinned host, "

@@ -80,7 +80,8 @@ typedef struct {
     const void* nccl_unique_id; /* ncclUniqueId (128 bytes), identical on all ranks       */
     int rank;
     int world;
-    int shard_mode;             /* 0-based; -1 = the largest mode, first on ties           */
+    int shard_mode;             /* 0-based; -1 = the largest mode, the LAST on ties (keeps
+                                   mode 0, the fibre/lane mode, whole when it can)         */
     /* Optional: sum across ranks on the host instead of NCCL (several ranks driven from host
      * threads on one device in tests, or a custom transport).  Called synchronously with a
      * host buffer of `count` doubles that must be replaced by the element-wise sum over all

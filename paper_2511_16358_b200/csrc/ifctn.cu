@@ -66,6 +66,7 @@ struct Shape {
     int vw = 4;
     // distribution
     int rank = 0, world = 1, shard = 0;
+    bool dpath = false;  // distributed code path (world > 1, or a 1-rank comm / hook)
     int64_t sbegin = 0, send = 0;
     int64_t ld[MAXN] = {};  // local dims
     // layout
@@ -126,10 +127,10 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
         s.world = dist->world;
         s.rank = dist->rank;
         int sm = dist->shard_mode;
-        if (sm < 0) {
-            sm = 0;
+        if (sm < 0) {  // the largest mode; ties go to the highest index, which keeps the
+            sm = 0;    // fibre mode (mode 1, the lane dimension of every pass) whole
             for (int m = 1; m < order; ++m)
-                if (dims[m] > dims[sm]) sm = m;
+                if (dims[m] >= dims[sm]) sm = m;
         }
         if (sm >= order) fail(IFCTN_E_ARG, "shard_mode out of range");
         if (dims[sm] < dist->world) fail(IFCTN_E_SHAPE, "shard mode smaller than the world size");
@@ -138,6 +139,15 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
         s.world = 1;
         s.rank = 0;
         s.shard = 0;
+    }
+    // a single rank with a communicator (or host hook) runs the distributed code path too:
+    // projections, all-reduces (1-rank NCCL) and split finalisers — used to test the path
+    s.dpath = dist && (dist->world > 1 || dist->nccl_unique_id || dist->host_allreduce);
+    if (s.dpath && dist->world == 1) {
+        if (dist->rank != 0) fail(IFCTN_E_ARG, "dist rank out of range");
+        int sm = dist->shard_mode < 0 ? 0 : dist->shard_mode;
+        if (sm >= order) fail(IFCTN_E_ARG, "shard_mode out of range");
+        s.shard = sm;
     }
     shard_range_of(s.dims[s.shard], s.world, s.rank, &s.sbegin, &s.send);
     for (int m = 0; m < order; ++m) s.ld[m] = s.dims[m];
@@ -697,7 +707,7 @@ struct Solver : SolverBase {
                 q.flags = dflags;
                 q.proj = proj;
                 b.sol_grid = dim3((unsigned)s.ld[k]);
-                b.dist = s.world > 1 && k != s.shard;
+                b.dist = s.dpath && k != s.shard;
                 if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
                     const int R = s.R(k, i);
                     b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT);
@@ -714,8 +724,8 @@ struct Solver : SolverBase {
         nlaunch_sweep = 3 * (int64_t)blocks.size() + 2;
         // ΔG² of the shard-mode chains (local columns) is summed across ranks; the rest is
         // replicated: delta layout is block order, so blocks (s, ·) are one contiguous range
-        sh_off = s.world > 1 ? s.delta_off[s.shard][s.shard == 0 ? 1 : 0] : 0;
-        sh_len = s.world > 1 ? (int64_t)(s.N - 1) * s.ld[s.shard] : 0;
+        sh_off = s.dpath ? s.delta_off[s.shard][s.shard == 0 ? 1 : 0] : 0;
+        sh_len = s.dpath ? (int64_t)(s.N - 1) * s.ld[s.shard] : 0;
         // fused a5(s) + a2 of block (0,1) of sweep s+1 (same G, X read and written once)
         has_fused = false;
         if (!(flags & kFlagNoFuse) && blocks[0].k == 0 && blocks[0].i == 1) {
@@ -762,7 +772,7 @@ struct Solver : SolverBase {
     // norms of the pass that just ran (ngroups partials) → scal (all-reduced across ranks)
     void enqueue_finalize(int64_t ngroups, int obj_only) {
         prof_mark();
-        const bool multi = s.world > 1;
+        const bool multi = s.dpath;
         finalize_norms<<<1, 1024, 0, st>>>(norms, ngroups, delta, obj_only ? 0 : s.ndelta, sh_off, sh_len, p5,
                                             scal, dflags, obj_only, multi ? 0 : 1);
         CU(cudaGetLastError());
@@ -1115,7 +1125,7 @@ struct Solver : SolverBase {
     // In-place sum across ranks of `count` device doubles, ordered on the context's stream:
     // NCCL all-reduce (capturable into the sweep graph), or the caller's host_allreduce.
     void allreduce_dev(double* buf, size_t count) {
-        if (s.world <= 1) return;
+        if (!s.dpath) return;
         if (host_allreduce) {
             if (count > (size_t)s.proj_elems) fail(IFCTN_E_STATE, "all-reduce larger than the staging buffer");
             CU(cudaMemcpyAsync(hred, buf, count * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1210,7 +1220,7 @@ ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims, const
             sv->lay = ifctn::make_layout(s);
             sv->rho = rho;
             sv->flags = flags;
-            if (s.world > 1) {
+            if (s.dpath) {
                 if (dist->host_allreduce) {
                     sv->host_allreduce = dist->host_allreduce;
                     sv->host_user = dist->user;

@@ -127,3 +127,23 @@ def test_sharded_fused_sequence_and_rse():
     [t.join() for t in th]
     r_ref = ref.rse(dev(p.truth))
     assert abs(vals[0] - r_ref) <= 1e-6 and vals[0] == vals[1]
+
+
+@pytest.mark.parametrize("name,mode", [("C3s", 1), ("C5s", 0), ("C2", 2)])
+def test_nccl_single_rank_path_matches_single_gpu(name, mode):
+    """The NCCL code path on one GPU: a 1-rank communicator built from torch's ncclUniqueId
+    runs every projection / all-reduce / split finaliser (captured in the sweep graphs) and
+    must reproduce the single-GPU result bit for bit (1-rank all-reduce = copy)."""
+    import torch.cuda.nccl as tnccl
+
+    from paper_2511_16358_b200.dist import make_dist
+    p = make_config(name)
+    a = make_solver(p)
+    d = make_dist(0, 1, mode, nccl_id=tnccl.unique_id())
+    b = make_solver(p, dist=d)
+    for s in (a, b):
+        s.sweep(3)
+        s.sweep(2, trace=True)
+    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
+    assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
+    assert b.launch_count() > a.launch_count()  # the extra projection / combine launches ran
