@@ -309,7 +309,7 @@ def run_ours(args):
                          "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": k2_gbs / hbm,
                          "traffic": traffic,
                          "bytes_per_launch": k2_bytes, "avg_launch_ms": statistics.mean(k2),
-                         "launches_per_step": B},
+                         "launches_per_step": len(k2)},
             "refill": {"achieved": refill_gbs, "frac": refill_gbs / hbm, "ms": refill_ms,
                        "bytes": refill_bytes},
             "a2_ms_by_block": {f"{k},{i}": round(k2[b], 4) for b, (k, i) in enumerate(

@@ -188,9 +188,14 @@ struct PassParams {
     int64_t nb0;
     int64_t vf2_off, hres2_elems;  // tiled pass: resident H_{0,r0} block after H_{0,1}
     int64_t h01_off, hres3_elems;  // fused pass: H_{0,1} (global offset; resident when tiled)
-    int ntf;                       // tiled pass: scalar factors touching mode 1 or r0
-    int64_t tf_off[MAXP], tf_ld[MAXP];
-    int tf_p[MAXP], tf_q[MAXP];
+    // tiled pass: scalar factors touching mode 1 (A: H_{1,q}, q fixed in the tile), r0 (B: the
+    // sf_* lists) or both (C: H_{1,r0}, -1 when {1,r0} is the kept pair); value of an entry is
+    // H[off + idx[fix]·mul + x·inc] with x = v (A) or i_{r0} (B)
+    int nta;
+    int64_t ta_off[MAXSF], ta_mul[MAXSF], ta_inc[MAXSF];
+    int ta_fix[MAXSF];
+    int64_t tc_off, tc_ld;
+    int64_t sfv_stride;            // per-warp elements of the sf scratch
 };
 
 template <typename T>

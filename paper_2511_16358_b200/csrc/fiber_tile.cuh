@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * D;
-    T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sf_cap;
+    T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sfv_stride;
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);  // [H_{0,1} | H_{0,r0}]
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
     {
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     const int kdim0 = (int)P.kdim[0];
     const int nb0 = (int)P.nb0;
     const int rdim0 = (int)P.rdim[0];
-    const int fstep = (int)P.fstride[P.rmode[0]];
+    const int fstep0 = (int)P.fstride[P.rmode[0]];
     const int h1step = P.vf_off >= 0 ? I1p : 0;      // H_{0,1} is a factor (not the kept pair)
     const T* h1 = hres + ebc;                         // H_{0,1} block or the ones column
     const T* h2 = hres + P.hres_elems + ebc;          // H_{0,r0} block
@@ -128,7 +128,12 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
         ++pq;
         ++p_n;
         if (pq >= q1) return;
-        // advance the odometer
+        // advance the odometer (fast path: the fastest reduced index does not wrap)
+        if (p_ridx[0] + 1 < rdim0) {
+            p_ridx[0] += 1;
+            p_fib += fstep0;
+            return;
+        }
         bool wrapped = true;
 #pragma unroll
         for (int j = 0; j < MAXN; ++j) {
@@ -182,23 +187,38 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
             ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) ws[e] *= ss;
-        const int r0m = P.rmode[0];
-        for (int e = lane; e < F * rl; e += 32) {
-            const int f = e / rl, t = e - f * rl;
-            int ix[MAXN];
-#pragma unroll
-            for (int m = 0; m < MAXN; ++m) ix[m] = idx[m];
-            ix[1] = b0 + min(f, nvalid - 1);
-            ix[r0m] = ridx[0] + t;
-            T val = T(1);
-            for (int u = 0; u < P.ntf; ++u)
-                val *= Hb[P.tf_off[u] + (int64_t)ix[P.tf_q[u]] * P.tf_ld[u] + ix[P.tf_p[u]]];
-            sfv[f * RL + t] = val;
+        // scalar factors touching mode 1 or r0, factorised: sf(f,t) = A(v_f)·B(i_{r0,t})·C(v_f, i_{r0,t})
+        //   A = Π_q H_{1,q}(v, i_q), B = Π_q H_{r0,q}(i_{r0}, i_q) (q fixed in the tile),
+        //   C = H_{1,r0}(v, i_{r0}) unless {1, r0} is the kept pair.
+        T* At = sfv + P.sf_cap;
+        T* Bt = At + F;
+        if (lane < F) {
+            T a = T(1);
+            const int v = b0 + min(lane, nvalid - 1);
+            for (int u = 0; u < P.nta; ++u)
+                a *= Hb[P.ta_off[u] + (int64_t)idx[P.ta_fix[u]] * P.ta_mul[u] + (int64_t)v * P.ta_inc[u]];
+            At[lane] = a;
+        }
+        for (int t = lane; t < rl; t += 32) {
+            T b = T(1);
+            for (int u = 0; u < P.nsf; ++u)
+                b *= Hb[P.sf_off[u] + (int64_t)idx[P.sf_fixmode[u]] * P.sf_fixmul[u] + (int64_t)(ridx[0] + t) * P.sf_inc[u]];
+            Bt[t] = b;
+        }
+        __syncwarp();
+        {
+            const T* cb = P.tc_off >= 0 ? Hb + P.tc_off + (int64_t)ridx[0] * P.tc_ld + b0 : nullptr;
+            for (int e = lane; e < F * rl; e += 32) {
+                const int f = e % F, t = e / F;  // F is a power of two: shifts
+                T val = At[f] * Bt[t];
+                if (cb) val *= cb[(int64_t)t * P.tc_ld + min(f, nvalid - 1)];
+                sfv[t * F + f] = val;
+            }
         }
         __syncwarp();
         const T* h2run = h2 + (int64_t)ridx[0] * I1p;
         const int64_t fib0 = kFused ? decode(q, vb, b0, nvalid, ridx) : 0;  // fused: X address
-        const int fstep = (int)P.fstride[P.rmode[0]];
+        const int fstep = fstep0;
         T q0 = T(0), q1 = T(0), q2 = T(0);
         for (int t = 0; t < rl; ++t) {
             const int s = (int)(cn & (uint32_t)(D - 1));
@@ -215,7 +235,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
                 if (f < nvalid) {
                     T h[EPL], w[EPL], x[EPL];
                     lds_vec<T, EPL>(h1 + (b0 + f) * h1step, h);
-                    weight<T, EPL>(wr, h, sfv[f * RL + t], w);
+                    weight<T, EPL>(wr, h, sfv[t * F + f], w);
                     lds_vec<T, EPL>(sx + f * SR + eb, x);
                     if constexpr (kFused) {
                         T h01[EPL], tt[EPL], xn[EPL];

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * D;
-    T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sf_cap;
+    T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sfv_stride;
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
 
@@ -339,11 +339,27 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
 #pragma unroll
         for (int e = 0; e < EPL; ++e) ws[e] *= ss;
         const int len = C.run_len, ri0 = C.ri0;
-        for (int q = lane; q < len; q += 32) {
-            T f = T(1);
-            for (int t = 0; t < P.nsf; ++t)
-                f *= Hb[P.sf_off[t] + (int64_t)idx[P.sf_fixmode[t]] * P.sf_fixmul[t] + (int64_t)(ri0 + q) * P.sf_inc[t]];
-            sfv[q] = f;
+        {
+            // per-run bases of the fast scalar factors (registers), then 32-bit offsets
+            const T* sfb[MAXSF];
+            int sfi[MAXSF];
+#pragma unroll
+            for (int t = 0; t < MAXSF; ++t) {
+                sfb[t] = Hb;
+                sfi[t] = 0;
+                if (t < P.nsf) {
+                    sfb[t] = Hb + P.sf_off[t] + (int64_t)idx[P.sf_fixmode[t]] * P.sf_fixmul[t] +
+                             (int64_t)ri0 * P.sf_inc[t];
+                    sfi[t] = (int)P.sf_inc[t];
+                }
+            }
+            for (int q = lane; q < len; q += 32) {
+                T f = T(1);
+#pragma unroll
+                for (int t = 0; t < MAXSF; ++t)
+                    if (t < P.nsf) f *= sfb[t][q * sfi[t]];
+                sfv[q] = f;
+            }
         }
         __syncwarp();
         const int64_t ebase = (int64_t)C.fib * I1p;

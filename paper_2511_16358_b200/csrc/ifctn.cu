@@ -431,6 +431,7 @@ struct Solver : SolverBase {
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
     int64_t nlaunch_sweep = 0, last_launches = 0;
     int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
+    int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
     int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
     int64_t sh_off = 0, sh_len = 0;        // ΔG² range of the shard-mode chains
     double* p5 = nullptr;                  // norm partials (see finalize_norms)
@@ -542,6 +543,7 @@ struct Solver : SolverBase {
         // weight factors: every pair p<q except {k,i} when contracting
         p.vf_off = -1;
         p.vf2_off = -1;
+        p.tc_off = -1;
         if (vblk) {  // tiled pass (fiber_tile.cuh): fast indices are mode 1 and r0
             for (int a = 0; a < N; ++a)
                 for (int b = a + 1; b < N; ++b) {
@@ -555,12 +557,23 @@ struct Solver : SolverBase {
                             p.vs_mode[p.nvs] = b;
                             ++p.nvs;
                         }
-                    } else if (a == 1 || b == 1 || a == r0 || b == r0) {
-                        p.tf_off[p.ntf] = off;
-                        p.tf_ld[p.ntf] = s.hld[a];
-                        p.tf_p[p.ntf] = a;
-                        p.tf_q[p.ntf] = b;
-                        ++p.ntf;
+                    } else if ((a == 1 && b == r0) || (a == r0 && b == 1)) {
+                        p.tc_off = off;        // H_{1,r0}(v, i_r0) at off + i_r0·ld_1 + v
+                        p.tc_ld = s.hld[1];
+                    } else if (a == 1 || b == 1) {
+                        const int q = (a == 1) ? b : a;  // H_{1,q}(v, i_q), q > 1
+                        p.ta_off[p.nta] = off;
+                        p.ta_fix[p.nta] = q;
+                        p.ta_mul[p.nta] = s.hld[1];
+                        p.ta_inc[p.nta] = 1;
+                        ++p.nta;
+                    } else if (a == r0 || b == r0) {
+                        const int fix = (a == r0) ? b : a;
+                        p.sf_off[p.nsf] = off;
+                        p.sf_fixmode[p.nsf] = fix;
+                        p.sf_fixmul[p.nsf] = (a == r0) ? s.hld[a] : 1;
+                        p.sf_inc[p.nsf] = (a == r0) ? 1 : s.hld[a];
+                        ++p.nsf;
                     } else {
                         p.ss_off[p.nss] = off;
                         p.ss_ld[p.nss] = s.hld[a];
@@ -624,7 +637,9 @@ struct Solver : SolverBase {
             p.nfib = p.nb0 * p.kdim[1] * p.FR * F;
         }
         p.sfv_off = align_up((int64_t)nwarps * 8 * 8, 128);  // ≤ 8 stage barriers per warp
-        p.hres_off = align_up(p.sfv_off + (int64_t)nwarps * p.sf_cap * s.esize, 128);
+        // per warp: the sf table (sf_cap) + tiled-pass scratch for A (≤ 8) and B (≤ sf_cap/F)
+        p.sfv_stride = vblk ? 2 * (int64_t)p.sf_cap + 8 : p.sf_cap;
+        p.hres_off = align_up(p.sfv_off + (int64_t)nwarps * p.sfv_stride * s.esize, 128);
         p.stage_off = align_up(p.hres_off + (p.hres_elems + p.hres2_elems + p.hres3_elems) * s.esize, 128);
         const size_t smem = (size_t)(p.stage_off + (int64_t)nwarps * kern.ring * s.esize);
         pp.fn = kern.fn;
@@ -634,6 +649,7 @@ struct Solver : SolverBase {
         int nb = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pp.fn, kPassThreads, smem));
         if (nb < 1) nb = 1;
+        if (tune_ctas > 0) nb = std::min(nb, tune_ctas);
         // grid: one wave of warps ("groups"), equal fibre counts
         int64_t gmax = (int64_t)nsm * nb * nwarps;
         gmax = std::min(gmax, s.groups_bound);
@@ -821,6 +837,7 @@ struct Solver : SolverBase {
         int smo = 0;
         CU(cudaDeviceGetAttribute(&smo, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         smem_limit = (size_t)smo;
+        if (const char* e = getenv("IFCTN_TUNE_CTAS")) tune_ctas = atoi(e);  // experiments only
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
