@@ -212,6 +212,12 @@ struct ReduceParams {
     int kmode0IsK;       // RED1: kmode[0] == k
     int64_t kdim0;
     int64_t VB, nb0;     // v-blocking: block width (1 = off), blocks along kmode[0]
+    // grid = (NV, ntile, Z): CTA (v, tile, z) sums elements [tile·ET, tile·ET+ET) of v over
+    // its z-th share of the slots; Z > 1 combines the Z partials in z order in the last CTA
+    // to arrive (scr/cnt), so the sum order is fixed for a given Z.
+    int ET, ntile, Z;
+    double* scr;         // ≥ NV·ntile·Z·ET·2 doubles when Z > 1
+    unsigned* cnt;       // ≥ NV·ntile counters, zero between launches
 };
 
 template <typename T>

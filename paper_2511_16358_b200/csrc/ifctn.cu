@@ -245,8 +245,12 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
 }
 
 struct Layout {
-    int64_t x, bits, g, h, pb, pw, beta, omega, delta, norms, scal, flags, rse, proj, total;
+    int64_t x, bits, g, h, pb, pw, beta, omega, delta, norms, scal, flags, rse, proj, rscr, rcnt, total;
 };
+
+// split-slot reduce (reduce_partials with Z > 1): scratch doubles and arrival counters
+constexpr int64_t kRedScr = 2 * 2048 * 32 * 2;
+constexpr int64_t kRedCnt = 2048;
 
 static Layout make_layout(const Shape& s) {
     Layout L{};
@@ -270,6 +274,8 @@ static Layout make_layout(const Shape& s) {
     L.flags = take(4 * 4);
     L.rse = take(2 * 1024 * 8 + 16);
     L.proj = take(s.proj_elems * 8);
+    L.rscr = take(kRedScr * 8);
+    L.rcnt = take(kRedCnt * 4);
     L.total = o;
     return L;
 }
@@ -283,6 +289,21 @@ static bool is_device_ptr(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Device-addressable view of p: p itself for device/managed memory, the mapped device address
+// for pinned (page-locked) host memory — kernels then read/write it directly over the host
+// link with no staging copy — and nullptr for pageable host memory.
+static void* device_view(const void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return const_cast<void*>(p);
+    if (a.type == cudaMemoryTypeHost && a.devicePointer) return a.devicePointer;
+    return nullptr;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -311,13 +332,18 @@ struct PassPlan {
     size_t smem = 0;
 };
 
+struct RedLaunch {
+    const void* fn = nullptr;
+    dim3 grid;
+};
+
 template <typename T>
 struct BlockPlan {
     int k = 0, i = 0;
     bool vblk = false;
     PassPlan<T> pass;
     ReduceParams<T> red;
-    dim3 red_grid;
+    RedLaunch red_l;
     SolveParams<T> sol;
     dim3 sol_grid;
     const void* sol_fn = nullptr;
@@ -418,7 +444,8 @@ struct Solver : SolverBase {
     // device views
     T *X, *G, *H, *pb, *pw;
     uint32_t* bits;
-    double *beta, *omega, *delta, *norms, *scal, *rsep, *proj;
+    double *beta, *omega, *delta, *norms, *scal, *rsep, *proj, *rscr;
+    unsigned* rcnt;
     int* dflags;
     double* hscal = nullptr;  // pinned
     int* hflags = nullptr;    // pinned
@@ -426,6 +453,7 @@ struct Solver : SolverBase {
     PassPlan<T> refill, obj, model;
     PassPlan<T> fused;          // a5 ⊕ a2(0,1), see enqueue_mid()
     ReduceParams<T> fused_red;
+    RedLaunch fused_red_l;
     bool has_fused = false;
     cudaGraphExec_t gexec = nullptr;                                    // one plain sweep
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
@@ -675,6 +703,37 @@ struct Solver : SolverBase {
         return b1 <= 32 * 1024 && b2 <= 32 * 1024;
     }
 
+    // stage-2 reduce launch.  Lv = 1 with enough v to fill the GPU: a warp per v
+    // (reduce_partials_warp).  Otherwise CTAs (v, element tile of ET ≤ 32, slot share z); Z > 1
+    // only when the (v, tile) CTAs alone would leave SMs idle and every thread still sums ≥ 4
+    // slots.
+    RedLaunch split_reduce(ReduceParams<T>& r) {
+        r.scr = rscr;
+        r.cnt = rcnt;
+        r.ET = 1;
+        r.ntile = 1;
+        r.Z = 1;
+        const int64_t nslots = (r.FR * r.VB) / r.L + 2;
+        if (r.Lv == 1 && r.NV >= 16 * (int64_t)nsm && nslots <= 1024)
+            return {(const void*)reduce_partials_warp<T>, dim3((unsigned)((r.NV + 7) / 8))};
+        int ET = 1;
+        while (ET < r.Lv && ET < 32) ET <<= 1;
+        r.ET = ET;
+        r.ntile = (int)((r.Lv + ET - 1) / ET);
+        const int64_t base = r.NV * r.ntile;
+        const int64_t ny = 256 / ET;
+        int64_t Z = 1;
+        const int64_t target = 2 * (int64_t)nsm;
+        if (base < target && base <= kRedCnt) {
+            Z = (target + base - 1) / base;
+            Z = std::min(Z, std::max<int64_t>(1, nslots / (ny * 4)));
+            Z = std::min(Z, kRedScr / (base * ET * 2));
+            Z = std::max<int64_t>(1, std::min<int64_t>(Z, 64));
+        }
+        r.Z = (int)Z;
+        return {(const void*)reduce_partials<T>, dim3((unsigned)r.NV, (unsigned)r.ntile, (unsigned)Z)};
+    }
+
     void plan() {
         const int N = s.N;
         blocks.clear();
@@ -705,7 +764,7 @@ struct Solver : SolverBase {
                 r.kdim0 = b.pass.p.kdim[0];
                 r.VB = vblk ? b.pass.p.nfib / (b.pass.p.nb0 * b.pass.p.kdim[1] * b.pass.p.FR) : 1;
                 r.nb0 = vblk ? b.pass.p.nb0 : r.kdim0;
-                b.red_grid = dim3((unsigned)r.NV);
+                b.red_l = split_reduce(r);
                 SolveParams<T>& q = b.sol;
                 q.beta = beta;
                 q.omega = omega;
@@ -753,6 +812,7 @@ struct Solver : SolverBase {
             fused_red.L = fused.p.L;
             fused_red.VB = vb ? fused.p.nfib / (fused.p.nb0 * fused.p.kdim[1] * fused.p.FR) : 1;
             fused_red.nb0 = vb ? fused.p.nb0 : fused_red.kdim0;
+            fused_red_l = split_reduce(fused_red);
             has_fused = true;
         }
     }
@@ -769,7 +829,7 @@ struct Solver : SolverBase {
 
     void enqueue_contract(const BlockPlan<T>& b) {
         launch(b.pass.fn, b.pass.grid, dim3(kPassThreads), b.pass.smem, b.pass.p);
-        launch((const void*)reduce_partials<T>, b.red_grid, dim3(256), 0, b.red);
+        launch(b.red_l.fn, b.red_l.grid, dim3(256), 0, b.red);
     }
 
     void enqueue_solve(const BlockPlan<T>& b) {
@@ -822,7 +882,7 @@ struct Solver : SolverBase {
         const BlockPlan<T>& b0 = blocks[0];
         launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fused.p);
         enqueue_finalize(fused.p.ngroups, 0);
-        launch((const void*)reduce_partials<T>, b0.red_grid, dim3(256), 0, fused_red);
+        launch(fused_red_l.fn, fused_red_l.grid, dim3(256), 0, fused_red);
         enqueue_solve(b0);
         for (size_t b = 1; b < blocks.size(); ++b) enqueue_block(blocks[b]);
     }
@@ -866,28 +926,31 @@ struct Solver : SolverBase {
         dflags = (int*)(ws + lay.flags);
         rsep = (double*)(ws + lay.rse);
         proj = (double*)(ws + lay.proj);
+        rscr = (double*)(ws + lay.rscr);
+        rcnt = (unsigned*)(ws + lay.rcnt);
 
         begin();
         CU(cudaMemsetAsync(ws, 0, lay.total, st));
         // inputs → device (temporary copies when the caller passed host memory)
         const size_t obytes = (size_t)s.nloc * s.esize;
-        const T* dobs = (const T*)observed;
-        const uint8_t* dmask = mask;
+        // pinned host inputs are read in place by pack_input (one pass over the host link)
+        const T* dobs = (const T*)device_view(observed);
+        const uint8_t* dmask = (const uint8_t*)device_view(mask);
         void* tmp_o = nullptr;
         void* tmp_m = nullptr;
-        if (!is_device_ptr(observed)) {
+        if (!dobs) {
             CU(cudaMallocAsync(&tmp_o, obytes, st));
             CU(cudaMemcpyAsync(tmp_o, observed, obytes, cudaMemcpyHostToDevice, st));
             dobs = (const T*)tmp_o;
         }
-        if (!is_device_ptr(mask)) {
+        if (!dmask) {
             CU(cudaMallocAsync(&tmp_m, (size_t)s.nloc, st));
             CU(cudaMemcpyAsync(tmp_m, mask, (size_t)s.nloc, cudaMemcpyHostToDevice, st));
             dmask = (const uint8_t*)tmp_m;
         }
         const int64_t nw = (s.npad + 31) / 32;
-        pack_input<T><<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(dobs, dmask, s.I1, s.I1p, s.npad,
-                                                                    (flags & IFCTN_FLAG_X_FULL) ? 1 : 0, X, bits);
+        pack_input<T><<<(unsigned)std::min<int64_t>((nw + 7) / 8, 64 * nsm), 256, 0, st>>>(
+            dobs, dmask, s.I1, s.I1p, s.npad, (flags & IFCTN_FLAG_X_FULL) ? 1 : 0, X, bits);
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(G, G0, (size_t)s.gtotal * s.esize,
                            is_device_ptr(G0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -1030,26 +1093,32 @@ struct Solver : SolverBase {
         if (what != IFCTN_MODEL && what != IFCTN_X) fail(IFCTN_E_ARG, "what must be IFCTN_MODEL or IFCTN_X");
         begin();
         const size_t bytes = (size_t)s.nloc * s.esize;
-        const bool dev = is_device_ptr(out);
-        T* dout = (T*)out;
-        void* tmp = nullptr;
-        if (!dev) {
-            CU(cudaMallocAsync(&tmp, bytes, st));
-            dout = (T*)tmp;
-        }
-        if (what == IFCTN_X) {
-            unpack_x<T><<<(unsigned)((s.nloc + 255) / 256), 256, 0, st>>>(X, s.I1, s.I1p, s.nloc, dout);
-            CU(cudaGetLastError());
+        const bool host = !is_device_ptr(out);
+        if (what == IFCTN_X && s.I1 == s.I1p) {
+            // unpadded fibres: X already is the natural layout, one copy
+            CU(cudaMemcpyAsync(out, X, bytes, cudaMemcpyDefault, st));
         } else {
-            PassParams<T> p = model.p;
-            p.out = dout;
-            launch(model.fn, model.grid, dim3(kPassThreads), model.smem, p);
+            // device or pinned host out: written in place by the kernel; pageable: staged
+            T* dout = (T*)device_view(out);
+            void* tmp = nullptr;
+            if (!dout) {
+                CU(cudaMallocAsync(&tmp, bytes, st));
+                dout = (T*)tmp;
+            }
+            if (what == IFCTN_X) {
+                unpack_x<T><<<(unsigned)((s.nloc + 255) / 256), 256, 0, st>>>(X, s.I1, s.I1p, s.nloc, dout);
+                CU(cudaGetLastError());
+            } else {
+                PassParams<T> p = model.p;
+                p.out = dout;
+                launch(model.fn, model.grid, dim3(kPassThreads), model.smem, p);
+            }
+            if (tmp) {
+                CU(cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, st));
+                CU(cudaFreeAsync(tmp, st));
+            }
         }
-        if (!dev) {
-            CU(cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, st));
-            CU(cudaFreeAsync(tmp, st));
-            CU(cudaStreamSynchronize(st));
-        }
+        if (host) CU(cudaStreamSynchronize(st));
         end();
     }
 
@@ -1066,9 +1135,9 @@ struct Solver : SolverBase {
         if (!truth) fail(IFCTN_E_ARG, "truth must not be NULL");
         begin();
         const size_t bytes = (size_t)s.nloc * s.esize;
-        const T* dt = (const T*)truth;
+        const T* dt = (const T*)device_view(truth);
         void* tmp = nullptr;
-        if (!is_device_ptr(truth)) {
+        if (!dt) {
             CU(cudaMallocAsync(&tmp, bytes, st));
             CU(cudaMemcpyAsync(tmp, truth, bytes, cudaMemcpyHostToDevice, st));
             dt = (const T*)tmp;

@@ -8,63 +8,136 @@ namespace ifctn {
 
 // ---- stage 2 of a2: fixed-order fp64 sum of the partial slots of every kept value v ------
 // Slots of v are g + v for g in [⌊vFR/L⌋, ⌊((v+1)FR−1)/L⌋] (each group covers L fibres).
+// v-blocking (fiber_pass_vb): v = (kidx0, kidx1) lies in block vb at offset vv; the warps that
+// covered block vb are g0..g1 and their slot of v is (g + vb)·VB + vv.  VB = 1 is the plain
+// layout (vb = v).  Returns the element offset of (v, first slot, e = 0) and the slot count.
 template <typename T>
-__global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
-    __shared__ double sb[256], sw[256];
-    const int64_t v = blockIdx.x;
-    // v-blocking (fiber_pass_vb): v = (kidx0, kidx1) lies in block vb at offset vv; the warps
-    // that covered block vb are g0..g1 and their slot of v is (g + vb)·VB + vv.  VB = 1 is the
-    // plain layout (vb = v).
+__device__ __forceinline__ int64_t slot_base(const ReduceParams<T>& P, int64_t v, int64_t& nslots) {
     const int64_t kx0 = v % P.kdim0, kx1 = v / P.kdim0;
     const int64_t vb = kx0 / P.VB + P.nb0 * kx1, vv = kx0 % P.VB;
     const int64_t g0 = (vb * P.FR * P.VB) / P.L;
     const int64_t g1 = ((vb + 1) * P.FR * P.VB - 1) / P.L;
-    const int64_t nslots = g1 - g0 + 1;
-    const int ex = (int)(P.Lv < 256 ? P.Lv : 256);
-    // round ex up to a power of two so the y-split is a clean tree
-    int exp2 = 1;
-    while (exp2 < ex) exp2 <<= 1;
-    const int ny = 256 / exp2;
-    const int tx = threadIdx.x % exp2;
-    const int ty = threadIdx.x / exp2;
-    for (int64_t e0 = 0; e0 < P.Lv; e0 += exp2) {
-        const int64_t e = e0 + tx;
-        double b = 0.0, w = 0.0;
-        if (e < P.Lv) {
-            for (int64_t s = ty; s < nslots; s += ny) {
-                const int64_t o = ((g0 + s + vb) * P.VB + vv) * P.Lv + e;
-                b += (double)P.part_b[o];
-                w += (double)P.part_w[o];
-            }
+    nslots = g1 - g0 + 1;
+    return ((g0 + vb) * P.VB + vv) * P.Lv;
+}
+
+// β/ω destination of (v, e); −1 for the padding rows of mode 1
+template <typename T>
+__device__ __forceinline__ int64_t out_index(const ReduceParams<T>& P, int64_t v, int64_t e) {
+    if (P.kept1) {
+        if (e >= P.I1) return -1;
+        return P.kIsMode0 ? (e * P.Ii + v) : (v * P.Ii + e);
+    }
+    const int64_t x0 = v % P.kdim0, x1 = v / P.kdim0;  // kmode[0], kmode[1] indices
+    const int64_t j = P.kmode0IsK ? x0 : x1;
+    const int64_t a = P.kmode0IsK ? x1 : x0;
+    return j * P.Ii + a;
+}
+
+// Lv = 1 (RED1 blocks, many v with few slots each): one warp per v, lanes stride the slots,
+// butterfly sum (fixed order).
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T> P) {
+    const int64_t v = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (v >= P.NV) return;
+    const int lane = threadIdx.x & 31;
+    int64_t nslots;
+    const int64_t base = slot_base(P, v, nslots);
+    const int64_t stride = P.VB;  // Lv = 1: consecutive slots are VB elements apart
+    double b = 0.0, w = 0.0;
+    for (int64_t s = lane; s < nslots; s += 32) {
+        b += (double)P.part_b[base + s * stride];
+        w += (double)P.part_w[base + s * stride];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+        w += __shfl_xor_sync(0xffffffffu, w, off);
+    }
+    if (lane == 0) {
+        const int64_t o = out_index(P, v, 0);
+        if (o >= 0) {
+            P.beta[o] = b;
+            P.omega[o] = w;
         }
-        sb[threadIdx.x] = b;
-        sw[threadIdx.x] = w;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
+    __shared__ double sb[256], sw[256];
+    const int64_t v = blockIdx.x;
+    int64_t nslots;
+    const int64_t base = slot_base(P, v, nslots);
+    // this CTA: elements e = tile·ET + tx, slots [s0, s1) split over ny = 256/ET thread rows
+    const int ET = P.ET, ny = 256 / ET;
+    const int tx = threadIdx.x % ET, ty = threadIdx.x / ET;
+    const int z = blockIdx.z;
+    const int64_t chunk = (nslots + P.Z - 1) / P.Z;
+    const int64_t s0 = z * chunk, s1 = min(nslots, s0 + chunk);
+    const int64_t e = (int64_t)blockIdx.y * ET + tx;
+    double b = 0.0, w = 0.0;
+    if (e < P.Lv) {
+        const int64_t stride = (int64_t)ny * P.VB * P.Lv;
+        int64_t o = base + (s0 + ty) * P.VB * P.Lv + e;
+        int64_t s = s0 + ty;
+        // 4 independent loads in flight per thread; the adds stay in slot order
+        for (; s + 3 * ny < s1; s += 4 * ny, o += 4 * stride) {
+            const T b0 = P.part_b[o], b1 = P.part_b[o + stride], b2 = P.part_b[o + 2 * stride],
+                    b3 = P.part_b[o + 3 * stride];
+            const T w0 = P.part_w[o], w1 = P.part_w[o + stride], w2 = P.part_w[o + 2 * stride],
+                    w3 = P.part_w[o + 3 * stride];
+            b += (double)b0; b += (double)b1; b += (double)b2; b += (double)b3;
+            w += (double)w0; w += (double)w1; w += (double)w2; w += (double)w3;
+        }
+        for (; s < s1; s += ny, o += stride) {
+            b += (double)P.part_b[o];
+            w += (double)P.part_w[o];
+        }
+    }
+    sb[threadIdx.x] = b;
+    sw[threadIdx.x] = w;
+    __syncthreads();
+    for (int st = ny >> 1; st > 0; st >>= 1) {
+        if (ty < st) {
+            sb[threadIdx.x] += sb[threadIdx.x + st * ET];
+            sw[threadIdx.x] += sw[threadIdx.x + st * ET];
+        }
         __syncthreads();
-        for (int st = ny >> 1; st > 0; st >>= 1) {
-            if (ty < st) {
-                sb[threadIdx.x] += sb[threadIdx.x + st * exp2];
-                sw[threadIdx.x] += sw[threadIdx.x + st * exp2];
-            }
-            __syncthreads();
+    }
+    if (P.Z > 1) {
+        // publish this z-share, last CTA of (v, tile) to arrive sums the Z shares in z order
+        const int64_t id = (int64_t)blockIdx.y * P.NV + v;
+        double* my = P.scr + ((id * P.Z + z) * ET) * 2;
+        if (ty == 0) {
+            my[2 * tx] = sb[tx];
+            my[2 * tx + 1] = sw[tx];
         }
-        if (ty == 0 && e < P.Lv) {
-            int64_t out;
-            bool write = true;
-            if (P.kept1) {
-                if (e >= P.I1) write = false;
-                out = P.kIsMode0 ? (e * P.Ii + v) : (v * P.Ii + e);
-            } else {
-                const int64_t x0 = v % P.kdim0, x1 = v / P.kdim0;  // kmode[0], kmode[1] indices
-                const int64_t j = P.kmode0IsK ? x0 : x1;
-                const int64_t a = P.kmode0IsK ? x1 : x0;
-                out = j * P.Ii + a;
-            }
-            if (write) {
-                P.beta[out] = sb[threadIdx.x];
-                P.omega[out] = sw[threadIdx.x];
-            }
-        }
+        __threadfence();
         __syncthreads();
+        __shared__ unsigned last;
+        if (threadIdx.x == 0) last = (atomicAdd(P.cnt + id, 1u) == (unsigned)(P.Z - 1));
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        if (ty == 0) {
+            double bb = 0.0, ww = 0.0;
+            const double* p = P.scr + id * P.Z * ET * 2 + 2 * tx;
+            for (int zz = 0; zz < P.Z; ++zz) {
+                bb += __ldcg(p + zz * ET * 2);
+                ww += __ldcg(p + zz * ET * 2 + 1);
+            }
+            sb[tx] = bb;
+            sw[tx] = ww;
+        }
+        if (threadIdx.x == 0) P.cnt[id] = 0u;
+    }
+    if (ty == 0 && e < P.Lv) {
+        const int64_t o = out_index(P, v, e);
+        if (o >= 0) {
+            P.beta[o] = sb[tx];
+            P.omega[o] = sw[tx];
+        }
     }
 }
 
@@ -278,28 +351,27 @@ __global__ void combine_norms(const double* p5, double* scal, int* flags, int ob
 template <typename T>
 __global__ void pack_input(const T* obs, const uint8_t* mask, int64_t I1, int64_t I1p,
                            int64_t npad, int xfull, T* X, uint32_t* bits) {
-    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t e0 = w * 32;
-    if (e0 >= npad) return;
-    uint32_t b = 0;
-    for (int t = 0; t < 32; ++t) {
-        const int64_t e = e0 + t;
-        if (e >= npad) {
-            b |= 1u << t;
-            continue;
-        }
-        const int64_t f = e / I1p, i1 = e - f * I1p;
+    // one warp per 32-element mask word: lane t loads element 32w + t (coalesced, so pinned
+    // host inputs stream well over the host link) and the ballot is the word
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (npad + 31) / 32;
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nw; w += wstride) {
+        const int64_t e = w * 32 + lane;
         T x = T(0);
-        uint32_t m = 1;
-        if (i1 < I1) {
-            const int64_t u = f * I1 + i1;
-            m = mask[u] != 0;
-            x = (m || xfull) ? obs[u] : T(0);
+        bool m = true;
+        if (e < npad) {
+            const int64_t f = e / I1p, i1 = e - f * I1p;
+            if (i1 < I1) {
+                const int64_t u = f * I1 + i1;
+                m = mask[u] != 0;
+                x = (m || xfull) ? obs[u] : T(0);
+            }
+            X[e] = x;
         }
-        X[e] = x;
-        b |= m << t;
+        const uint32_t b = __ballot_sync(0xffffffffu, m);
+        if (lane == 0) bits[w] = b;
     }
-    bits[w] = b;
 }
 
 template <typename T>

@@ -48,6 +48,28 @@ def test_host_and_device_inputs_agree():
     assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
 
 
+@pytest.mark.parametrize("name", ["C2s", "C4s"])   # mode-1 fibres unpadded / padded (I1p > I1)
+def test_pinned_host_inputs_and_outputs(name):
+    """Pinned host buffers are read / written in place by the kernels (zero-copy), pageable
+    ones are staged: both must give the device-buffer result bit for bit."""
+    from paper_2511_16358_b200 import IFCTN_MODEL, IFCTN_X, Solver
+    p = make_config(name)
+    a = make_solver(p)
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+    b = Solver(p.dims, p.ranks, pin(p.observed), pin(p.mask), pin(p.G0), rho=p.rho)
+    for s in (a, b):
+        s.sweep(2)
+    for what in (IFCTN_X, IFCTN_MODEL):
+        ref = a.reconstruct(what).cpu().numpy()
+        out_pin = torch.empty(p.n, dtype=torch.from_numpy(ref[:1]).dtype).pin_memory()
+        out_pag = np.empty_like(ref)
+        b.reconstruct(what, out=out_pin)
+        b.reconstruct(what, out=out_pag)
+        assert np.array_equal(out_pin.numpy().view(np.uint8), ref.view(np.uint8))
+        assert np.array_equal(out_pag.view(np.uint8), ref.view(np.uint8))
+    assert a.rse(dev(p.truth)) == b.rse(pin(p.truth)) == b.rse(np.ascontiguousarray(p.truth))
+
+
 # ------------------------------------------------------------------ model t (a1 + a5) ---
 
 @pytest.mark.parametrize("name", SMALL + ["C2"])
