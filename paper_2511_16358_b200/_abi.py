@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libifctn.so")
+# IFCTN_LIB: an experiment build of the same library (scripts/variants.sh), never a fallback
+LIB_PATH = os.environ.get("IFCTN_LIB") or os.path.join(_HERE, "libifctn.so")
 
 IFCTN_F32, IFCTN_F64 = 0, 1
 IFCTN_MODEL, IFCTN_X = 0, 1

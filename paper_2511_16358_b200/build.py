@@ -23,20 +23,24 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """Compile libifctn.so.  `out`/`defines` build experiment variants (scripts/variants.sh)."""
+    if out == OUT and not defines and not force and not needs_build():
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [nvcc] + NVCC_FLAGS + ["-o", tmp, SRC, "-ldl"]
+    tmp = out + f".tmp{os.getpid()}"
+    cmd = [nvcc] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", tmp, SRC, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    outs = [a[6:] for a in args if a.startswith("--out=")]
+    print(build(force="--force" in args, verbose=True, out=outs[0] if outs else OUT, defines=defs))

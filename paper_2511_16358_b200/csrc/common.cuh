@@ -18,7 +18,10 @@ constexpr int kPassMinBlocks = 2;              // ≤ 128 registers: ≥ 16 warp
 // Compile-time shape of one fibre-pass instance (fiber_pass.cuh): EPL mode-1 positions per
 // lane, LPF lanes per fibre (FP = 32/LPF fibres per warp step), ring rows per fibre (X and,
 // without a resident H block, the H column), F fibres per TMA stage (≈ 2 KB), D stages.
-template <typename T, int EPL, int LPF, bool HRES, bool LOADX>
+// MASK (refill passes): each stage also carries the Ω bit words of its fibres, MWF 32-bit
+// words per fibre slot (16-B aligned copies that cover the fibre's bits plus the funnel
+// word), or the whole stage's bits in one copy when its fibres are contiguous.
+template <typename T, int EPL, int LPF, bool HRES, bool LOADX, bool MASK = false>
 struct PassCfg {
     static constexpr int FP = 32 / LPF;
     static constexpr int SR = LPF * EPL;  // shared-memory row stride (elements)
@@ -27,7 +30,11 @@ struct PassCfg {
     static constexpr int FK = (2048 / (NROW > 0 ? NROW : 1) / ROWB) / FP;
     static constexpr int F = FP * (FK > 1 ? FK : 1);
     static constexpr int D = 4;
-    static constexpr int RING = D * NROW * F * SR;  // ring elements per warp
+    static constexpr int XH = NROW * F * SR;                       // X/H elements per stage
+    static constexpr int MWF = MASK ? ((SR / 32 + 9 + 3) & ~3) : 0;  // mask words per fibre
+    static constexpr int MW = F * MWF;                             // mask words per stage
+    static constexpr int STAGE = XH + MW * 4 / (int)sizeof(T);     // elements per stage
+    static constexpr int RING = D * STAGE;                         // ring elements per warp
 };
 
 enum PassMode : int {
@@ -88,6 +95,14 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Before a TMA refills a ring slot the consumers only READ (their loads have retired: the
+// values were used before the __syncwarp that precedes the refill), so no proxy fence is
+// needed there; IFCTN_STAGE_FENCE restores it for experiments.
+__device__ __forceinline__ void fence_stage_refill() {
+#ifdef IFCTN_STAGE_FENCE
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -128,6 +143,15 @@ __device__ __forceinline__ void tma_g2s_a(uint32_t dst, const void* src, uint32_
 __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
     uint32_t done;
     do {
+#ifdef IFCTN_SPIN_WAIT
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+#else
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -135,6 +159,7 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
             : "=r"(done)
             : "r"(bar), "r"(parity), "r"(1000000u)
             : "memory");
+#endif
     } while (!done);
 }
 
@@ -196,6 +221,7 @@ struct PassParams {
     int ta_fix[MAXSF];
     int64_t tc_off, tc_ld;
     int64_t sfv_stride;            // per-warp elements of the sf scratch
+    unsigned* sched;               // tiled pass: [next chunk, retired warps], zero between launches
 };
 
 template <typename T>

@@ -25,9 +25,13 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     // PASS_FUSED: a5 refill of sweep s fused with block (0,1)'s a2 of sweep s+1 (K = {0,1}):
     // t = M·H_{0,1}(i_0, v), X_new written back and used for β.
     constexpr bool kFused = (MODE == PASS_FUSED);
-    using Cfg = PassCfg<T, EPL, LPF, true, true>;
+    // KEPT1/FUSED tiles keep modes {1, 2} (code 0, 1): H_{0,1} is the excluded pair, so only
+    // RED1 tiles multiply by an H_{0,1} column
+    constexpr bool kH1 = (MODE == PASS_RED1);
+    using Cfg = PassCfg<T, EPL, LPF, true, true, kFused>;
     constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR;
-    constexpr int STAGE = F * SR;
+    constexpr int STAGE = Cfg::STAGE;
+    constexpr int MWF = Cfg::MWF;
     constexpr int NS = F / FP;  // accumulator sets per lane
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
@@ -58,8 +62,16 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     fence_proxy_async_smem();
     __syncthreads();
 
-    const int group = blockIdx.x * nwarps + warp;
-    if (group >= P.ngroups) return;
+    // Dynamic schedule: the stage range is cut into P.ngroups fixed chunks of L/F stages;
+    // warps claim chunks from a global counter (P.sched[0]).  A chunk's partial slots and norm
+    // slot are indexed by the chunk, not by the warp, so the result does not depend on which
+    // warp ran it.  The last warp to retire resets the counters for the next launch.
+    const int nchunks = (int)P.ngroups;
+    const int LQ = (int)(P.L / F);            // stages per chunk
+    const int QT = (int)(P.nfib / F);         // stages in total
+    int c_first = 0;
+    if (lane == 0) c_first = (int)atomicAdd(P.sched, 1u);
+    c_first = __shfl_sync(0xffffffffu, c_first, 0);
 
     const uint32_t bar0 = smem_u32(bars);
     const uint32_t stg0 = smem_u32(stg);
@@ -81,9 +93,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     const uint32_t rowbytes = (uint32_t)(I1p * sizeof(T));
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;  // fused: ‖ΔX‖², ‖X‖², ‖X_new − t‖²
 
-    // stages = positions q = vb·FR + r (r in odometer order, r0 fastest); warp range [q0, q1)
-    const int q0 = group * (int)(P.L / F);
-    const int q1 = min(q0 + (int)(P.L / F), (int)(P.nfib / F));
+    // stages = positions q = vb·FR + r (r in odometer order, r0 fastest)
     auto decode = [&](int q, int& vb, int& b0, int& nvalid, int (&ridx)[MAXN]) {
         vb = q / FR;
         int r = q - vb * FR;
@@ -104,20 +114,54 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     };
 
     // ---- producer (lane 0): one stage (F contiguous fibres) per position, D ahead --------
-    // incremental odometer over r (rmode[0] fastest); full decode only when vb changes
-    int pq = q0;
+    // incremental odometer over r (rmode[0] fastest); full decode only when vb changes.  At
+    // the end of its chunk the producer claims the next one (at most one chunk ahead of the
+    // consumers, who adopt it from lane 0 when they finish theirs).
+    int p_chunk = c_first;
+    bool p_ahead = false;
+    int pq = c_first < nchunks ? c_first * LQ : 0;
+    int pq1 = c_first < nchunks ? min(pq + LQ, QT) : 0;
     uint32_t p_n = 0;
     int p_vb, p_b0, p_nvalid, p_ridx[MAXN];
-    int p_fib = decode(q0, p_vb, p_b0, p_nvalid, p_ridx);
+    int p_fib = decode(pq, p_vb, p_b0, p_nvalid, p_ridx);
     auto produce = [&]() {
-        if (pq >= q1) return;
+        if (pq >= pq1) {
+            if (p_ahead || p_chunk >= nchunks) return;
+            p_chunk = (int)atomicAdd(P.sched, 1u);
+            p_ahead = true;
+            if (p_chunk >= nchunks) return;
+            pq = p_chunk * LQ;
+            pq1 = min(pq + LQ, QT);
+            p_fib = decode(pq, p_vb, p_b0, p_nvalid, p_ridx);
+        }
         const int fib = p_fib;
         const int nvalid = p_nvalid;
         const int s = (int)(p_n & (uint32_t)(D - 1));
         const uint32_t bar = bar0 + 8u * (uint32_t)s;
         const uint32_t sx = stg0 + (uint32_t)(s * STAGE * (int)sizeof(T));
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx_a(bar, (uint32_t)nvalid * rowbytes);
+        fence_stage_refill();
+        const int64_t pg0 = (int64_t)fib * I1p;
+        uint32_t mbytes = 0;
+        int64_t ma0 = 0;
+        if constexpr (kFused) {
+            if (SR == I1p) {
+                mbytes = mask_span(pg0, (int64_t)nvalid * I1p, ma0);
+            } else {
+                for (int f = 0; f < nvalid; ++f) mbytes += mask_span(pg0 + (int64_t)f * I1p, I1p, ma0);
+            }
+        }
+        mbar_arrive_expect_tx_a(bar, (uint32_t)nvalid * rowbytes + mbytes);
+        if constexpr (kFused) {
+            const uint32_t sm = sx + (uint32_t)(Cfg::XH * (int)sizeof(T));
+            if (SR == I1p) {
+                tma_g2s_a(sm, P.mask + ma0, mbytes, bar);
+            } else {
+                for (int f = 0; f < nvalid; ++f) {
+                    const uint32_t b = mask_span(pg0 + (int64_t)f * I1p, I1p, ma0);
+                    tma_g2s_a(sm + (uint32_t)(f * MWF * 4), P.mask + ma0, b, bar);
+                }
+            }
+        }
         const T* xs = P.X + (int64_t)fib * I1p;
         if (SR == I1p) {
             tma_g2s_a(sx, xs, (uint32_t)nvalid * rowbytes, bar);
@@ -127,7 +171,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
         }
         ++pq;
         ++p_n;
-        if (pq >= q1) return;
+        if (pq >= pq1) return;
         // advance the odometer (fast path: the fastest reduced index does not wrap)
         if (p_ridx[0] + 1 < rdim0) {
             p_ridx[0] += 1;
@@ -159,163 +203,194 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
 #pragma unroll
         for (int e = 0; e < EPL; ++e) sb[t][e] = sw[t][e] = T(0);
     uint32_t cn = 0;
-    int q = q0;
-    while (q < q1) {
-        int vb, b0, nvalid, ridx[MAXN];
-        decode(q, vb, b0, nvalid, ridx);
-        const int seg_end = min(q1, (vb + 1) * FR);           // end of this kept block
-        const int rl = min(min(seg_end - q, rdim0 - ridx[0]), RL);  // tile: r0 run
-        // ---- tile setup: slow factors and the (v, i_{r0}) scalar table --------------------
-        int idx[MAXN];
+    for (int chunk = c_first; chunk < nchunks;) {
+        const int group = chunk;  // partial-slot / norm-slot index
+        int q = chunk * LQ;
+        const int q1 = min(q + LQ, QT);
+        while (q < q1) {
+            int vb, b0, nvalid, ridx[MAXN];
+            decode(q, vb, b0, nvalid, ridx);
+            const int seg_end = min(q1, (vb + 1) * FR);           // end of this kept block
+            const int rl = min(min(seg_end - q, rdim0 - ridx[0]), RL);  // tile: r0 run
+            // ---- tile setup: slow factors and the (v, i_{r0}) scalar table --------------------
+            int idx[MAXN];
 #pragma unroll
-        for (int m = 0; m < MAXN; ++m) idx[m] = 0;
-        if (P.nkept >= 2) idx[P.kmode[1]] = vb / nb0;
+            for (int m = 0; m < MAXN; ++m) idx[m] = 0;
+            if (P.nkept >= 2) idx[P.kmode[1]] = vb / nb0;
 #pragma unroll
-        for (int j = 0; j < MAXN; ++j)
-            if (j < P.nred) idx[P.rmode[j]] = ridx[j];
-        T ws[EPL];
+            for (int j = 0; j < MAXN; ++j)
+                if (j < P.nred) idx[P.rmode[j]] = ridx[j];
+            T ws[EPL];
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) ws[e] = ev[e] ? T(1) : T(0);
-        for (int t = 0; t < P.nvs; ++t) {
-            const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * I1p + eb;
+            for (int e = 0; e < EPL; ++e) ws[e] = ev[e] ? T(1) : T(0);
+            for (int t = 0; t < P.nvs; ++t) {
+                const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * I1p + eb;
 #pragma unroll
-            for (int e = 0; e < EPL; ++e)
-                if (ev[e]) ws[e] *= base[e];
-        }
-        T ss = T(1);
-        for (int t = 0; t < P.nss; ++t)
-            ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) ws[e] *= ss;
-        // scalar factors touching mode 1 or r0, factorised: sf(f,t) = A(v_f)·B(i_{r0,t})·C(v_f, i_{r0,t})
-        //   A = Π_q H_{1,q}(v, i_q), B = Π_q H_{r0,q}(i_{r0}, i_q) (q fixed in the tile),
-        //   C = H_{1,r0}(v, i_{r0}) unless {1, r0} is the kept pair.
-        T* At = sfv + P.sf_cap;
-        T* Bt = At + F;
-        if (lane < F) {
-            T a = T(1);
-            const int v = b0 + min(lane, nvalid - 1);
-            for (int u = 0; u < P.nta; ++u)
-                a *= Hb[P.ta_off[u] + (int64_t)idx[P.ta_fix[u]] * P.ta_mul[u] + (int64_t)v * P.ta_inc[u]];
-            At[lane] = a;
-        }
-        for (int t = lane; t < rl; t += 32) {
-            T b = T(1);
-            for (int u = 0; u < P.nsf; ++u)
-                b *= Hb[P.sf_off[u] + (int64_t)idx[P.sf_fixmode[u]] * P.sf_fixmul[u] + (int64_t)(ridx[0] + t) * P.sf_inc[u]];
-            Bt[t] = b;
-        }
-        __syncwarp();
-        {
-            const T* cb = P.tc_off >= 0 ? Hb + P.tc_off + (int64_t)ridx[0] * P.tc_ld + b0 : nullptr;
-            for (int e = lane; e < F * rl; e += 32) {
-                const int f = e % F, t = e / F;  // F is a power of two: shifts
-                T val = At[f] * Bt[t];
-                if (cb) val *= cb[(int64_t)t * P.tc_ld + min(f, nvalid - 1)];
-                sfv[t * F + f] = val;
+                for (int e = 0; e < EPL; ++e)
+                    if (ev[e]) ws[e] *= base[e];
             }
-        }
-        __syncwarp();
-        const T* h2run = h2 + (int64_t)ridx[0] * I1p;
-        const int64_t fib0 = kFused ? decode(q, vb, b0, nvalid, ridx) : 0;  // fused: X address
-        const int fstep = fstep0;
-        T q0 = T(0), q1 = T(0), q2 = T(0);
-        for (int t = 0; t < rl; ++t) {
-            const int s = (int)(cn & (uint32_t)(D - 1));
-            mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
-            const T* sx = stg + s * STAGE;
-            T hr[EPL];
-            lds_vec<T, EPL>(h2run + t * I1p, hr);
-            T wr[EPL];
+            T ss = T(1);
+            for (int t = 0; t < P.nss; ++t)
+                ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) wr[e] = ws[e] * hr[e];
-#pragma unroll
-            for (int st = 0; st < NS; ++st) {
-                const int f = st * FP + fsub;
-                if (f < nvalid) {
-                    T h[EPL], w[EPL], x[EPL];
-                    lds_vec<T, EPL>(h1 + (b0 + f) * h1step, h);
-                    weight<T, EPL>(wr, h, sfv[t * F + f], w);
-                    lds_vec<T, EPL>(sx + f * SR + eb, x);
-                    if constexpr (kFused) {
-                        T h01[EPL], tt[EPL], xn[EPL];
-                        lds_vec<T, EPL>(h3 + (b0 + f) * I1p, h01);
-#pragma unroll
-                        for (int e = 0; e < EPL; ++e) tt[e] = w[e] * h01[e];
-                        const int64_t ge = (fib0 + (int64_t)t * fstep + f) * I1p + eb;
-                        refill_chunk<T, EPL>(x, tt, mask_bits(P.mask, ge), P.rho, P.inv1p, xn, q0, q1, q2);
-                        store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
-                        accumulate<T, EPL>(w, xn, sb[st], sw[st]);
-                    } else {
-                        accumulate<T, EPL>(w, x, sb[st], sw[st]);
-                    }
+            for (int e = 0; e < EPL; ++e) ws[e] *= ss;
+            // scalar factors touching mode 1 or r0, factorised: sf(f,t) = A(v_f)·B(i_{r0,t})·C(v_f, i_{r0,t})
+            //   A = Π_q H_{1,q}(v, i_q), B = Π_q H_{r0,q}(i_{r0}, i_q) (q fixed in the tile),
+            //   C = H_{1,r0}(v, i_{r0}) unless {1, r0} is the kept pair.
+            T* At = sfv + P.sf_cap;
+            T* Bt = At + F;
+            if (lane < F) {
+                T a = T(1);
+                const int v = b0 + min(lane, nvalid - 1);
+                for (int u = 0; u < P.nta; ++u)
+                    a *= Hb[P.ta_off[u] + (int64_t)idx[P.ta_fix[u]] * P.ta_mul[u] + (int64_t)v * P.ta_inc[u]];
+                At[lane] = a;
+            }
+            for (int t = lane; t < rl; t += 32) {
+                T b = T(1);
+                for (int u = 0; u < P.nsf; ++u)
+                    b *= Hb[P.sf_off[u] + (int64_t)idx[P.sf_fixmode[u]] * P.sf_fixmul[u] + (int64_t)(ridx[0] + t) * P.sf_inc[u]];
+                Bt[t] = b;
+            }
+            __syncwarp();
+            {
+                const T* cb = P.tc_off >= 0 ? Hb + P.tc_off + (int64_t)ridx[0] * P.tc_ld + b0 : nullptr;
+                for (int e = lane; e < F * rl; e += 32) {
+                    const int f = e % F, t = e / F;  // F is a power of two: shifts
+                    T val = At[f] * Bt[t];
+                    if (cb) val *= cb[(int64_t)t * P.tc_ld + min(f, nvalid - 1)];
+                    sfv[t * F + f] = val;
                 }
             }
             __syncwarp();
-            ++cn;
-            if (lane == 0) produce();
-        }
-        __syncwarp();  // sfv is rewritten by the next tile
-        if constexpr (kFused) {
-            n0 += (double)q0;
-            n1 += (double)q1;
-            n2 += (double)q2;
-        }
-        q += rl;
-        if (q >= seg_end) {  // kept block finished (or range end): flush its F values
+            const T* h2run = h2 + (int64_t)ridx[0] * I1p;
+            const int64_t fib0 = kFused ? decode(q, vb, b0, nvalid, ridx) : 0;  // fused: X address
+            const int fstep = fstep0;
+            Norms3<T> qn;
+            T* xw = kFused ? P.Xw + fib0 * I1p : nullptr;  // fused: X_new of the stage's first fibre
+            for (int t = 0; t < rl; ++t) {
+                const int s = (int)(cn & (uint32_t)(D - 1));
+                mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
+                const T* sx = stg + s * STAGE;
+                const uint32_t* smw = reinterpret_cast<const uint32_t*>(sx + Cfg::XH);
+                T hr[EPL];
+                lds_vec<T, EPL>(h2run + t * I1p, hr);
+                T wr[EPL];
 #pragma unroll
-            for (int st = 0; st < NS; ++st) {
-                const int f = st * FP + fsub;
-                const int64_t slot = ((int64_t)group + vb) * F + f;
-                if constexpr (MODE == PASS_KEPT1 || kFused) {
+                for (int e = 0; e < EPL; ++e) wr[e] = ws[e] * hr[e];
+#pragma unroll
+                for (int st = 0; st < NS; ++st) {
+                    const int f = st * FP + fsub;
                     if (f < nvalid) {
-                        T* pbd = P.part_b + slot * P.Lv + eb;
-                        T* pwd = P.part_w + slot * P.Lv + eb;
-                        if (lane_full) {
-                            stg_vec<T, EPL>(pbd, sb[st]);
-                            stg_vec<T, EPL>(pwd, sw[st]);
+                        T w[EPL], x[EPL];
+                        if constexpr (kH1) {
+                            T h[EPL];
+                            lds_vec<T, EPL>(h1 + (b0 + f) * h1step, h);
+                            weight<T, EPL>(wr, h, sfv[t * F + f], w);
+                        } else {  // H_{0,1} is the excluded pair: M = wr · sf
+                            scale<T, EPL>(wr, sfv[t * F + f], w);
+                        }
+                        lds_vec<T, EPL>(sx + f * SR + eb, x);
+                        if constexpr (kFused) {
+                            T h01[EPL], tt[EPL], xn[EPL];
+                            lds_vec<T, EPL>(h3 + (b0 + f) * I1p, h01);
+                            mul<T, EPL>(w, h01, tt);
+                            // Ω bits: the staged word range starts at the 128-bit boundary at or
+                            // below the stage's (merged) or the fibre's first element
+                            const int fo = f * I1p;
+                            const int sl = (int)((uint32_t)(xw - P.Xw) & 127u);
+                            const uint32_t bits = (SR == I1p) ? mask_bits_l(smw, sl + fo + eb)
+                                                              : mask_bits_l(smw + f * MWF, ((sl + fo) & 127) + eb);
+                            refill_chunk<T, EPL>(x, tt, bits, P.rho, P.inv1p, xn, qn);
+                            store_chunk<T, EPL>(xw + fo + eb, xn, lane_full, ev);
+                            accumulate<T, EPL>(w, xn, sb[st], sw[st]);
                         } else {
-#pragma unroll
-                            for (int e = 0; e < EPL; ++e)
-                                if (ev[e]) {
-                                    pbd[e] = sb[st][e];
-                                    pwd[e] = sw[st][e];
-                                }
+                            accumulate<T, EPL>(w, x, sb[st], sw[st]);
                         }
                     }
-                } else {
-                    T tb = T(0), tw = T(0);
-#pragma unroll
-                    for (int e = 0; e < EPL; ++e) {
-                        tb += sb[st][e];
-                        tw += sw[st][e];
-                    }
-#pragma unroll
-                    for (int o = LPF / 2; o > 0; o >>= 1) {  // the fibre's LPF lanes
-                        tb += __shfl_xor_sync(0xffffffffu, tb, o);
-                        tw += __shfl_xor_sync(0xffffffffu, tw, o);
-                    }
-                    if ((lane % LPF) == 0 && f < nvalid) {
-                        P.part_b[slot] = tb;
-                        P.part_w[slot] = tw;
-                    }
                 }
+                __syncwarp();
+                ++cn;
+                if constexpr (kFused) xw += (int64_t)fstep * I1p;
+                if (lane == 0) produce();
+            }
+            __syncwarp();  // sfv is rewritten by the next tile
+            if constexpr (kFused) {
+                n0 += qn.s0();
+                n1 += qn.s1();
+                n2 += qn.s2();
+            }
+            q += rl;
+            if (q >= seg_end) {  // kept block finished (or range end): flush its F values
 #pragma unroll
-                for (int e = 0; e < EPL; ++e) sb[st][e] = sw[st][e] = T(0);
+                for (int st = 0; st < NS; ++st) {
+                    const int f = st * FP + fsub;
+                    const int64_t slot = ((int64_t)group + vb) * F + f;
+                    if constexpr (MODE == PASS_KEPT1 || kFused) {
+                        if (f < nvalid) {
+                            T* pbd = P.part_b + slot * P.Lv + eb;
+                            T* pwd = P.part_w + slot * P.Lv + eb;
+                            if (lane_full) {
+                                stg_vec<T, EPL>(pbd, sb[st]);
+                                stg_vec<T, EPL>(pwd, sw[st]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < EPL; ++e)
+                                    if (ev[e]) {
+                                        pbd[e] = sb[st][e];
+                                        pwd[e] = sw[st][e];
+                                    }
+                            }
+                        }
+                    } else {
+                        T tb = T(0), tw = T(0);
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) {
+                            tb += sb[st][e];
+                            tw += sw[st][e];
+                        }
+#pragma unroll
+                        for (int o = LPF / 2; o > 0; o >>= 1) {  // the fibre's LPF lanes
+                            tb += __shfl_xor_sync(0xffffffffu, tb, o);
+                            tw += __shfl_xor_sync(0xffffffffu, tw, o);
+                        }
+                        if ((lane % LPF) == 0 && f < nvalid) {
+                            P.part_b[slot] = tb;
+                            P.part_w[slot] = tw;
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) sb[st][e] = sw[st][e] = T(0);
+                }
             }
         }
-    }
-    if constexpr (kFused) {
+        if constexpr (kFused) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            n0 += __shfl_xor_sync(0xffffffffu, n0, o);
-            n1 += __shfl_xor_sync(0xffffffffu, n1, o);
-            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+            for (int o = 16; o > 0; o >>= 1) {
+                n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+                n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+                n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+            }
+            if (lane == 0) {
+                P.norms[(int64_t)group * 3 + 0] = n0;
+                P.norms[(int64_t)group * 3 + 1] = n1;
+                P.norms[(int64_t)group * 3 + 2] = n2;
+            }
+            n0 = n1 = n2 = 0.0;
         }
+        // next chunk: the one the producer claimed
+        int nx = 0;
         if (lane == 0) {
-            P.norms[(int64_t)group * 3 + 0] = n0;
-            P.norms[(int64_t)group * 3 + 1] = n1;
-            P.norms[(int64_t)group * 3 + 2] = n2;
+            nx = p_chunk;
+            p_ahead = false;
+        }
+        chunk = __shfl_sync(0xffffffffu, nx, 0);
+    }
+    if (lane == 0) {
+        const unsigned total = gridDim.x * (unsigned)nwarps;
+        if (atomicAdd(P.sched + 1, 1u) == total - 1) {
+            P.sched[0] = 0u;
+            P.sched[1] = 0u;
         }
     }
 }

@@ -73,6 +73,39 @@ __device__ __forceinline__ void weight(const T (&ws)[N], const T (&h)[N], T sf, 
     }
 }
 
+// w = ws · sf
+template <typename T, int N>
+__device__ __forceinline__ void scale(const T (&ws)[N], T sf, T (&w)[N]) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+        const float2 s2 = make_float2(sf, sf);
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 r = __fmul2_rn(make_float2(ws[e], ws[e + 1]), s2);
+            w[e] = r.x;
+            w[e + 1] = r.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) w[e] = ws[e] * sf;
+    }
+}
+
+// o = a ⊙ b
+template <typename T, int N>
+__device__ __forceinline__ void mul(const T (&a)[N], const T (&b)[N], T (&o)[N]) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 r = __fmul2_rn(make_float2(a[e], a[e + 1]), make_float2(b[e], b[e + 1]));
+            o[e] = r.x;
+            o[e + 1] = r.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) o[e] = a[e] * b[e];
+    }
+}
+
 // sb += w ⊙ x, sw += w ⊙ w   (fp32: packed FFMA2 pairs)
 template <typename T, int N>
 __device__ __forceinline__ void accumulate(const T (&w)[N], const T (&x)[N], T (&sb)[N], T (&sw)[N]) {
@@ -96,20 +129,74 @@ __device__ __forceinline__ void accumulate(const T (&w)[N], const T (&x)[N], T (
     }
 }
 
-// Eq. 9 on EPL entries (reading R1: per-entry prox minimiser), with the norm accumulators of
-// the stop test and the objective: q0 += (x_new − x)², q1 += x², q2 += (x_new − t)².
+// Norm accumulators of the refill / objective passes (per run, then fp64): q0 = ‖ΔX‖²,
+// q1 = ‖X‖², q2 = ‖X_new − t‖².  fp32 keeps (even, odd) element pairs for packed FFMA2.
+template <typename T>
+struct Norms3 {
+    T q0 = T(0), q1 = T(0), q2 = T(0);
+    __device__ double s0() const { return (double)q0; }
+    __device__ double s1() const { return (double)q1; }
+    __device__ double s2() const { return (double)q2; }
+};
+template <>
+struct Norms3<float> {
+    float2 q0 = make_float2(0.f, 0.f), q1 = make_float2(0.f, 0.f), q2 = make_float2(0.f, 0.f);
+    __device__ double s0() const { return (double)q0.x + (double)q0.y; }
+    __device__ double s1() const { return (double)q1.x + (double)q1.y; }
+    __device__ double s2() const { return (double)q2.x + (double)q2.y; }
+};
+
+// Eq. 9 on EPL entries (reading R1: per-entry prox minimiser) plus the norm accumulators of
+// the stop test and the objective.
 template <typename T, int N>
 __device__ __forceinline__ void refill_chunk(const T (&x)[N], const T (&t)[N], uint32_t bits, T rho,
-                                             T inv1p, T (&xn)[N], T& q0, T& q1, T& q2) {
+                                             T inv1p, T (&xn)[N], Norms3<T>& q) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+        const float2 r2 = make_float2(rho, rho), i2 = make_float2(inv1p, inv1p);
+        const float2 m1 = make_float2(-1.f, -1.f);
 #pragma unroll
-    for (int e = 0; e < N; ++e) {
-        const bool obs = (bits >> e) & 1u;
-        xn[e] = obs ? x[e] : (t[e] + rho * x[e]) * inv1p;
-        const T d = xn[e] - x[e];
-        const T g = xn[e] - t[e];
-        q0 = fma(d, d, q0);
-        q1 = fma(x[e], x[e], q1);
-        q2 = fma(g, g, q2);
+        for (int e = 0; e < N; e += 2) {
+            const float2 x2 = make_float2(x[e], x[e + 1]), t2 = make_float2(t[e], t[e + 1]);
+            const float2 u = __fmul2_rn(__ffma2_rn(r2, x2, t2), i2);  // (t + ρx)/(1 + ρ)
+            xn[e] = ((bits >> e) & 1u) ? x[e] : u.x;
+            xn[e + 1] = ((bits >> (e + 1)) & 1u) ? x[e + 1] : u.y;
+            const float2 n2 = make_float2(xn[e], xn[e + 1]);
+            const float2 d = __ffma2_rn(x2, m1, n2);  // x_new − x
+            const float2 g = __ffma2_rn(t2, m1, n2);  // x_new − t
+            q.q0 = __ffma2_rn(d, d, q.q0);
+            q.q1 = __ffma2_rn(x2, x2, q.q1);
+            q.q2 = __ffma2_rn(g, g, q.q2);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const bool obs = (bits >> e) & 1u;
+            xn[e] = obs ? x[e] : fma(rho, x[e], t[e]) * inv1p;
+            const T d = xn[e] - x[e];
+            const T g = xn[e] - t[e];
+            q.q0 = fma(d, d, q.q0);
+            q.q1 = fma(x[e], x[e], q.q1);
+            q.q2 = fma(g, g, q.q2);
+        }
+    }
+}
+
+// objective pass: q2 += (x − t)²
+template <typename T, int N>
+__device__ __forceinline__ void objective_chunk(const T (&x)[N], const T (&t)[N], Norms3<T>& q) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+        const float2 m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 g = __ffma2_rn(make_float2(t[e], t[e + 1]), m1, make_float2(x[e], x[e + 1]));
+            q.q2 = __ffma2_rn(g, g, q.q2);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            const T g = x[e] - t[e];
+            q.q2 = fma(g, g, q.q2);
+        }
     }
 }
 
@@ -124,9 +211,24 @@ __device__ __forceinline__ void store_chunk(T* dst, const T (&v)[N], bool full, 
     }
 }
 
-__device__ __forceinline__ uint32_t mask_bits(const uint32_t* mask, int64_t ge) {
-    const uint32_t* mw = mask + (ge >> 5);
-    return __funnelshift_r(__ldg(mw), __ldg(mw + 1), (uint32_t)(ge & 31));
+// Ω bits staged in shared memory (PassCfg MASK): `mw` holds the 16-B-aligned word range that
+// starts at word (g0 >> 5) & ~3 of the fibre (or stage) whose first element is g0.
+__device__ __forceinline__ uint32_t mask_bits_s(const uint32_t* mw, int64_t g0, int64_t ge) {
+    const int lb = (int)(ge - (((g0 >> 5) & ~(int64_t)3) << 5));
+    return __funnelshift_r(mw[lb >> 5], mw[(lb >> 5) + 1], (uint32_t)(lb & 31));
+}
+
+// same with the bit offset lb relative to the staged range's first word
+__device__ __forceinline__ uint32_t mask_bits_l(const uint32_t* mw, int lb) {
+    return __funnelshift_r(mw[lb >> 5], mw[(lb >> 5) + 1], (uint32_t)(lb & 31));
+}
+
+// Producer side: bytes of the aligned word range covering elements [g0, g0 + n) plus the
+// funnel word, and its first word.
+__device__ __forceinline__ uint32_t mask_span(int64_t g0, int64_t n, int64_t& a0) {
+    a0 = (g0 >> 5) & ~(int64_t)3;
+    const int64_t a1 = ((((g0 + n - 1) >> 5) + 2) + 3) & ~(int64_t)3;
+    return (uint32_t)((a1 - a0) * 4);
 }
 
 // Fibre walker: positions pos = v·FR + r of one warp's range, cut into runs (consecutive
@@ -208,9 +310,11 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
     constexpr bool kContract = (MODE == PASS_KEPT1 || MODE == PASS_RED1 || kFused);
     constexpr bool kNorms = (MODE == PASS_REFILL || MODE == PASS_OBJ || kFused);
     constexpr bool kLoadX = (MODE != PASS_MODEL);
-    using Cfg = PassCfg<T, EPL, LPF, HRES, kLoadX>;
+    constexpr bool kMask = (MODE == PASS_REFILL || kFused);
+    using Cfg = PassCfg<T, EPL, LPF, HRES, kLoadX, kMask>;
     constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR, NROW = Cfg::NROW;
-    constexpr int STAGE = NROW * F * SR;  // elements per ring stage
+    constexpr int STAGE = Cfg::STAGE;  // elements per ring stage (X, H rows, Ω words)
+    constexpr int MWF = Cfg::MWF;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int fsub = lane / LPF;                 // fibre of the step served by this lane
@@ -277,8 +381,29 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
         const int s = (int)(p_n & (uint32_t)(D - 1));
         const uint32_t bar = bar0 + 8u * (uint32_t)s;
         const uint32_t sx = stg0 + (uint32_t)(s * STAGE * (int)sizeof(T));
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx_a(bar, (uint32_t)nf * rowbytes * (uint32_t)NROW);
+        fence_stage_refill();
+        uint32_t mbytes = 0;
+        int64_t ma0 = 0;
+        const int64_t pg0 = p_x - P.X;  // first element of the stage's first fibre
+        if constexpr (kMask) {
+            if (xmerge) {
+                mbytes = mask_span(pg0, (int64_t)nf * I1p, ma0);
+            } else {
+                for (int f = 0; f < nf; ++f) mbytes += mask_span(pg0 + (int64_t)f * xstep, I1p, ma0);
+            }
+        }
+        mbar_arrive_expect_tx_a(bar, (uint32_t)nf * rowbytes * (uint32_t)NROW + mbytes);
+        if constexpr (kMask) {
+            const uint32_t sm = sx + (uint32_t)(Cfg::XH * (int)sizeof(T));
+            if (xmerge) {
+                tma_g2s_a(sm, P.mask + ma0, mbytes, bar);
+            } else {
+                for (int f = 0; f < nf; ++f) {
+                    const uint32_t b = mask_span(pg0 + (int64_t)f * xstep, I1p, ma0);
+                    tma_g2s_a(sm + (uint32_t)(f * MWF * 4), P.mask + ma0, b, bar);
+                }
+            }
+        }
         if constexpr (kLoadX) {
             if (xmerge) {
                 tma_g2s_a(sx, p_x, (uint32_t)nf * rowbytes, bar);
@@ -371,13 +496,15 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
             for (int e = 0; e < EPL; ++e) h01v[e] = ev[e] ? hb[e] : T(0);
         }
 
-        T q0 = T(0), q1 = T(0), q2 = T(0);
+        Norms3<T> qn;
         for (int off = 0; off < len; off += F) {
             const int nf = min(F, len - off);
             const int s = (int)(cn & (uint32_t)(D - 1));
             mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
             const T* sx = stg + s * STAGE;
             const T* sh = sx + (kLoadX ? F * SR : 0);
+            const uint32_t* smw = reinterpret_cast<const uint32_t*>(sx + Cfg::XH);
+            const int64_t sg0 = ebase + (int64_t)off * xstep;  // stage's first element
 #pragma unroll
             for (int st = 0; st < F / FP; ++st) {
                 const int f = st * FP + fsub;
@@ -392,8 +519,9 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
 #pragma unroll
                         for (int e = 0; e < EPL; ++e) t[e] = w[e] * h01v[e];
-                        const int64_t ge = ebase + (int64_t)(off + f) * xstep + eb;
-                        refill_chunk<T, EPL>(x, t, mask_bits(P.mask, ge), P.rho, P.inv1p, xn, q0, q1, q2);
+                        const int64_t gf = sg0 + (int64_t)f * xstep, ge = gf + eb;
+                        const uint32_t bits = xmerge ? mask_bits_s(smw, sg0, ge) : mask_bits_s(smw + f * MWF, gf, ge);
+                        refill_chunk<T, EPL>(x, t, bits, P.rho, P.inv1p, xn, qn);
                         store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
                         accumulate<T, EPL>(w, xn, sb, sw);
                     } else if constexpr (kContract) {
@@ -403,17 +531,14 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                     } else if constexpr (MODE == PASS_REFILL) {
                         T x[EPL], xn[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
-                        const int64_t ge = ebase + (int64_t)(off + f) * xstep + eb;
-                        refill_chunk<T, EPL>(x, w, mask_bits(P.mask, ge), P.rho, P.inv1p, xn, q0, q1, q2);
+                        const int64_t gf = sg0 + (int64_t)f * xstep, ge = gf + eb;
+                        const uint32_t bits = xmerge ? mask_bits_s(smw, sg0, ge) : mask_bits_s(smw + f * MWF, gf, ge);
+                        refill_chunk<T, EPL>(x, w, bits, P.rho, P.inv1p, xn, qn);
                         store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
                     } else if constexpr (MODE == PASS_OBJ) {
                         T x[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
-#pragma unroll
-                        for (int e = 0; e < EPL; ++e) {
-                            const T g = x[e] - w[e];
-                            q2 = fma(g, g, q2);
-                        }
+                        objective_chunk<T, EPL>(x, w, qn);
                     } else {  // PASS_MODEL: dense user layout, scalar stores
                         const int64_t fb = C.fib + (int64_t)(off + f) * fstep;
 #pragma unroll
@@ -427,9 +552,9 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
             if (lane == 0) produce();
         }
         if constexpr (kNorms) {
-            n0 += (double)q0;
-            n1 += (double)q1;
-            n2 += (double)q2;
+            n0 += qn.s0();
+            n1 += qn.s1();
+            n2 += qn.s2();
         }
         __syncwarp();  // sfv is rewritten by the next run
         // ---- flush the segment's partials into slot group + v ---------------------------

@@ -51,6 +51,7 @@ static int pow2ceil(int x) {
 }
 
 constexpr int64_t kGroupBoundThreads = 160LL * 2048;  // ≥ resident threads of any B200 part
+constexpr int64_t kChunksPerWarp = 1;                  // tiled pass: dynamic chunks per warp (IFCTN_TUNE_CHUNKS)
 constexpr unsigned kFlagNoVBlock = IFCTN_FLAG_NO_VBLOCK;
 constexpr unsigned kFlagNoFuse = IFCTN_FLAG_NO_FUSE;
 
@@ -245,7 +246,7 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
 }
 
 struct Layout {
-    int64_t x, bits, g, h, pb, pw, beta, omega, delta, norms, scal, flags, rse, proj, rscr, rcnt, total;
+    int64_t x, bits, g, h, pb, pw, beta, omega, delta, norms, scal, flags, rse, proj, rscr, rcnt, sched, total;
 };
 
 // split-slot reduce (reduce_partials with Z > 1): scratch doubles and arrival counters
@@ -276,6 +277,7 @@ static Layout make_layout(const Shape& s) {
     L.proj = take(s.proj_elems * 8);
     L.rscr = take(kRedScr * 8);
     L.rcnt = take(kRedCnt * 4);
+    L.sched = take(64);
     L.total = o;
     return L;
 }
@@ -363,7 +365,8 @@ struct PassKernel {
 // MODE >= 100: the v-blocked contraction kernel for MODE - 100
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 static PassKernel pk() {
-    using Cfg = PassCfg<T, EPL, LPF, HRES, (MODE % 100) != PASS_MODEL>;
+    constexpr int M0 = MODE % 100;
+    using Cfg = PassCfg<T, EPL, LPF, HRES, M0 != PASS_MODEL, M0 == PASS_REFILL || M0 == PASS_FUSED>;
     if constexpr (MODE >= 100) {
         constexpr int M = MODE - 100;
         if constexpr ((M == PASS_KEPT1 || M == PASS_RED1 || M == PASS_FUSED) && HRES)
@@ -445,7 +448,7 @@ struct Solver : SolverBase {
     T *X, *G, *H, *pb, *pw;
     uint32_t* bits;
     double *beta, *omega, *delta, *norms, *scal, *rsep, *proj, *rscr;
-    unsigned* rcnt;
+    unsigned *rcnt, *sched;
     int* dflags;
     double* hscal = nullptr;  // pinned
     int* hflags = nullptr;    // pinned
@@ -460,6 +463,7 @@ struct Solver : SolverBase {
     int64_t nlaunch_sweep = 0, last_launches = 0;
     int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
     int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
+    int64_t chunks_per_warp = kChunksPerWarp;  // tiled-pass chunks per warp (env knob)
     int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
     int64_t sh_off = 0, sh_len = 0;        // ΔG² range of the shard-mode chains
     double* p5 = nullptr;                  // norm partials (see finalize_norms)
@@ -678,15 +682,20 @@ struct Solver : SolverBase {
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pp.fn, kPassThreads, smem));
         if (nb < 1) nb = 1;
         if (tune_ctas > 0) nb = std::min(nb, tune_ctas);
-        // grid: one wave of warps ("groups"), equal fibre counts
+        // grid: one wave of warps.  Plain walk: one fibre range ("group") per warp, equal
+        // fibre counts.  Tiled pass: kChunksPerWarp× more fixed chunks ("groups") than warps,
+        // claimed dynamically (fiber_tile.cuh), so no SM idles while others finish.
         int64_t gmax = (int64_t)nsm * nb * nwarps;
         gmax = std::min(gmax, s.groups_bound);
         const int64_t unit = vblk ? kern.F : 1;  // v-blocked ranges hold whole runs
         const int64_t nunits = p.nfib / unit;
-        const int64_t L = std::max<int64_t>(1, (nunits + gmax - 1) / gmax) * unit;
+        const int64_t nchunk = vblk ? std::min(gmax * chunks_per_warp, s.groups_bound) : gmax;
+        const int64_t L = std::max<int64_t>(1, (nunits + nchunk - 1) / nchunk) * unit;
         p.L = L;
         p.ngroups = (p.nfib + L - 1) / L;
-        pp.grid = dim3((unsigned)((p.ngroups + nwarps - 1) / nwarps));
+        p.sched = sched;
+        const int64_t warps = vblk ? std::min(gmax, p.ngroups) : p.ngroups;
+        pp.grid = dim3((unsigned)((warps + nwarps - 1) / nwarps));
         pp.smem = smem;
         return pp;
     }
@@ -898,6 +907,7 @@ struct Solver : SolverBase {
         CU(cudaDeviceGetAttribute(&smo, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         smem_limit = (size_t)smo;
         if (const char* e = getenv("IFCTN_TUNE_CTAS")) tune_ctas = atoi(e);  // experiments only
+        if (const char* e = getenv("IFCTN_TUNE_CHUNKS")) chunks_per_warp = std::max(1, atoi(e));
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
@@ -928,6 +938,7 @@ struct Solver : SolverBase {
         proj = (double*)(ws + lay.proj);
         rscr = (double*)(ws + lay.rscr);
         rcnt = (unsigned*)(ws + lay.rcnt);
+        sched = (unsigned*)(ws + lay.sched);
 
         begin();
         CU(cudaMemsetAsync(ws, 0, lay.total, st));

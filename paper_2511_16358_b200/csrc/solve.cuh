@@ -388,13 +388,19 @@ __global__ void __launch_bounds__(256) rse_partial(const T* truth, const T* X, i
                                                    int64_t I1p, int64_t n, double* part) {
     __shared__ double s0[256], s1[256];
     double a = 0.0, b = 0.0;
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t f = u / I1, i1 = u - f * I1;
-        const double t = (double)truth[u];
-        const double d = t - (double)X[f * I1p + i1];
-        a += d * d;
-        b += t * t;
+    // warps stride over mode-1 fibres, lanes over i_1 (coalesced, no index division)
+    const int64_t nfib = n / I1;
+    const int lane = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t f = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < nfib; f += wstride) {
+        const T* tf = truth + f * I1;
+        const T* xf = X + f * I1p;
+        for (int64_t i1 = lane; i1 < I1; i1 += 32) {
+            const double t = (double)tf[i1];
+            const double d = t - (double)xf[i1];
+            a += d * d;
+            b += t * t;
+        }
     }
     s0[threadIdx.x] = a;
     s1[threadIdx.x] = b;
