@@ -14,6 +14,10 @@ constexpr int MAXSF = MAXN - 2;                // pairs involving the fast mode 
 constexpr int MAXR = 8;                        // IFCTN_MAX_RANK
 constexpr int kPassThreads = 256;              // fiber-pass CTA size
 constexpr int kPassMinBlocks = 2;              // ≤ 128 registers: ≥ 16 warps per SM
+#ifndef IFCTN_RING_D
+#define IFCTN_RING_D 3
+#endif
+constexpr int kRingStages = IFCTN_RING_D;      // TMA ring depth per warp (stages in flight)
 
 // Compile-time shape of one fibre-pass instance (fiber_pass.cuh): EPL mode-1 positions per
 // lane, LPF lanes per fibre (FP = 32/LPF fibres per warp step), ring rows per fibre (X and,
@@ -29,7 +33,7 @@ struct PassCfg {
     static constexpr int ROWB = SR * (int)sizeof(T);
     static constexpr int FK = (2048 / (NROW > 0 ? NROW : 1) / ROWB) / FP;
     static constexpr int F = FP * (FK > 1 ? FK : 1);
-    static constexpr int D = 4;
+    static constexpr int D = kRingStages;
     static constexpr int XH = NROW * F * SR;                       // X/H elements per stage
     static constexpr int MWF = MASK ? ((SR / 32 + 9 + 3) & ~3) : 0;  // mask words per fibre
     static constexpr int MW = F * MWF;                             // mask words per stage

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
         }
         const int fib = p_fib;
         const int nvalid = p_nvalid;
-        const int s = (int)(p_n & (uint32_t)(D - 1));
+        const int s = (int)(p_n % (uint32_t)D);
         const uint32_t bar = bar0 + 8u * (uint32_t)s;
         const uint32_t sx = stg0 + (uint32_t)(s * STAGE * (int)sizeof(T));
         fence_stage_refill();
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
             Norms3<T> qn;
             T* xw = kFused ? P.Xw + fib0 * I1p : nullptr;  // fused: X_new of the stage's first fibre
             for (int t = 0; t < rl; ++t) {
-                const int s = (int)(cn & (uint32_t)(D - 1));
+                const int s = (int)(cn % (uint32_t)D);
                 mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
                 const T* sx = stg + s * STAGE;
                 const uint32_t* smw = reinterpret_cast<const uint32_t*>(sx + Cfg::XH);

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
             p_h = Hb + (has_fast ? P.vf_off + (int64_t)Pw.ri0 * I1p : P.ones_off);
         }
         const int nf = min(F, p_left);
-        const int s = (int)(p_n & (uint32_t)(D - 1));
+        const int s = (int)(p_n % (uint32_t)D);
         const uint32_t bar = bar0 + 8u * (uint32_t)s;
         const uint32_t sx = stg0 + (uint32_t)(s * STAGE * (int)sizeof(T));
         fence_stage_refill();
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
         Norms3<T> qn;
         for (int off = 0; off < len; off += F) {
             const int nf = min(F, len - off);
-            const int s = (int)(cn & (uint32_t)(D - 1));
+            const int s = (int)(cn % (uint32_t)D);
             mbar_wait_a(bar0 + 8u * (uint32_t)s, (cn / (uint32_t)D) & 1u);
             const T* sx = stg + s * STAGE;
             const T* sh = sx + (kLoadX ? F * SR : 0);

@@ -22,7 +22,10 @@ __global__ void __launch_bounds__(256) ldg_sum(const float4* __restrict__ x, siz
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int D, int STAGE_BYTES>
+// PERM = 8: logical stage L of the warp stream maps to physical stage (L mod FR)·8 + L / FR
+// (FR = stages / 8), i.e. a warp's consecutive stages are 8 stages (16 KB) apart — the access
+// pattern of the tiled a2 pass (8 v-blocks of 2 KB per 16 KB).
+template <int D, int STAGE_BYTES, int PERM = 1>
 __global__ void __launch_bounds__(256) tma_ring(const char* __restrict__ x, size_t nbytes, float* out) {
     extern __shared__ __align__(128) unsigned char sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -35,13 +38,15 @@ __global__ void __launch_bounds__(256) tma_ring(const char* __restrict__ x, size
     const size_t nst = nbytes / STAGE_BYTES;
     const size_t gw = (size_t)blockIdx.x * nw + warp, tw = (size_t)gridDim.x * nw;
     const size_t per = (nst + tw - 1) / tw;
+    const size_t FR = nst / PERM;
+    auto phys = [&](size_t L) { return PERM == 1 ? L : (L % FR) * PERM + L / FR; };
     const size_t s0 = gw * per, s1 = s0 + per < nst ? s0 + per : nst;
     auto issue = [&](size_t st, int n) {
         const int s = n % D;
         const uint32_t bar = su32(&bars[s]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE_BYTES));
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(su32(ring + s * STAGE_BYTES)), "l"(x + st * STAGE_BYTES), "r"(STAGE_BYTES), "r"(bar) : "memory");
+                     ::"r"(su32(ring + s * STAGE_BYTES)), "l"(x + phys(st) * STAGE_BYTES), "r"(STAGE_BYTES), "r"(bar) : "memory");
     };
     int pn = 0;
     if (lane == 0)
@@ -66,7 +71,26 @@ __global__ void __launch_bounds__(256) tma_ring(const char* __restrict__ x, size
     if (acc == 123456.f) out[0] = acc;
 }
 
-int main() {
+template <int D, int SB, int PERM>
+void run_ring(const char* x, size_t nbytes, float* out, int nsm, int bps, int threads,
+              cudaEvent_t a, cudaEvent_t b) {
+    const size_t smem = 8 * D * (threads / 32) + (size_t)(threads / 32) * D * SB;
+    cudaFuncSetAttribute(tma_ring<D, SB, PERM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto fn = [&] { tma_ring<D, SB, PERM><<<nsm * bps, threads, smem>>>(x, nbytes, out); };
+    for (int w = 0; w < 3; ++w) fn();
+    cudaEventRecord(a);
+    const int reps = 10;
+    for (int r = 0; r < reps; ++r) fn();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("tma ring D%d %5dB perm%d %d CTA/SM x %2d warps (%3zu KB smem, %3d KB in flight/SM) %7.1f us %7.1f GB/s\n",
+           D, SB, PERM, bps, threads / 32, smem / 1024, bps * (threads / 32) * D * SB / 1024,
+           1e3 * ms / reps, nbytes / (ms / reps / 1e3) / 1e9);
+}
+
+int main(int argc, char** argv) {
     const size_t nbytes = 2147483648ull;
     char* x;
     float* out;
@@ -78,50 +102,18 @@ int main() {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    auto timeit = [&](const char* name, auto fn) {
-        for (int w = 0; w < 3; ++w) fn();
-        cudaEventRecord(a);
-        const int reps = 10;
-        for (int r = 0; r < reps; ++r) fn();
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms;
-        cudaEventElapsedTime(&ms, a, b);
-        printf("%-34s %8.1f us  %7.1f GB/s\n", name, 1e3 * ms / reps, nbytes / (ms / reps / 1e3) / 1e9);
-    };
-    for (int bps : {4, 8, 16}) {
-        char nm[64];
-        snprintf(nm, sizeof nm, "ldg_sum %d CTA/SM", bps);
-        timeit(nm, [&] { ldg_sum<<<nsm * bps, 256>>>((const float4*)x, nbytes / 16, out); });
-    }
-    {
-        constexpr int D = 4, SB = 2048;
-        const size_t smem = 8 * D * 8 + 8ull * D * SB;
-        cudaFuncSetAttribute(tma_ring<D, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        for (int bps : {1, 2, 3}) {
-            char nm[64];
-            snprintf(nm, sizeof nm, "tma ring D4 2KB %d CTA/SM", bps);
-            timeit(nm, [&] { tma_ring<D, SB><<<nsm * bps, 256, smem>>>(x, nbytes, out); });
-        }
-    }
-    {
-        constexpr int D = 8, SB = 2048;
-        const size_t smem = 8 * D * 8 + 8ull * D * SB;
-        cudaFuncSetAttribute(tma_ring<D, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int rep = 0; rep < 2; ++rep) {
         for (int bps : {1, 2}) {
-            char nm[64];
-            snprintf(nm, sizeof nm, "tma ring D8 2KB %d CTA/SM", bps);
-            timeit(nm, [&] { tma_ring<D, SB><<<nsm * bps, 256, smem>>>(x, nbytes, out); });
-        }
-    }
-    {
-        constexpr int D = 4, SB = 4096;
-        const size_t smem = 8 * D * 8 + 8ull * D * SB;
-        cudaFuncSetAttribute(tma_ring<D, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        for (int bps : {1, 2}) {
-            char nm[64];
-            snprintf(nm, sizeof nm, "tma ring D4 4KB %d CTA/SM", bps);
-            timeit(nm, [&] { tma_ring<D, SB><<<nsm * bps, 256, smem>>>(x, nbytes, out); });
+            for (int th : {256, 512}) {
+                if (bps * th > 1024) continue;
+                run_ring<2, 2048, 8>(x, nbytes, out, nsm, bps, th, a, b);
+                run_ring<4, 2048, 8>(x, nbytes, out, nsm, bps, th, a, b);
+                run_ring<4, 1024, 8>(x, nbytes, out, nsm, bps, th, a, b);
+                run_ring<8, 1024, 8>(x, nbytes, out, nsm, bps, th, a, b);
+                run_ring<3, 2048, 8>(x, nbytes, out, nsm, bps, th, a, b);
+                run_ring<2, 4096, 8>(x, nbytes, out, nsm, bps, th, a, b);
+                if (th == 256) run_ring<4, 4096, 8>(x, nbytes, out, nsm, bps, th, a, b);
+            }
         }
     }
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));

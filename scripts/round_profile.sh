@@ -1,11 +1,25 @@
 #!/bin/bash
-# Full bench + ncu evidence for profiles/: launch list of the bench command and a --set full
-# capture of the top kernels (one plain a2 pass, one tiled a2 pass, the refill).
+# Evidence for profiles/<TAG>/ (run from the repo root under gpurun, one GPU):
+#   1. full bench line (stdout JSON) and its stderr
+#   2. ncu launch list of the short bench command (gpu__time_duration per launch)
+#   3. ncu --set full of every launch of one plain-launch C5 sweep (20 a2 passes, reduces,
+#      solves, refill) -> per-kernel raw metrics + source hot spots of the top kernels;
+#      the .ncu-rep files are summarised on the box and deleted (size cap on gpurun_out/)
 TAG=${1:-r1}
-python bench.py > gpurun_out/bench_full_$TAG.json 2> gpurun_out/bench_full_$TAG.err
-python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-extras > gpurun_out/bench_short_$TAG.json 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-extras > gpurun_out/ncu_launches_$TAG.log 2>&1
-python scripts/ncu_target.py --config C5 --sweeps 1 > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:fiber_pass -s 0 -c 2 -o gpurun_out/full_$TAG python scripts/ncu_target.py --config C5 --sweeps 1 > gpurun_out/ncu_full_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:fiber_pass -s 20 -c 1 -o gpurun_out/full_refill_$TAG python scripts/ncu_target.py --config C5 --sweeps 1 >> gpurun_out/ncu_full_$TAG.log 2>&1
-ls -la gpurun_out | tail -12
+OUT=gpurun_out/prof_$TAG
+mkdir -p $OUT
+python bench.py > $OUT/bench_full.json 2> $OUT/bench_full.err
+python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-extras > $OUT/bench_short.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-extras > $OUT/ncu_launches.log 2>&1
+python scripts/launch_summary.py $OUT/launches.csv > $OUT/launches.txt 2>&1
+python scripts/ncu_target.py --config C5 --sweeps 1 > $OUT/ncu_target_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"fiber_pass|reduce_partials|block_solve|finalize" \
+    -c 62 -o $OUT/sweep -f python scripts/ncu_target.py --config C5 --sweeps 1 > $OUT/ncu_sweep.log 2>&1
+python scripts/ncu_summary.py $OUT/sweep.ncu-rep 0 > $OUT/ncu_sweep_summary.txt 2>&1
+python scripts/ncu_per_launch.py $OUT/sweep.ncu-rep > $OUT/ncu_sweep_per_launch.txt 2>&1
+for l in 0 1 5 60; do
+  python scripts/ncu_summary.py $OUT/sweep.ncu-rep $l > $OUT/ncu_src_launch$l.txt 2>&1
+done
+rm -f $OUT/sweep.ncu-rep
+ls -la $OUT
