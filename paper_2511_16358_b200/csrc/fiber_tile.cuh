@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
                             const int sl = (int)((uint32_t)(xw - P.Xw) & 127u);
                             const uint32_t bits = (SR == I1p) ? mask_bits_l(smw, sl + fo + eb)
                                                               : mask_bits_l(smw + f * MWF, ((sl + fo) & 127) + eb);
-                            refill_chunk<T, EPL>(x, tt, bits, P.rho, P.inv1p, xn, qn);
+                            refill_lite<T, EPL>(x, tt, bits, P.rho, P.inv1p, xn, qn);
                             store_chunk<T, EPL>(xw + fo + eb, xn, lane_full, ev);
                             accumulate<T, EPL>(w, xn, sb[st], sw[st]);
                         } else {

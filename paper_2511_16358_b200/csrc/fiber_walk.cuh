@@ -181,6 +181,32 @@ __device__ __forceinline__ void refill_chunk(const T (&x)[N], const T (&t)[N], u
     }
 }
 
+// Eq. 9 for the fused pass (a5 of sweep s inside a2(0,1) of sweep s+1; only used when the
+// sweep loop needs no stop test or trace): X_new plus q1 = ‖X_new‖², kept for the
+// non-finite check of the finaliser.
+template <typename T, int N>
+__device__ __forceinline__ void refill_lite(const T (&x)[N], const T (&t)[N], uint32_t bits, T rho,
+                                            T inv1p, T (&xn)[N], Norms3<T>& q) {
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+        const float2 r2 = make_float2(rho, rho), i2 = make_float2(inv1p, inv1p);
+#pragma unroll
+        for (int e = 0; e < N; e += 2) {
+            const float2 x2 = make_float2(x[e], x[e + 1]), t2 = make_float2(t[e], t[e + 1]);
+            const float2 u = __fmul2_rn(__ffma2_rn(r2, x2, t2), i2);  // (t + ρx)/(1 + ρ)
+            xn[e] = ((bits >> e) & 1u) ? x[e] : u.x;
+            xn[e + 1] = ((bits >> (e + 1)) & 1u) ? x[e + 1] : u.y;
+            const float2 n2 = make_float2(xn[e], xn[e + 1]);
+            q.q1 = __ffma2_rn(n2, n2, q.q1);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+            xn[e] = ((bits >> e) & 1u) ? x[e] : fma(rho, x[e], t[e]) * inv1p;
+            q.q1 = fma(xn[e], xn[e], q.q1);
+        }
+    }
+}
+
 // objective pass: q2 += (x − t)²
 template <typename T, int N>
 __device__ __forceinline__ void objective_chunk(const T (&x)[N], const T (&t)[N], Norms3<T>& q) {
@@ -521,7 +547,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                         for (int e = 0; e < EPL; ++e) t[e] = w[e] * h01v[e];
                         const int64_t gf = sg0 + (int64_t)f * xstep, ge = gf + eb;
                         const uint32_t bits = xmerge ? mask_bits_s(smw, sg0, ge) : mask_bits_s(smw + f * MWF, gf, ge);
-                        refill_chunk<T, EPL>(x, t, bits, P.rho, P.inv1p, xn, qn);
+                        refill_lite<T, EPL>(x, t, bits, P.rho, P.inv1p, xn, qn);
                         store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
                         accumulate<T, EPL>(w, xn, sb, sw);
                     } else if constexpr (kContract) {
