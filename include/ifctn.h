@@ -61,7 +61,7 @@ typedef enum {
 typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 
 #define IFCTN_MAX_ORDER 6
-#define IFCTN_MAX_RANK 8
+#define IFCTN_MAX_RANK 64
 
 /* ifctn_create flags */
 #define IFCTN_FLAG_NONE 0u

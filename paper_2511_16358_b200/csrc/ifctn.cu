@@ -348,6 +348,8 @@ struct BlockPlan {
     RedLaunch red_l;
     SolveParams<T> sol;
     dim3 sol_grid;
+    unsigned sol_threads = 128;
+    size_t sol_smem = 0;
     const void* sol_fn = nullptr;
     // multi-GPU, k ≠ shard mode: project → all-reduce → solve
     bool dist = false;
@@ -426,6 +428,13 @@ static const void* pick_solve_sm(int R) {
 
 template <typename T>
 static const void* pick_solve(int R, int sm = SOLVE_FULL) {
+    if (R > MAXR_SMALL) {
+        const void* fn = sm == SOLVE_PROJECT     ? (const void*)block_solve_big<T, SOLVE_PROJECT>
+                         : sm == SOLVE_FROM_PROJ ? (const void*)block_solve_big<T, SOLVE_FROM_PROJ>
+                                                 : (const void*)block_solve_big<T, SOLVE_FULL>;
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_solve_smem(MAXR)));
+        return fn;
+    }
     if (sm == SOLVE_PROJECT) return pick_solve_sm<T, SOLVE_PROJECT>(R);
     if (sm == SOLVE_FROM_PROJ) return pick_solve_sm<T, SOLVE_FROM_PROJ>(R);
     return pick_solve_sm<T, SOLVE_FULL>(R);
@@ -790,7 +799,13 @@ struct Solver : SolverBase {
                 q.delta = delta + s.delta_off[k][i];
                 q.flags = dflags;
                 q.proj = proj;
+                q.R = s.R(k, i);
                 b.sol_grid = dim3((unsigned)s.ld[k]);
+                if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): CTA-wide SYRK + Cholesky
+                    b.sol_threads = kBigSolveThreads;
+                    b.sol_smem = big_solve_smem(q.R);
+                    if (b.sol_smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "rank too large for the solve kernel");
+                }
                 b.dist = s.dpath && k != s.shard;
                 if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
                     const int R = s.R(k, i);
@@ -843,10 +858,10 @@ struct Solver : SolverBase {
 
     void enqueue_solve(const BlockPlan<T>& b) {
         if (b.dist) {
-            launch(b.proj_fn, b.sol_grid, dim3(128), 0, b.sol);
+            launch(b.proj_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, b.sol);
             allreduce_dev(proj, (size_t)b.proj_count);
         }
-        launch(b.sol_fn, b.sol_grid, dim3(128), 0, b.sol);
+        launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, b.sol);
     }
 
     void enqueue_block(const BlockPlan<T>& b) {

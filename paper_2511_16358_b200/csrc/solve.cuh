@@ -276,6 +276,215 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     }
 }
 
+// ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------
+// Same mathematics as block_solve (Eq. 8) with the rank a runtime value ≤ 64.
+// One CTA per column j:
+//   Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ as a register-tiled fp64 SYRK over a-tiles staged
+//   in shared memory (each thread one 4×4 tile of the upper triangle), rhs_j alongside;
+//   + ρI, ρc_old; a right-looking Cholesky in shared memory (one column per step, the
+//   trailing update spread over the CTA); forward/back substitution in warp 0; then the
+//   column is written, ‖Δc‖² recorded and row j of H_{k,i} refreshed.
+constexpr int kBigSolveThreads = 256;
+constexpr int kBigSolveTA = 32;  // a-tile (columns of G_{i,k} staged per step)
+
+__host__ __device__ inline int big_solve_rp(int R) { return (R + 3) & ~3; }
+__host__ __device__ inline size_t big_solve_smem(int R) {
+    const int Rp = big_solve_rp(R);
+    return sizeof(double) * ((size_t)Rp * Rp + 2 * (size_t)kBigSolveTA * Rp + kBigSolveTA + 3 * (size_t)Rp);
+}
+
+template <typename T, int SM>
+__global__ void __launch_bounds__(kBigSolveThreads) block_solve_big(const SolveParams<T> P) {
+    extern __shared__ __align__(16) double bsm[];
+    const int R = P.R, Rp = big_solve_rp(R);
+    const int NG = R * (R + 1) / 2;
+    const int NA = NG + R;
+    constexpr int TA = kBigSolveTA;
+    double* A = bsm;                 // Rp × Rp, row-major; Cholesky factor in the lower part
+    double* gs = A + Rp * Rp;        // TA × Rp: G_{i,k}(:, a)
+    double* gw = gs + TA * Rp;       // TA × Rp: ω(a, j)·G_{i,k}(:, a)
+    double* bt = gw + TA * Rp;       // TA: β(a, j)
+    double* rhs = bt + TA;           // Rp
+    double* cvec = rhs + Rp;         // Rp: solution (then its T-rounded value)
+    double* cold = cvec + Rp;        // Rp
+    __shared__ int ok;
+    const int64_t j = blockIdx.x;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int nt = Rp / 4;
+    const int ntiles = nt * (nt + 1) / 2;
+    // this thread's 4×4 tile (tr ≤ ts) of the upper triangle
+    int tr = -1, ts = -1;
+    if (tid < ntiles) {
+        int t = tid, row = 0;
+        while (t >= nt - row) {
+            t -= nt - row;
+            ++row;
+        }
+        tr = row;
+        ts = row + t;
+    }
+    if constexpr (SM != SOLVE_FROM_PROJ) {
+        double acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+        double racc = 0.0;
+        for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
+            const int na = (int)min((int64_t)TA, P.Ii - a0);
+            __syncthreads();  // previous tile consumed
+            for (int e = tid; e < TA * Rp; e += nthr) {
+                const int a = e / Rp, r = e - a * Rp;
+                double g = 0.0, w = 0.0;
+                if (a < na && r < R) {
+                    g = (double)P.Gik[(a0 + a) * R + r];
+                    w = g * P.omega[j * P.Ii + a0 + a];
+                }
+                gs[e] = g;
+                gw[e] = w;
+            }
+            for (int a = tid; a < TA; a += nthr) bt[a] = a < na ? P.beta[j * P.Ii + a0 + a] : 0.0;
+            __syncthreads();
+            if (tr >= 0) {
+                for (int a = 0; a < na; ++a) {
+                    const double* g = gs + a * Rp + 4 * tr;
+                    const double* w = gw + a * Rp + 4 * ts;
+                    const double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3];
+                    const double w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3];
+                    acc[0][0] = fma(g0, w0, acc[0][0]); acc[0][1] = fma(g0, w1, acc[0][1]);
+                    acc[0][2] = fma(g0, w2, acc[0][2]); acc[0][3] = fma(g0, w3, acc[0][3]);
+                    acc[1][0] = fma(g1, w0, acc[1][0]); acc[1][1] = fma(g1, w1, acc[1][1]);
+                    acc[1][2] = fma(g1, w2, acc[1][2]); acc[1][3] = fma(g1, w3, acc[1][3]);
+                    acc[2][0] = fma(g2, w0, acc[2][0]); acc[2][1] = fma(g2, w1, acc[2][1]);
+                    acc[2][2] = fma(g2, w2, acc[2][2]); acc[2][3] = fma(g2, w3, acc[2][3]);
+                    acc[3][0] = fma(g3, w0, acc[3][0]); acc[3][1] = fma(g3, w1, acc[3][1]);
+                    acc[3][2] = fma(g3, w2, acc[3][2]); acc[3][3] = fma(g3, w3, acc[3][3]);
+                }
+            }
+            if (tid < R)
+                for (int a = 0; a < na; ++a) racc = fma(bt[a], gs[a * Rp + tid], racc);
+        }
+        // Gram (both triangles) and rhs into shared memory
+        if (tr >= 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int r = 4 * tr + u, c = 4 * ts + v;
+                    A[r * Rp + c] = acc[u][v];
+                    A[c * Rp + r] = acc[u][v];
+                }
+        }
+        if (tid < R) rhs[tid] = racc;
+        __syncthreads();
+        if constexpr (SM == SOLVE_PROJECT) {
+            // this rank's partial [upper triangle (r ≤ s, row-major), rhs] for the all-reduce
+            for (int t = tid; t < NA; t += nthr) {
+                double v;
+                if (t < NG) {
+                    int r = 0, q = t;
+                    while (q >= R - r) {
+                        q -= R - r;
+                        ++r;
+                    }
+                    v = A[r * Rp + r + q];
+                } else {
+                    v = rhs[t - NG];
+                }
+                P.proj[j * NA + t] = v;
+            }
+            return;
+        }
+    } else {
+        for (int t = tid; t < NA; t += nthr) {
+            const double v = P.proj[j * NA + t];
+            if (t < NG) {
+                int r = 0, q = t;
+                while (q >= R - r) {
+                    q -= R - r;
+                    ++r;
+                }
+                A[r * Rp + r + q] = v;
+                A[(r + q) * Rp + r] = v;
+            } else {
+                rhs[t - NG] = v;
+            }
+        }
+        __syncthreads();
+    }
+    // + ρI, + ρ c_old
+    if (tid < R) {
+        const double co = (double)P.Gki[j * R + tid];
+        cold[tid] = co;
+        A[tid * Rp + tid] += P.rho;
+        rhs[tid] += P.rho * co;
+    }
+    if (tid == 0) ok = 1;
+    __syncthreads();
+    // right-looking Cholesky, lower factor in place
+    for (int cc = 0; cc < R; ++cc) {
+        if (tid == 0) {
+            const double d = A[cc * Rp + cc];
+            if (!(d > 0.0)) ok = 0;
+            A[cc * Rp + cc] = sqrt(d > 0.0 ? d : 1.0);
+        }
+        __syncthreads();
+        const double inv = 1.0 / A[cc * Rp + cc];
+        for (int r = cc + 1 + tid; r < R; r += nthr) A[r * Rp + cc] *= inv;
+        __syncthreads();
+        const int M = R - cc - 1;
+        for (int m = tid; m < M * M; m += nthr) {
+            const int r = cc + 1 + m / M, c = cc + 1 + m % M;
+            if (c <= r) A[r * Rp + c] = fma(-A[r * Rp + cc], A[c * Rp + cc], A[r * Rp + c]);
+        }
+        __syncthreads();
+    }
+    // L y = rhs, Lᵀ c = y (warp 0, column-oriented)
+    if (tid < 32) {
+        for (int r = 0; r < R; ++r) {
+            const double y = rhs[r] / A[r * Rp + r];
+            __syncwarp();
+            for (int q = r + 1 + tid; q < R; q += 32) rhs[q] = fma(-A[q * Rp + r], y, rhs[q]);
+            if (tid == 0) rhs[r] = y;
+            __syncwarp();
+        }
+        for (int r = R - 1; r >= 0; --r) {
+            const double c = rhs[r] / A[r * Rp + r];
+            __syncwarp();
+            for (int q = tid; q < r; q += 32) rhs[q] = fma(-A[r * Rp + q], c, rhs[q]);
+            if (tid == 0) cvec[r] = c;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (!ok) {
+        if (tid == 0) atomicOr(P.flags, 1);
+        if (tid < R) cvec[tid] = cold[tid];
+        __syncthreads();
+    }
+    if (tid < R) {
+        const T cT = (T)cvec[tid];
+        P.Gki[j * R + tid] = cT;
+        cvec[tid] = (double)cT;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double d2 = 0.0;
+        for (int r = 0; r < R; ++r) {
+            const double dd = cvec[r] - cold[r];
+            d2 += dd * dd;
+        }
+        P.delta[j] = d2;
+    }
+    // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a)
+    for (int64_t a = tid; a < P.Ii; a += nthr) {
+        double h = 0.0;
+        for (int r = 0; r < R; ++r) h = fma(cvec[r], (double)P.Gik[a * R + r], h);
+        const int64_t o = P.k_lt_i ? (P.h_off + a * P.h_ld + j) : (P.h_off + j * P.h_ld + a);
+        P.H[o] = (T)h;
+    }
+}
+
 // ---- a1: build H_{p,q} = G_{p,q}ᵀ G_{q,p} for one pair (K=R skinny product; FMA pipes) ---
 template <typename T>
 __global__ void pair_gram(const T* Gpq, const T* Gqp, int R, int64_t Ip, int64_t Iq, T* H,

@@ -227,6 +227,13 @@ CONFIGS = {
                 init_kind="uniform", sweeps=20),
     "C5s": dict(dims=(9, 8, 6, 5, 4), R=4, dtype="float32", truth_kind="normal", sr=0.20,
                 init_kind="normal", sweeps=10),
+    # Large-rank operating point of the paper's MSI grid: R_{1,2} = 36,
+    # R_{1,3} = R_{2,3} = 9, the largest values of P:L485, on the C2 recipe; and its
+    # oracle-speed twin.
+    "C2r": dict(dims=(256, 256, 31), R=[[0, 36, 9], [36, 0, 9], [9, 9, 0]], dtype="float32",
+                truth_kind="smooth", scale_noise=0.01, sr=0.10, init_kind="uniform", sweeps=100),
+    "C2rs": dict(dims=(40, 36, 7), R=[[0, 36, 9], [36, 0, 9], [9, 9, 0]], dtype="float32",
+                 truth_kind="smooth", scale_noise=0.01, sr=0.10, init_kind="uniform", sweeps=20),
 }
 
 

@@ -89,7 +89,7 @@ def test_sharded_sweeps_match_single_gpu(name, world, sweeps):
         assert out[r][1] == out[0][1]
 
 
-@pytest.mark.parametrize("name,world,mode", [("C3s", 2, 0), ("C4s", 2, 3), ("C2s", 3, 2)])
+@pytest.mark.parametrize("name,world,mode", [("C3s", 2, 0), ("C4s", 2, 3), ("C2s", 3, 2), ("C2rs", 2, 2)])
 def test_sharded_one_sweep_vs_oracle(name, world, mode):
     """Sharding along a chosen mode (including mode 1 = the fibre mode): one sweep, north-star
     bar against the float64 oracle."""
