@@ -329,6 +329,7 @@ def run_ours(args):
         line["cpu_baseline"] = oracle_cpu_baseline(p)
     if not args.no_extras and world == 1:
         line["other_configs"] = other_configs(torch)
+        line["rank_grid"] = rank_grid_extra(torch)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if tdist is not None:
@@ -372,7 +373,7 @@ def other_configs(torch):
     from paper_2511_16358_b200 import Solver
     from synth import make_config
     out = {}
-    for name in ("C1", "C2", "C3", "C4"):
+    for name in ("C1", "C2", "C3", "C4", "C2r"):
         p = make_config(name)
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
         s = Solver(p.dims, p.ranks, dev(p.observed), dev(p.mask), dev(p.G0), rho=p.rho)
@@ -385,10 +386,46 @@ def other_configs(torch):
         sps = p.sweeps / (ms / 1e3)
         out[name] = {"dims": list(p.dims), "dtype": str(p.dtype), "sweeps_timed": p.sweeps,
                      "sweeps_per_s": sps, "us_per_sweep": 1e3 * ms / p.sweeps,
+                     "ranks_max": int(p.ranks.max()),
                      "profiled_kernel_us_per_sweep": 1e3 * sum(prof),
+                     # launches per block are (a2 pass, reduce, solve): the a3/a4 share
+                     "profiled_solve_us_per_sweep": 1e3 * sum(prof[3 * b + 2]
+                                                              for b in range(p.N * (p.N - 1))),
                      "effective_gbs": bytes_per_sweep(p.dims, p.N, p.dtype.itemsize) * sps / 1e9,
                      "rse_after_3_plus_timed": rse,
                      "regime": "launch/latency-bound" if name == "C1" else "L2-resident"}
+    return out
+
+
+def rank_grid_extra(torch):
+    """the paper's MSI rank grid (P:L485, 18 instances) on the C2 recipe, 100
+    sweeps each, through ifctn_grid_run at concurrency 1 and 8 (wall time of the whole grid,
+    inputs resident, contexts created inside the timed region)."""
+    import time as _t
+
+    from paper_2511_16358_b200.grid import rank_grid
+    from synth import MSI_GRID, grid_rank_matrix, init_factors, make_config
+    p = make_config("C2")
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    inst = []
+    for (r12, r3) in MSI_GRID:
+        R = grid_rank_matrix(r12, r3)
+        g, _ = init_factors(p.dims, R, p.observed, p.mask, p.dtype, "uniform", 0)
+        inst.append(dict(ranks=R, rho=p.rho, init=dev(g)))
+    obs, mask, truth = dev(p.observed), dev(p.mask), dev(p.truth)
+    out = {"workload": "C2 recipe x MSI rank grid (P:L485): R12 in {3,6,9,15,30,36} x R13=R23 in {3,6,9}",
+           "instances": len(inst), "sweeps_per_instance": p.sweeps}
+    rank_grid(p.dims, obs, mask, inst[:2], 2, truth=truth, concurrency=2)   # warm-up
+    for conc in (1, 8):
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        res = rank_grid(p.dims, obs, mask, inst, p.sweeps, truth=truth, concurrency=conc)
+        torch.cuda.synchronize()
+        el = _t.perf_counter() - t0
+        best = min(range(len(res)), key=lambda q: res[q]["rse"])
+        out[f"concurrency_{conc}"] = {"seconds": el, "instances_per_s": len(inst) / el,
+                                      "sweeps_per_s": len(inst) * p.sweeps / el,
+                                      "best_rse": res[best]["rse"], "best_ranks": list(MSI_GRID[best])}
     return out
 
 

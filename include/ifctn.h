@@ -190,6 +190,42 @@ ifctn_status ifctn_profile_sweep(ifctn_ctx* ctx, float* ms, int capacity, int* c
 /* Kernel launches the last ifctn_sweep enqueued (graph nodes count as launches).         */
 int64_t ifctn_launch_count(const ifctn_ctx* ctx);
 
+/* ---- Multi-instance driver: the paper's rank-grid protocol -------------
+ * The paper reports its runtimes "including the time required to tune all parameters"
+ * over rank grids such as R_{1,2} ∈ {3,6,9,15,30,36}, R_{1,3} = R_{2,3} ∈ {3,6,9}
+ * (P:L485-486).  ifctn_grid_run solves `count` independent instances that share O, Ω (and
+ * the truth for the RSE) and differ in ranks, ρ and G⁰, `concurrency` of them at a time on
+ * one GPU, each in its own context on its own CUDA stream (small instances are launch- and
+ * latency-bound, so concurrent streams fill the GPU).  Instances run in waves of
+ * `concurrency`; every instance is bit-identical to a lone ifctn_create + ifctn_sweep(t_max,
+ * eps = 0) run (same kernels, deterministic reductions).  Workspaces are allocated once per
+ * slot (the largest instance's size) and reused.  Multi-GPU: give every process its own
+ * slice of the instance list (no communication; bench/grid.py partitions and gathers).
+ *   observed, mask, truth   as in ifctn_create / ifctn_rse (host or device); truth may be
+ *                           NULL (results[].rse = NaN)
+ *   instances[count]        ranks (order×order), ρ and G⁰ of each instance (caller-owned)
+ *   t_max                   sweeps per instance (≥ 1); no stop test
+ *   concurrency             instances resident at once (≥ 1)
+ *   results[count]          per instance: final RSE, objective ½‖X − t‖², device seconds of
+ *                           its sweeps, and its status (the call returns the first failure) */
+typedef struct {
+    const int32_t* ranks;
+    double rho;
+    const void* init_factors;
+} ifctn_instance;
+
+typedef struct {
+    double rse;
+    double objective;
+    double seconds;
+    int status;
+} ifctn_instance_result;
+
+ifctn_status ifctn_grid_run(int order, const int64_t* dims, ifctn_dtype dtype,
+                            const void* observed, const uint8_t* mask, const void* truth,
+                            const ifctn_instance* instances, int count, int t_max,
+                            int concurrency, ifctn_instance_result* results);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,16 @@ class ifctn_trace_row(ctypes.Structure):
                 ("objective", ctypes.c_double), ("dx2", ctypes.c_double), ("dg2", ctypes.c_double)]
 
 
+class ifctn_instance(ctypes.Structure):
+    _fields_ = [("ranks", ctypes.POINTER(ctypes.c_int32)), ("rho", ctypes.c_double),
+                ("init_factors", ctypes.c_void_p)]
+
+
+class ifctn_instance_result(ctypes.Structure):
+    _fields_ = [("rse", ctypes.c_double), ("objective", ctypes.c_double),
+                ("seconds", ctypes.c_double), ("status", ctypes.c_int)]
+
+
 _lib = None
 
 # name -> (restype, argtypes); the exported C-ABI (checked against include/ifctn.h by tests)
@@ -71,6 +81,8 @@ SIGNATURES = {
     "ifctn_status_string": (ctypes.c_char_p, [_I]),
     "ifctn_last_error": (ctypes.c_char_p, [_VP]),
     "ifctn_launch_count": (ctypes.c_int64, [_VP]),
+    "ifctn_grid_run": (_I, [_I, _I64P, _I, _VP, _VP, _VP, ctypes.POINTER(ifctn_instance), _I, _I, _I,
+                            ctypes.POINTER(ifctn_instance_result)]),
 }
 
 
@@ -198,3 +210,26 @@ def ifctn_last_error(ctx=None) -> str:
 
 def ifctn_launch_count(ctx) -> int:
     return int(lib().ifctn_launch_count(ctx))
+
+
+def ifctn_grid_run(order, dims, dtype, observed_ptr, mask_ptr, truth_ptr, instances, t_max,
+                   concurrency):
+    """instances: list of (ranks_flat, rho, init_ptr); returns a list of result dicts."""
+    n = len(instances)
+    arr = (ifctn_instance * max(n, 1))()
+    keep = []
+    for q, (ranks_flat, rho, init_ptr) in enumerate(instances):
+        r = _i32arr(ranks_flat)
+        keep.append(r)
+        arr[q].ranks = ctypes.cast(r, ctypes.POINTER(ctypes.c_int32))
+        arr[q].rho = float(rho)
+        arr[q].init_factors = init_ptr
+    res = (ifctn_instance_result * max(n, 1))()
+    st = lib().ifctn_grid_run(order, _i64arr(dims), dtype, observed_ptr, mask_ptr, truth_ptr, arr, n,
+                              int(t_max), int(concurrency), res)
+    out = [dict(rse=res[q].rse, objective=res[q].objective, seconds=res[q].seconds,
+                status=res[q].status) for q in range(n)]
+    if st != 0:
+        msg = lib().ifctn_last_error(None)
+        raise IfctnError(st, (msg.decode() if msg else "") + f" (per-instance: {[o['status'] for o in out]})")
+    return out

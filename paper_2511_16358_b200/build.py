@@ -8,6 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ifctn.cu")
+SRCS = [SRC, os.path.join(HERE, "csrc", "grid.cu")]
 OUT = os.path.join(HERE, "libifctn.so")
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
        [os.path.join(ROOT, "include", "ifctn.h")]
@@ -29,7 +30,7 @@ def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [nvcc] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", tmp, SRC, "-ldl"]
+    cmd = [nvcc] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", tmp] + SRCS + ["-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -432,7 +432,6 @@ static const void* pick_solve(int R, int sm = SOLVE_FULL) {
         const void* fn = sm == SOLVE_PROJECT     ? (const void*)block_solve_big<T, SOLVE_PROJECT>
                          : sm == SOLVE_FROM_PROJ ? (const void*)block_solve_big<T, SOLVE_FROM_PROJ>
                                                  : (const void*)block_solve_big<T, SOLVE_FULL>;
-        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_solve_smem(MAXR)));
         return fn;
     }
     if (sm == SOLVE_PROJECT) return pick_solve_sm<T, SOLVE_PROJECT>(R);
@@ -801,10 +800,21 @@ struct Solver : SolverBase {
                 q.proj = proj;
                 q.R = s.R(k, i);
                 b.sol_grid = dim3((unsigned)s.ld[k]);
-                if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): CTA-wide SYRK + Cholesky
-                    b.sol_threads = kBigSolveThreads;
-                    b.sol_smem = big_solve_smem(q.R);
+                if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): a CTA per column
+                    b.sol_threads = kBigThreads;
+                    // stage all of G_{i,k} at once when it fits in ≈ 96 KB, else 32-column tiles
+                    const size_t cap = std::min<size_t>(smem_limit - 8 * 1024, 96 * 1024);
+                    q.ta = (int)s.ld[i];
+                    if (big_solve_smem(q.R, q.ta, (int)s.esize) > cap) q.ta = 32;
+                    b.sol_smem = big_solve_smem(q.R, q.ta, (int)s.esize);
                     if (b.sol_smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "rank too large for the solve kernel");
+                    for (int m = 0; m < 3; ++m) {  // allow the device maximum (static smem aside)
+                        const void* fn = pick_solve<T>(q.R, m);
+                        cudaFuncAttributes fa;
+                        CU(cudaFuncGetAttributes(&fa, fn));
+                        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(smem_limit - fa.sharedSizeBytes)));
+                    }
                 }
                 b.dist = s.dpath && k != s.shard;
                 if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
@@ -1032,8 +1042,10 @@ struct Solver : SolverBase {
     void check_flags_sync() {
         CU(cudaMemcpyAsync(hflags, dflags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
+#ifndef IFCTN_EXP_NOCHECK  // timing experiments with parts of a kernel switched off
         if (hflags[0]) fail(IFCTN_E_NOT_SPD, "non-positive Cholesky pivot in a column solve");
         if (hflags[1]) fail(IFCTN_E_NONFINITE, "non-finite value in the sweep norms");
+#endif
     }
 
     void sweep(int t_max, double eps, int* done, ifctn_trace_row* trace) override {

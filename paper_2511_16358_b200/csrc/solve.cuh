@@ -278,51 +278,63 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
 
 // ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------
 // Same mathematics as block_solve (Eq. 8) with the rank a runtime value ≤ 64.
-// One CTA per column j:
-//   Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ as a register-tiled fp64 SYRK over a-tiles staged
-//   in shared memory (each thread one 4×4 tile of the upper triangle), rhs_j alongside;
-//   + ρI, ρc_old; a right-looking Cholesky in shared memory (one column per step, the
-//   trailing update spread over the CTA); forward/back substitution in warp 0; then the
-//   column is written, ‖Δc‖² recorded and row j of H_{k,i} refreshed.
-constexpr int kBigSolveThreads = 256;
-constexpr int kBigSolveTA = 32;  // a-tile (columns of G_{i,k} staged per step)
+// One CTA (256 threads) per column j:
+//   * G_{i,k} is staged in shared memory in tiles of `ta` columns a — normally all of it at
+//     once (one round of loads in flight), reused by the H refresh;
+//   * Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ: task = (4×4 tile of the upper triangle,
+//     a-residue h mod KS), KS = the a-split that fills the CTA; the KS partial tiles are
+//     added into the Gram in h order (fixed order, deterministic); rhs_j alongside;
+//   * warp 0: + ρI, ρ c_old, Cholesky (one column per step, lanes own rows, the pivot column
+//     scaled after the trailing update, inverse pivots kept on the diagonal), forward/back
+//     substitution, the column and ‖Δc‖²;
+//   * row j of H_{k,i} (8 threads per a).
+constexpr int kBigThreads = 256;
+constexpr int kBigEnt = 9;  // ⌈64·65/2 / 256⌉ lower-triangle entries per thread
 
 __host__ __device__ inline int big_solve_rp(int R) { return (R + 3) & ~3; }
-__host__ __device__ inline size_t big_solve_smem(int R) {
+// shared memory: G tile (ta·R + Rp values of T, 16-B rounded) + fp64 [Gram Rp², ω, β (ta each),
+// rhs, c, c_old (Rp each)]
+__host__ __device__ inline size_t big_solve_smem(int R, int ta, int esize) {
     const int Rp = big_solve_rp(R);
-    return sizeof(double) * ((size_t)Rp * Rp + 2 * (size_t)kBigSolveTA * Rp + kBigSolveTA + 3 * (size_t)Rp);
+    const size_t g = (((size_t)ta * R + Rp) * esize + 15) & ~(size_t)15;
+    return g + sizeof(double) * ((size_t)Rp * Rp + 2 * (size_t)ta + 3 * (size_t)Rp);
 }
 
 template <typename T, int SM>
-__global__ void __launch_bounds__(kBigSolveThreads) block_solve_big(const SolveParams<T> P) {
+__global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
     extern __shared__ __align__(16) double bsm[];
-    const int R = P.R, Rp = big_solve_rp(R);
-    const int NG = R * (R + 1) / 2;
-    const int NA = NG + R;
-    constexpr int TA = kBigSolveTA;
-    double* A = bsm;                 // Rp × Rp, row-major; Cholesky factor in the lower part
-    double* gs = A + Rp * Rp;        // TA × Rp: G_{i,k}(:, a)
-    double* gw = gs + TA * Rp;       // TA × Rp: ω(a, j)·G_{i,k}(:, a)
-    double* bt = gw + TA * Rp;       // TA: β(a, j)
-    double* rhs = bt + TA;           // Rp
-    double* cvec = rhs + Rp;         // Rp: solution (then its T-rounded value)
-    double* cold = cvec + Rp;        // Rp
+    const int R = P.R, Rp = big_solve_rp(R), TA = P.ta;
+    const int NG = R * (R + 1) / 2, NA = NG + R;
+    T* gs = reinterpret_cast<T*>(bsm);  // G_{i,k}(:, a0 .. a0+ta), row stride R
+    double* A = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(bsm) +
+                                          ((((size_t)TA * R + Rp) * sizeof(T) + 15) & ~(size_t)15));
+    double* om = A + Rp * Rp;        // ω(a, j)
+    double* be = om + TA;            // β(a, j)
+    double* rhs = be + TA;
+    double* cv = rhs + Rp;
+    double* cold = cv + Rp;
     __shared__ int ok;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int64_t j = blockIdx.x;
-    const int tid = threadIdx.x, nthr = blockDim.x;
     const int nt = Rp / 4;
     const int ntiles = nt * (nt + 1) / 2;
-    // this thread's 4×4 tile (tr ≤ ts) of the upper triangle
-    int tr = -1, ts = -1;
-    if (tid < ntiles) {
-        int t = tid, row = 0;
-        while (t >= nt - row) {
-            t -= nt - row;
-            ++row;
+    const int KS = max(1, min(8, nthr / ntiles));   // a-split per tile
+    const int task_t = tid % ntiles, task_h = tid / ntiles;
+    const bool has_task = task_h < KS;
+    const bool one_tile = (int64_t)TA >= P.Ii;
+    int tr = 0, ts = 0;
+    if (has_task) {
+        int q = task_t;
+        while (q >= nt - tr) {
+            q -= nt - tr;
+            ++tr;
         }
-        tr = row;
-        ts = row + t;
+        ts = tr + q;
     }
+    auto stage = [&](int64_t a0, int na) {
+        for (int e = tid; e < na * R; e += nthr) gs[e] = P.Gik[a0 * R + e];
+        for (int e = na * R + tid; e < na * R + Rp; e += nthr) gs[e] = T(0);  // 4-wide over-read
+    };
     if constexpr (SM != SOLVE_FROM_PROJ) {
         double acc[4][4];
 #pragma unroll
@@ -332,48 +344,49 @@ __global__ void __launch_bounds__(kBigSolveThreads) block_solve_big(const SolveP
         double racc = 0.0;
         for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
             const int na = (int)min((int64_t)TA, P.Ii - a0);
-            __syncthreads();  // previous tile consumed
-            for (int e = tid; e < TA * Rp; e += nthr) {
-                const int a = e / Rp, r = e - a * Rp;
-                double g = 0.0, w = 0.0;
-                if (a < na && r < R) {
-                    g = (double)P.Gik[(a0 + a) * R + r];
-                    w = g * P.omega[j * P.Ii + a0 + a];
-                }
-                gs[e] = g;
-                gw[e] = w;
-            }
-            for (int a = tid; a < TA; a += nthr) bt[a] = a < na ? P.beta[j * P.Ii + a0 + a] : 0.0;
             __syncthreads();
-            if (tr >= 0) {
-                for (int a = 0; a < na; ++a) {
-                    const double* g = gs + a * Rp + 4 * tr;
-                    const double* w = gw + a * Rp + 4 * ts;
-                    const double g0 = g[0], g1 = g[1], g2 = g[2], g3 = g[3];
-                    const double w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3];
-                    acc[0][0] = fma(g0, w0, acc[0][0]); acc[0][1] = fma(g0, w1, acc[0][1]);
-                    acc[0][2] = fma(g0, w2, acc[0][2]); acc[0][3] = fma(g0, w3, acc[0][3]);
-                    acc[1][0] = fma(g1, w0, acc[1][0]); acc[1][1] = fma(g1, w1, acc[1][1]);
-                    acc[1][2] = fma(g1, w2, acc[1][2]); acc[1][3] = fma(g1, w3, acc[1][3]);
-                    acc[2][0] = fma(g2, w0, acc[2][0]); acc[2][1] = fma(g2, w1, acc[2][1]);
-                    acc[2][2] = fma(g2, w2, acc[2][2]); acc[2][3] = fma(g2, w3, acc[2][3]);
-                    acc[3][0] = fma(g3, w0, acc[3][0]); acc[3][1] = fma(g3, w1, acc[3][1]);
-                    acc[3][2] = fma(g3, w2, acc[3][2]); acc[3][3] = fma(g3, w3, acc[3][3]);
+            stage(a0, na);
+            for (int a = tid; a < na; a += nthr) {
+                om[a] = P.omega[j * P.Ii + a0 + a];
+                be[a] = P.beta[j * P.Ii + a0 + a];
+            }
+            __syncthreads();
+            if (has_task) {
+                for (int a = task_h; a < na; a += KS) {
+                    const double w = om[a];
+                    const T* gr = gs + a * R + 4 * tr;
+                    const T* gc = gs + a * R + 4 * ts;
+                    const double r0 = w * (double)gr[0], r1 = w * (double)gr[1], r2 = w * (double)gr[2],
+                                 r3 = w * (double)gr[3];
+                    const double c0 = (double)gc[0], c1 = (double)gc[1], c2 = (double)gc[2], c3 = (double)gc[3];
+                    acc[0][0] = fma(r0, c0, acc[0][0]); acc[0][1] = fma(r0, c1, acc[0][1]);
+                    acc[0][2] = fma(r0, c2, acc[0][2]); acc[0][3] = fma(r0, c3, acc[0][3]);
+                    acc[1][0] = fma(r1, c0, acc[1][0]); acc[1][1] = fma(r1, c1, acc[1][1]);
+                    acc[1][2] = fma(r1, c2, acc[1][2]); acc[1][3] = fma(r1, c3, acc[1][3]);
+                    acc[2][0] = fma(r2, c0, acc[2][0]); acc[2][1] = fma(r2, c1, acc[2][1]);
+                    acc[2][2] = fma(r2, c2, acc[2][2]); acc[2][3] = fma(r2, c3, acc[2][3]);
+                    acc[3][0] = fma(r3, c0, acc[3][0]); acc[3][1] = fma(r3, c1, acc[3][1]);
+                    acc[3][2] = fma(r3, c2, acc[3][2]); acc[3][3] = fma(r3, c3, acc[3][3]);
                 }
             }
             if (tid < R)
-                for (int a = 0; a < na; ++a) racc = fma(bt[a], gs[a * Rp + tid], racc);
+                for (int a = 0; a < na; ++a) racc = fma(be[a], (double)gs[a * R + tid], racc);
         }
-        // Gram (both triangles) and rhs into shared memory
-        if (tr >= 0) {
+        // Gram = Σ_h partial tiles, h ascending; both triangles
+        for (int e = tid; e < Rp * Rp; e += nthr) A[e] = 0.0;
+        for (int h = 0; h < KS; ++h) {
+            __syncthreads();
+            if (has_task && task_h == h) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int r = 4 * tr + u, c = 4 * ts + v;
-                    A[r * Rp + c] = acc[u][v];
-                    A[c * Rp + r] = acc[u][v];
-                }
+                    for (int v = 0; v < 4; ++v) A[(4 * tr + u) * Rp + 4 * ts + v] += acc[u][v];
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < R * R; e += nthr) {
+            const int r = e / R, c = e - r * R;
+            if (c < r) A[r * Rp + c] = A[c * Rp + r];
         }
         if (tid < R) rhs[tid] = racc;
         __syncthreads();
@@ -396,6 +409,7 @@ __global__ void __launch_bounds__(kBigSolveThreads) block_solve_big(const SolveP
             return;
         }
     } else {
+        if (one_tile) stage(0, (int)P.Ii);  // for the H refresh
         for (int t = tid; t < NA; t += nthr) {
             const double v = P.proj[j * NA + t];
             if (t < NG) {
@@ -421,67 +435,130 @@ __global__ void __launch_bounds__(kBigSolveThreads) block_solve_big(const SolveP
     }
     if (tid == 0) ok = 1;
     __syncthreads();
-    // right-looking Cholesky, lower factor in place
-    for (int cc = 0; cc < R; ++cc) {
-        if (tid == 0) {
-            const double d = A[cc * Rp + cc];
-            if (!(d > 0.0)) ok = 0;
-            A[cc * Rp + cc] = sqrt(d > 0.0 ? d : 1.0);
+    // Cholesky with the lower triangle in registers: thread t owns entries m = t + q·256 of
+    // the packed lower triangle (row-major, (r, c) with c ≤ r), at most kBigEnt of them.
+    // Step cc: the owner of (cc, cc) publishes 1/sqrt(d); owners of (r, cc) publish
+    // l_r = A_r,cc/sqrt(d) (parity-double-buffered column); every owner of (r, c), c > cc,
+    // subtracts l_r·l_c.  Two barriers per step, no shared-memory read-modify-write chains.
+    {
+        __shared__ double colb[2][64];
+        __shared__ double dinv;
+        int er[kBigEnt], ec[kBigEnt];
+        double ev[kBigEnt];
+        const int NL = NG;  // lower-triangle entries
+#pragma unroll
+        for (int q = 0; q < kBigEnt; ++q) {
+            const int m = tid + q * kBigThreads;
+            int r = 0, c = 0;
+            if (m < NL) {  // m = r(r+1)/2 + c
+                r = (int)((sqrt(8.0 * m + 1.0) - 1.0) * 0.5);
+                while ((r + 1) * (r + 2) / 2 <= m) ++r;
+                while (r * (r + 1) / 2 > m) --r;
+                c = m - r * (r + 1) / 2;
+            }
+            er[q] = m < NL ? r : -1;
+            ec[q] = c;
+            ev[q] = m < NL ? A[r * Rp + c] : 0.0;
         }
-        __syncthreads();
-        const double inv = 1.0 / A[cc * Rp + cc];
-        for (int r = cc + 1 + tid; r < R; r += nthr) A[r * Rp + cc] *= inv;
-        __syncthreads();
-        const int M = R - cc - 1;
-        for (int m = tid; m < M * M; m += nthr) {
-            const int r = cc + 1 + m / M, c = cc + 1 + m % M;
-            if (c <= r) A[r * Rp + c] = fma(-A[r * Rp + cc], A[c * Rp + cc], A[r * Rp + c]);
+        bool okl = true;
+        for (int cc = 0; cc < R; ++cc) {
+            double* col = colb[cc & 1];
+#pragma unroll
+            for (int q = 0; q < kBigEnt; ++q)
+                if (er[q] == cc && ec[q] == cc) {
+                    const double d = ev[q];
+                    okl = d > 0.0;
+                    const double inv = 1.0 / sqrt(d > 0.0 ? d : 1.0);
+                    dinv = inv;
+                    ev[q] = inv;  // the diagonal keeps 1/L_cc
+                    if (!okl) ok = 0;
+                }
+            __syncthreads();
+            const double inv = dinv;
+#pragma unroll
+            for (int q = 0; q < kBigEnt; ++q)
+                if (ec[q] == cc && er[q] > cc) {
+                    ev[q] *= inv;
+                    col[er[q]] = ev[q];
+                }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < kBigEnt; ++q)
+                if (ec[q] > cc) ev[q] = fma(-col[er[q]], col[ec[q]], ev[q]);
         }
+#pragma unroll
+        for (int q = 0; q < kBigEnt; ++q)
+            if (er[q] >= 0) A[er[q] * Rp + ec[q]] = ev[q];
         __syncthreads();
     }
-    // L y = rhs, Lᵀ c = y (warp 0, column-oriented)
     if (tid < 32) {
+        // L y = rhs, Lᵀ c = y with rhs in registers (lane owns rows lane, lane + 32) and the
+        // pivot value broadcast by shuffle; the L entries are independent shared loads
+        double x0 = lane < R ? rhs[lane] : 0.0, x1 = lane + 32 < R ? rhs[lane + 32] : 0.0;
         for (int r = 0; r < R; ++r) {
-            const double y = rhs[r] / A[r * Rp + r];
-            __syncwarp();
-            for (int q = r + 1 + tid; q < R; q += 32) rhs[q] = fma(-A[q * Rp + r], y, rhs[q]);
-            if (tid == 0) rhs[r] = y;
-            __syncwarp();
+            const double lq0 = lane > r && lane < R ? A[lane * Rp + r] : 0.0;
+            const double lq1 = lane + 32 > r && lane + 32 < R ? A[(lane + 32) * Rp + r] : 0.0;
+            const double own = (r < 32 ? x0 : x1) * A[r * Rp + r];
+            const double y = __shfl_sync(0xffffffffu, own, r & 31);
+            if (lane == (r & 31)) {
+                if (r < 32) x0 = y;
+                else x1 = y;
+            }
+            x0 = fma(-lq0, y, x0);
+            x1 = fma(-lq1, y, x1);
         }
         for (int r = R - 1; r >= 0; --r) {
-            const double c = rhs[r] / A[r * Rp + r];
-            __syncwarp();
-            for (int q = tid; q < r; q += 32) rhs[q] = fma(-A[r * Rp + q], c, rhs[q]);
-            if (tid == 0) cvec[r] = c;
-            __syncwarp();
+            const double lr0 = lane < r ? A[r * Rp + lane] : 0.0;
+            const double lr1 = lane + 32 < r ? A[r * Rp + lane + 32] : 0.0;
+            const double own = (r < 32 ? x0 : x1) * A[r * Rp + r];
+            const double c = __shfl_sync(0xffffffffu, own, r & 31);
+            if (lane == (r & 31)) {
+                if (r < 32) x0 = c;
+                else x1 = c;
+            }
+            x0 = fma(-lr0, c, x0);
+            x1 = fma(-lr1, c, x1);
         }
-    }
-    __syncthreads();
-    if (!ok) {
-        if (tid == 0) atomicOr(P.flags, 1);
-        if (tid < R) cvec[tid] = cold[tid];
-        __syncthreads();
-    }
-    if (tid < R) {
-        const T cT = (T)cvec[tid];
-        P.Gki[j * R + tid] = cT;
-        cvec[tid] = (double)cT;
-    }
-    __syncthreads();
-    if (tid == 0) {
+        if (lane < R) cv[lane] = x0;
+        if (lane + 32 < R) cv[lane + 32] = x1;
+        __syncwarp();
+        if (!ok) {
+            if (lane == 0) atomicOr(P.flags, 1);
+            for (int r = lane; r < R; r += 32) cv[r] = cold[r];
+        }
+        __syncwarp();
         double d2 = 0.0;
-        for (int r = 0; r < R; ++r) {
-            const double dd = cvec[r] - cold[r];
+        for (int r = lane; r < R; r += 32) {
+            const T cT = (T)cv[r];
+            P.Gki[j * R + r] = cT;
+            const double dd = (double)cT - cold[r];
             d2 += dd * dd;
+            cv[r] = (double)cT;
         }
-        P.delta[j] = d2;
+        d2 = warp_sum(d2);
+        if (lane == 0) P.delta[j] = d2;
     }
-    // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a)
-    for (int64_t a = tid; a < P.Ii; a += nthr) {
-        double h = 0.0;
-        for (int r = 0; r < R; ++r) h = fma(cvec[r], (double)P.Gik[a * R + r], h);
-        const int64_t o = P.k_lt_i ? (P.h_off + a * P.h_ld + j) : (P.h_off + j * P.h_ld + a);
-        P.H[o] = (T)h;
+    // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a), 8 threads per a
+    const int row8 = tid >> 3, sub8 = tid & 7;
+    for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
+        const int na = (int)min((int64_t)TA, P.Ii - a0);
+        __syncthreads();
+        if (!one_tile) {
+            stage(a0, na);
+            __syncthreads();
+        }
+        for (int a = row8; a < na; a += nthr >> 3) {
+            double h = 0.0;
+            for (int r = sub8; r < R; r += 8) h = fma(cv[r], (double)gs[a * R + r], h);
+            h += __shfl_xor_sync(0xffffffffu, h, 1);
+            h += __shfl_xor_sync(0xffffffffu, h, 2);
+            h += __shfl_xor_sync(0xffffffffu, h, 4);
+            if (sub8 == 0) {
+                const int64_t ag = a0 + a;
+                const int64_t o = P.k_lt_i ? (P.h_off + ag * P.h_ld + j) : (P.h_off + j * P.h_ld + ag);
+                P.H[o] = (T)h;
+            }
+        }
     }
 }
 

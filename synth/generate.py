@@ -152,6 +152,36 @@ def _truth_factors(kind: str, dims, ranks, rng) -> dict:
     return G
 
 
+def init_factors(dims, ranks, observed, mask, dtype, init_kind="uniform", seed=0):
+    """G⁰ (stream seed+1) for the given rank matrix: N(0,1), or U[0,s) with
+    s = (m·4^P / Π_{p<q} R_{p,q})^{1/(2P)}, m = mean |O| on Ω (reading R8)."""
+    dims = tuple(int(d) for d in dims)
+    N = len(dims)
+    ranks = np.asarray(ranks)
+    rng1 = _rng(seed, 1)
+    P = N * (N - 1) // 2
+    sizes = factor_sizes(dims, ranks)
+    total = sum(R_ * Ik for (_, _, R_, Ik) in sizes)
+    if init_kind == "normal":
+        G0 = rng1.standard_normal(total)
+        irec = {"kind": "normal"}
+    else:
+        m = float(np.mean(np.abs(observed[mask.astype(bool)].astype(np.float64))))
+        pr = float(np.prod([ranks[p][q] for p in range(N) for q in range(p + 1, N)]))
+        s = (m * 4.0 ** P / pr) ** (1.0 / (2 * P))
+        G0 = rng1.uniform(0.0, s, total)
+        irec = {"kind": "uniform", "s": s}
+    return G0.astype(dtype), irec
+
+
+# The paper's MSI rank grid (P:L485): R_{1,2} ∈ {3,6,9,15,30,36}, R_{1,3} = R_{2,3} ∈ {3,6,9}
+MSI_GRID = [(r12, r3) for r12 in (3, 6, 9, 15, 30, 36) for r3 in (3, 6, 9)]
+
+
+def grid_rank_matrix(r12: int, r3: int) -> np.ndarray:
+    return np.array([[0, r12, r3], [r12, 0, r3], [r3, r3, 0]], np.int32)
+
+
 def make_problem(name, dims, R, dtype, truth_kind, *, scale_noise=None, mask_kind="uniform",
                  sr=None, fibre_missing_ratio=None, fibre_mode=2, init_kind="normal",
                  rho=0.1, sweeps=10, seed=0) -> Problem:
@@ -183,20 +213,7 @@ def make_problem(name, dims, R, dtype, truth_kind, *, scale_noise=None, mask_kin
         raise ValueError(mask_kind)
     observed = np.where(mask.astype(bool), truth, np.zeros((), dtype)).astype(dtype)
 
-    rng1 = _rng(seed, 1)
-    P = N * (N - 1) // 2
-    sizes = factor_sizes(dims, ranks)
-    total = sum(R_ * Ik for (_, _, R_, Ik) in sizes)
-    if init_kind == "normal":
-        G0 = rng1.standard_normal(total)
-        irec = {"kind": "normal"}
-    else:  # U[0,s) with s = (m·4^P / Π_{p<q} R_{p,q})^{1/(2P)} (reading R8)
-        m = float(np.mean(np.abs(observed[mask.astype(bool)].astype(np.float64))))
-        pr = float(np.prod([ranks[p][q] for p in range(N) for q in range(p + 1, N)]))
-        s = (m * 4.0 ** P / pr) ** (1.0 / (2 * P))
-        G0 = rng1.uniform(0.0, s, total)
-        irec = {"kind": "uniform", "s": s}
-    G0 = G0.astype(dtype)
+    G0, irec = init_factors(dims, ranks, observed, mask, dtype, init_kind, seed)
 
     recipe = {"truth": truth_kind, "noise_sigma": scale_noise, "mask": mrec, "init": irec,
               "seed": seed}

@@ -305,6 +305,8 @@ EDGE = [
     ("rank64_f64", (12, 10, 8), 64, "float64"),
     ("rank_mixed_order4", (10, 9, 8, 7), [[0, 12, 3, 9], [12, 0, 20, 2], [3, 20, 0, 8], [9, 2, 8, 0]],
      "float32"),
+    # G_{i,k} (12 × 2100) too large to stage at once: the tiled staging path of the solve
+    ("rank12_long_mode", (8, 2100, 3), 12, "float32"),
 ]
 
 
