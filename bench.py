@@ -382,6 +382,7 @@ def other_configs(torch):
         ms = time_sweeps(torch, s, p.sweeps)
         prof = s.profile_sweep()
         rse = s.rse(dev(p.truth))
+        met = s.metrics(dev(p.truth))
         s.close()
         sps = p.sweeps / (ms / 1e3)
         out[name] = {"dims": list(p.dims), "dtype": str(p.dtype), "sweeps_timed": p.sweeps,
@@ -393,6 +394,8 @@ def other_configs(torch):
                                                               for b in range(p.N * (p.N - 1))),
                      "effective_gbs": bytes_per_sweep(p.dims, p.N, p.dtype.itemsize) * sps / 1e9,
                      "rse_after_3_plus_timed": rse,
+                     "metrics_after_3_plus_timed": {k: (v if v == v and abs(v) != float("inf") else str(v))
+                                                    for k, v in met.items()},
                      "regime": "launch/latency-bound" if name == "C1" else "L2-resident"}
     return out
 

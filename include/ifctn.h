@@ -190,6 +190,23 @@ ifctn_status ifctn_profile_sweep(ifctn_ctx* ctx, float* ms, int capacity, int* c
 /* Kernel launches the last ifctn_sweep enqueued (graph nodes count as launches).         */
 int64_t ifctn_launch_count(const ifctn_ctx* ctx);
 
+/* ---- Evaluation metrics ------------------------------------------
+ * The paper's evaluation quantities of the current X against a truth tensor T (this rank's
+ * shard, host or device, same layout as `observed`), computed on the device in fp64 and
+ * all-reduced across ranks:
+ *   out[0] RSE  = ‖T − X‖_F / ‖T‖_F (reading R10)
+ *   out[1] RMSE = sqrt(Σ_{Ω^c} (T − X)² / |Ω^c|) over the missing entries (NaN if Ω^c = ∅)
+ *   out[2] PSNR = mean over the bands (slices of the last mode) of 10·log10(1/MSE_band),
+ *                 peak 1 (data in [0,1]); +inf when a band is reproduced exactly
+ *   out[3] SSIM (3rd-order tensors): per band the image over modes 1 and 2, single-scale SSIM
+ *                 with an 11×11 Gaussian window (σ = 1.5), K1 = 0.01, K2 = 0.03, L = 1, over
+ *                 the valid windows (one uniform whole-image window when a side is < 11),
+ *                 averaged over windows and bands; NaN for other orders or when the shard
+ *                 mode is an image mode
+ *   out[4] |Ω^c| (global)
+ * Errors: E_ARG for NULL pointers or ‖T‖ = 0.                                              */
+ifctn_status ifctn_metrics(ifctn_ctx* ctx, const void* truth, double* out);
+
 /* ---- Multi-instance driver: the paper's rank-grid protocol -------------
  * The paper reports its runtimes "including the time required to tune all parameters"
  * over rank grids such as R_{1,2} ∈ {3,6,9,15,30,36}, R_{1,3} = R_{2,3} ∈ {3,6,9}

@@ -145,6 +145,10 @@ class Solver:
     def rse(self, truth) -> float:
         return _abi.ifctn_rse(self.ctx, _ptr(truth))
 
+    def metrics(self, truth) -> dict:
+        """RSE, RMSE on Ω^c, band-mean PSNR, SSIM (ifctn_metrics)."""
+        return _abi.ifctn_metrics(self.ctx, _ptr(truth))
+
     def objective(self) -> float:
         return _abi.ifctn_objective(self.ctx)
 

@@ -74,6 +74,7 @@ SIGNATURES = {
     "ifctn_get_factors": (_I, [_VP, _VP]),
     "ifctn_rse": (_I, [_VP, _VP, ctypes.POINTER(ctypes.c_double)]),
     "ifctn_objective": (_I, [_VP, ctypes.POINTER(ctypes.c_double)]),
+    "ifctn_metrics": (_I, [_VP, _VP, ctypes.POINTER(ctypes.c_double)]),
     "ifctn_block_coefficients": (_I, [_VP, _I, _I, _VP, _VP]),
     "ifctn_block_update": (_I, [_VP, _I, _I]),
     "ifctn_x_update": (_I, [_VP, _VP]),
@@ -181,6 +182,12 @@ def ifctn_objective(ctx) -> float:
     r = ctypes.c_double(0)
     check(lib().ifctn_objective(ctx, ctypes.byref(r)), ctx)
     return r.value
+
+
+def ifctn_metrics(ctx, truth_ptr) -> dict:
+    out = (ctypes.c_double * 5)()
+    check(lib().ifctn_metrics(ctx, truth_ptr, out), ctx)
+    return dict(rse=out[0], rmse=out[1], psnr=out[2], ssim=out[3], missing=int(out[4]))
 
 
 def ifctn_block_coefficients(ctx, k, i, beta_ptr, omega_ptr):

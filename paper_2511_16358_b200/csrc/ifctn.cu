@@ -20,6 +20,7 @@
 #include "fiber_walk.cuh"
 #include "fiber_tile.cuh"
 #include "solve.cuh"
+#include "metrics.cuh"
 #include "nccl_lite.h"
 
 namespace ifctn {
@@ -319,6 +320,7 @@ struct SolverBase {
     virtual void reconstruct(int what, void* out) = 0;
     virtual void get_factors(void* out) = 0;
     virtual double rse(const void* truth) = 0;
+    virtual void metrics(const void* truth, double* out4) = 0;
     virtual double objective() = 0;
     virtual void block_coefficients(int k, int i, double* beta, double* omega) = 0;
     virtual void block_update(int k, int i) = 0;
@@ -1194,6 +1196,75 @@ struct Solver : SolverBase {
         return std::sqrt(num) / std::sqrt(den);
     }
 
+    // RSE, RMSE on Ω^c, band-mean PSNR (bands = slices of the last mode), SSIM
+    // (3rd-order: 11×11 Gaussian windows over modes 1, 2, per band).  Sums are per band and
+    // global-indexed, all-reduced across ranks; SSIM needs whole band images (NaN when the
+    // shard mode is an image mode).
+    void metrics(const void* truth, double* out4) override {
+        if (!truth) fail(IFCTN_E_ARG, "truth must not be NULL");
+        begin();
+        const int N = s.N;
+        const int last = N - 1;
+        const int64_t IN = s.dims[last];                     // global bands
+        const int64_t bl = s.ld[last];                       // local bands
+        const int64_t boff = (s.dpath && s.shard == last) ? s.sbegin : 0;
+        const int64_t fpb = s.nfib / bl;                     // fibres per band (N ≥ 2)
+        const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>((fpb + 63) / 64, (4 * nsm + bl - 1) / bl));
+        const int64_t chunk = (fpb + chunks - 1) / chunks;
+        const bool ssim_ok = (N == 3) && !(s.dpath && s.shard != last);
+        const bool gauss = s.ld[0] >= kSsimWin && s.ld[1] >= kSsimWin;
+        const int tiles_x = (int)((std::max<int64_t>(s.ld[0] - kSsimWin + 1, 1) + kSsimTile - 1) / kSsimTile);
+        const int tiles_y = (int)((std::max<int64_t>(s.ld[1] - kSsimWin + 1, 1) + kSsimTile - 1) / kSsimTile);
+        const int64_t ntiles = gauss ? (int64_t)tiles_x * tiles_y : 1;
+        const size_t nred = 4 + 2 * (size_t)IN;
+        const size_t bytes = sizeof(double) * ((size_t)bl * chunks * 5 + (size_t)bl * ntiles + nred + 8);
+        double* tmp = nullptr;
+        CU(cudaMallocAsync(&tmp, bytes, st));
+        double* part = tmp;
+        double* spart = part + bl * chunks * 5;
+        double* red = spart + bl * ntiles;
+        double* fin = red + nred;
+        const T* dt = (const T*)device_view(truth);
+        void* tmpt = nullptr;
+        if (!dt) {
+            CU(cudaMallocAsync(&tmpt, (size_t)s.nloc * s.esize, st));
+            CU(cudaMemcpyAsync(tmpt, truth, (size_t)s.nloc * s.esize, cudaMemcpyHostToDevice, st));
+            dt = (const T*)tmpt;
+        }
+        metric_sums<T><<<dim3((unsigned)chunks, (unsigned)bl), kMetThreads, 0, st>>>(dt, X, bits, s.I1, s.I1p, fpb,
+                                                                                      chunk, part);
+        CU(cudaGetLastError());
+        if (ssim_ok) {
+            if (gauss)
+                ssim_tiles<T><<<dim3((unsigned)ntiles, (unsigned)bl), kSsimTile * kSsimTile, 0, st>>>(
+                    dt, X, s.ld[0], s.I1p, s.ld[1], tiles_x, spart);
+            else
+                ssim_whole<T><<<(unsigned)bl, 256, 0, st>>>(dt, X, s.ld[0], s.I1p, s.ld[1], spart);
+            CU(cudaGetLastError());
+        }
+        metric_reduce<<<1, 1, 0, st>>>(part, chunks, bl, boff, IN, ssim_ok ? spart : nullptr, ntiles, red);
+        CU(cudaGetLastError());
+        allreduce_dev_chunked(red, nred);
+        const double band_n = (double)(s.nglob / IN);
+        const double nwin = gauss ? (double)((s.ld[0] - kSsimWin + 1) * (s.ld[1] - kSsimWin + 1)) : 1.0;
+        metric_finish<<<1, 1, 0, st>>>(red, IN, band_n, ssim_ok ? nwin * (double)IN : 0.0, fin);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(hscal + 8, fin, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (tmpt) CU(cudaFreeAsync(tmpt, st));
+        CU(cudaFreeAsync(tmp, st));
+        CU(cudaStreamSynchronize(st));
+        end();
+        if (!(hscal[12] > 0.0)) fail(IFCTN_E_ARG, "truth has zero norm");
+        for (int q = 0; q < 4; ++q) out4[q] = hscal[8 + q];
+        out4[4] = hscal[13];  // |Ω^c|
+    }
+
+    // all-reduce of an arbitrary-length fp64 buffer (host-callback staging is proj_elems long)
+    void allreduce_dev_chunked(double* buf, size_t count) {
+        const size_t step = host_allreduce ? (size_t)s.proj_elems : count;
+        for (size_t o = 0; o < count; o += step) allreduce_dev(buf + o, std::min(step, count - o));
+    }
+
     double objective() override {
         begin();
         launch(obj.fn, obj.grid, dim3(kPassThreads), obj.smem, obj.p);
@@ -1395,6 +1466,13 @@ ifctn_status ifctn_rse(ifctn_ctx* ctx, const void* truth, double* rse) {
     CTX_CALL(ctx, {
         if (!rse) ifctn::fail(IFCTN_E_ARG, "rse must not be NULL");
         *rse = ctx->s->rse(truth);
+    });
+}
+
+ifctn_status ifctn_metrics(ifctn_ctx* ctx, const void* truth, double* out) {
+    CTX_CALL(ctx, {
+        if (!out) ifctn::fail(IFCTN_E_ARG, "out must not be NULL");
+        ctx->s->metrics(truth, out);
     });
 }
 

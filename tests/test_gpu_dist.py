@@ -147,3 +147,36 @@ def test_nccl_single_rank_path_matches_single_gpu(name, mode):
     assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
     assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
     assert b.launch_count() > a.launch_count()  # the extra projection / combine launches ran
+
+
+@pytest.mark.parametrize("mode", [2, 0])
+def test_sharded_metrics_match_single_gpu(mode):
+    """Metrics of a sharded context (virtual ranks) equal the single-GPU values; SSIM needs
+    whole band images, so it is NaN when the shard mode is an image mode."""
+    import threading as _th
+    p = make_config("C2s")
+    ref = make_solver(p)
+    ref.sweep(2)
+    want = ref.metrics(dev(p.truth))
+    world = 2
+    solvers, sm, bounds, _ = run_sharded(p, world, 2, shard_mode=mode)
+    from paper_2511_16358_b200.dist import shard_tensor
+    got = [None] * world
+
+    def work(r):
+        b, e = bounds[r]
+        got[r] = solvers[r].metrics(dev(shard_tensor(p.truth, p.dims, sm, b, e)))
+
+    th = [_th.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for g in got:
+        for key in ("rse", "rmse", "psnr"):
+            assert g[key] == pytest.approx(want[key], rel=1e-9)
+        assert g["missing"] == want["missing"]
+        if mode == 2:
+            assert g["ssim"] == pytest.approx(want["ssim"], rel=1e-9)
+        else:
+            assert np.isnan(g["ssim"])
