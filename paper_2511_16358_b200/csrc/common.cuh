@@ -87,6 +87,13 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
     return r;
 }
 
+// ---- programmatic dependent launch (sweep kernels are launched with programmatic stream
+// serialization: the next kernel's CTAs may start while this one runs; each kernel lets its
+// dependents launch at once and waits for its predecessor's completion before touching data
+// the predecessor produced).  No-ops when launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- TMA bulk copies + mbarriers (sm_90+ PTX; UBLKCP / SYNCS in sm_100a SASS) -------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);

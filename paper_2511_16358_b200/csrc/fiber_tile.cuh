@@ -45,6 +45,11 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sfv_stride;
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);  // [H_{0,1} | H_{0,r0}]
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
+    for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
+    if (lane == 0)
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+    pdl_trigger();  // see fiber_walk.cuh: setup above overlaps the predecessor's tail
+    pdl_wait();
     {
         const float4* s1 = reinterpret_cast<const float4*>(P.H + P.hres_src);
         const float4* s2 = reinterpret_cast<const float4*>(P.H + P.vf2_off);
@@ -55,9 +60,6 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
         for (int e = threadIdx.x; e < n1 + n2 + n3; e += blockDim.x)
             dst[e] = e < n1 ? s1[e] : (e < n1 + n2 ? s2[e - n1] : s3[e - n1 - n2]);
     }
-    for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
-    if (lane == 0)
-        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
     fence_proxy_async_smem();
     __syncthreads();

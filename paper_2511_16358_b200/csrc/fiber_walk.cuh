@@ -353,16 +353,19 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
 
-    // CTA setup: the resident H_{0,r0} block (HRES), then per warp: zero the ring (row
-    // tails past I1p must read as 0), init the stage barriers.
+    // CTA setup: per warp zero the ring (row tails past I1p must read as 0) and init the
+    // stage barriers — independent of the previous kernel, so it overlaps its tail (PDL) —
+    // then, after the predecessor completed, the resident H_{0,r0} block (HRES).
+    for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
+    if (lane == 0)
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+    pdl_trigger();
+    pdl_wait();
     if constexpr (HRES) {
         const float4* src = reinterpret_cast<const float4*>(P.H + P.hres_src);
         float4* dst = reinterpret_cast<float4*>(hres);
         for (int e = threadIdx.x; e < (int)(P.hres_elems * sizeof(T) / 16); e += blockDim.x) dst[e] = src[e];
     }
-    for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
-    if (lane == 0)
-        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
     fence_proxy_async_smem();
     __syncthreads();

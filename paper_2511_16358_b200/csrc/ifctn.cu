@@ -473,6 +473,7 @@ struct Solver : SolverBase {
     int64_t nlaunch_sweep = 0, last_launches = 0;
     int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
     int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
+    bool pdl = false;                      // programmatic dependent launch (IFCTN_FLAG_PDL)
     int64_t chunks_per_warp = kChunksPerWarp;  // tiled-pass chunks per warp (env knob)
     int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
     int64_t sh_off = 0, sh_len = 0;        // ΔG² range of the shard-mode chains
@@ -523,7 +524,25 @@ struct Solver : SolverBase {
     void launch(const void* fn, dim3 g, dim3 b, size_t smem, const P& p) {
         prof_mark();
         void* args[] = {(void*)&p};
-        CU(cudaLaunchKernel(fn, g, b, args, smem, st));
+        launch_raw(fn, g, b, smem, args);
+    }
+
+    // With IFCTN_FLAG_PDL, sweep kernels go out with programmatic stream serialization: the
+    // next kernel's CTAs launch while this one drains and wait in griddepcontrol.wait
+    // (common.cuh) for its completion.  Off by default: measured no gain on C2–C5 and a loss
+    // on C2r (early-resident dependents take SM slots from the running kernel).
+    void launch_raw(const void* fn, dim3 g, dim3 b, size_t smem, void** args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = g;
+        cfg.blockDim = b;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = pdl ? at : nullptr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        CU(cudaLaunchKernelExC(&cfg, fn, args));
         ++ctr;
     }
 
@@ -885,16 +904,20 @@ struct Solver : SolverBase {
     void enqueue_finalize(int64_t ngroups, int obj_only) {
         prof_mark();
         const bool multi = s.dpath;
-        finalize_norms<<<1, 1024, 0, st>>>(norms, ngroups, delta, obj_only ? 0 : s.ndelta, sh_off, sh_len, p5,
-                                            scal, dflags, obj_only, multi ? 0 : 1);
-        CU(cudaGetLastError());
-        ++ctr;
+        {
+            const double* a0 = norms;
+            const double* a2 = delta;
+            int64_t a1 = ngroups, a3 = obj_only ? 0 : s.ndelta, a4 = sh_off, a5 = sh_len;
+            int a9 = obj_only, a10 = multi ? 0 : 1;
+            void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5, &p5, &scal, &dflags, &a9, &a10};
+            launch_raw((const void*)finalize_norms, dim3(1), dim3(1024), 0, args);
+        }
         if (multi) {
             allreduce_dev(p5, 4);
             prof_mark();
-            combine_norms<<<1, 32, 0, st>>>(p5, scal, dflags, obj_only);
-            CU(cudaGetLastError());
-            ++ctr;
+            int a3 = obj_only;
+            void* args[] = {&p5, &scal, &dflags, &a3};
+            launch_raw((const void*)combine_norms, dim3(1), dim3(32), 0, args);
         }
     }
 
@@ -934,6 +957,7 @@ struct Solver : SolverBase {
         CU(cudaDeviceGetAttribute(&smo, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         smem_limit = (size_t)smo;
         if (const char* e = getenv("IFCTN_TUNE_CTAS")) tune_ctas = atoi(e);  // experiments only
+        pdl = (flags & IFCTN_FLAG_PDL) != 0;
         if (const char* e = getenv("IFCTN_TUNE_CHUNKS")) chunks_per_warp = std::max(1, atoi(e));
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));

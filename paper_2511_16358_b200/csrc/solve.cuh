@@ -38,6 +38,8 @@ __device__ __forceinline__ int64_t out_index(const ReduceParams<T>& P, int64_t v
 // butterfly sum (fixed order).
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t v = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (v >= P.NV) return;
     const int lane = threadIdx.x & 31;
@@ -65,6 +67,8 @@ __global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T
 
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double sb[256], sw[256];
     const int64_t v = blockIdx.x;
     int64_t nslots;
@@ -157,6 +161,8 @@ enum SolveMode : int { SOLVE_FULL = 0, SOLVE_PROJECT = 1, SOLVE_FROM_PROJ = 2 };
 
 template <typename T, int R, int SM>
 __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
     __shared__ double red[4][NA];
@@ -302,6 +308,8 @@ __host__ __device__ inline size_t big_solve_smem(int R, int ta, int esize) {
 
 template <typename T, int SM>
 __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ __align__(16) double bsm[];
     const int R = P.R, Rp = big_solve_rp(R), TA = P.ta;
     const int NG = R * (R + 1) / 2, NA = NG + R;
@@ -599,6 +607,8 @@ __global__ void __launch_bounds__(1024) finalize_norms(const double* norms, int6
                                                        int64_t sh_off, int64_t sh_len, double* p5,
                                                        double* scal, int* flags, int obj_only,
                                                        int combine) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double s[5][1024];
     double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
     for (int64_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
@@ -629,6 +639,8 @@ __global__ void __launch_bounds__(1024) finalize_norms(const double* norms, int6
 }
 
 __global__ void combine_norms(const double* p5, double* scal, int* flags, int obj_only) {
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x == 0 && blockIdx.x == 0) combine_into(p5, scal, flags, obj_only);
 }
 
