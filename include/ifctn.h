@@ -68,6 +68,8 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NO_GRAPH 1u /* run sweeps as plain launches instead of a CUDA graph     */
 #define IFCTN_FLAG_X_FULL 2u   /* `observed` is a full X (values off Ω kept), for resume  */
 #define IFCTN_FLAG_NO_VBLOCK 8u /* diagnostic: plain fibre walk for every block (no v-blocking) */
+#define IFCTN_FLAG_NO_SOLVE_REDUCE 64u /* diagnostic: separate a2 reduce kernel even when the
+                                        * small-rank solve can absorb it                     */
 #define IFCTN_FLAG_PDL 32u      /* experimental: launch sweep kernels with programmatic
                                   * dependent launch (measured: no gain on C2-C5, a loss on
                                   * C2r — off by default)                                   */

@@ -273,6 +273,8 @@ struct SolveParams {
     int* flags;          // flags[0] |= 1 on a non-positive pivot
     double* proj;        // multi-GPU: per column [Gram upper triangle, rhs] partials
     int R;               // R_{k,i} (block_solve_big; block_solve has it as a template argument)
+    int fused_reduce;    // block_solve: sum β(a,j), ω(a,j) from the a2 partial slots itself
+    ReduceParams<T> red; //   (the reduce_partials launch of the block is then skipped)
     int ta;              // block_solve_big: columns a of G_{i,k} staged at once (≥ I_i: all)
 };
 

@@ -467,6 +467,7 @@ struct Solver : SolverBase {
     PassPlan<T> fused;          // a5 ⊕ a2(0,1), see enqueue_mid()
     ReduceParams<T> fused_red;
     RedLaunch fused_red_l;
+    SolveParams<T> fused_sol;  // block (0,1)'s solve after the fused pass (its slot layout)
     bool has_fused = false;
     cudaGraphExec_t gexec = nullptr;                                    // one plain sweep
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
@@ -475,6 +476,8 @@ struct Solver : SolverBase {
     int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
     bool pdl = false;                      // programmatic dependent launch (IFCTN_FLAG_PDL)
     int64_t chunks_per_warp = kChunksPerWarp;  // tiled-pass chunks per warp (env knob)
+    int64_t solve_slots = 64;              // max serial slot chain for the solve to absorb
+                                           // the reduce (env IFCTN_TUNE_SOLVE_SLOTS)
     int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
     int64_t sh_off = 0, sh_len = 0;        // ΔG² range of the shard-mode chains
     double* p5 = nullptr;                  // norm partials (see finalize_norms)
@@ -820,6 +823,16 @@ struct Solver : SolverBase {
                 q.flags = dflags;
                 q.proj = proj;
                 q.R = s.R(k, i);
+                q.red = r;
+                // The solve gathers its column from the slots itself (one launch fewer) when
+                // that gather is short and coalesced: RED1 blocks (one value per slot) with few
+                // slots per kept value, or KEPT1 blocks with i = 0 (a = i_1: consecutive a are
+                // consecutive slot entries) with a short serial chain per thread.  KEPT1 with
+                // k = 0 would gather one 4-B word per row: the parallel reduce runs first.
+                const int64_t slots_per_v = (r.FR * r.VB) / r.L + 2;
+                const int64_t chain = slots_per_v * ((s.ld[i] + 127) / 128);
+                const bool gather_ok = r.kept1 ? (i == 0 && chain <= solve_slots) : (slots_per_v <= 16 && s.ld[i] >= 16);
+                q.fused_reduce = (q.R <= MAXR_SMALL && gather_ok && !(flags & IFCTN_FLAG_NO_SOLVE_REDUCE)) ? 1 : 0;
                 b.sol_grid = dim3((unsigned)s.ld[k]);
                 if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): a CTA per column
                     b.sol_threads = kBigThreads;
@@ -868,6 +881,8 @@ struct Solver : SolverBase {
             fused_red.VB = vb ? fused.p.nfib / (fused.p.nb0 * fused.p.kdim[1] * fused.p.FR) : 1;
             fused_red.nb0 = vb ? fused.p.nb0 : fused_red.kdim0;
             fused_red_l = split_reduce(fused_red);
+            fused_sol = b0.sol;
+            fused_sol.red = fused_red;
             has_fused = true;
         }
     }
@@ -882,17 +897,23 @@ struct Solver : SolverBase {
             }
     }
 
-    void enqueue_contract(const BlockPlan<T>& b) {
+    // a2: the pass, then the second-stage reduce — unless the block's solve absorbs it
+    // (small ranks: block_solve sums its column's slots itself; `full` forces the reduce for
+    // ifctn_block_coefficients).  A skipped reduce keeps an empty profiling interval so that
+    // ifctn_profile_sweep still reports [pass, reduce, solve] per block.
+    void enqueue_contract(const BlockPlan<T>& b, bool full = false) {
         launch(b.pass.fn, b.pass.grid, dim3(kPassThreads), b.pass.smem, b.pass.p);
-        launch(b.red_l.fn, b.red_l.grid, dim3(256), 0, b.red);
+        if (full || !b.sol.fused_reduce) launch(b.red_l.fn, b.red_l.grid, dim3(256), 0, b.red);
+        else prof_mark();
     }
 
-    void enqueue_solve(const BlockPlan<T>& b) {
+    void enqueue_solve(const BlockPlan<T>& b, const SolveParams<T>* sp = nullptr) {
+        const SolveParams<T>& q = sp ? *sp : b.sol;
         if (b.dist) {
-            launch(b.proj_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, b.sol);
+            launch(b.proj_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
             allreduce_dev(proj, (size_t)b.proj_count);
         }
-        launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, b.sol);
+        launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
     }
 
     void enqueue_block(const BlockPlan<T>& b) {
@@ -941,8 +962,8 @@ struct Solver : SolverBase {
         const BlockPlan<T>& b0 = blocks[0];
         launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fused.p);
         enqueue_finalize(fused.p.ngroups, 0);
-        launch(fused_red_l.fn, fused_red_l.grid, dim3(256), 0, fused_red);
-        enqueue_solve(b0);
+        if (!b0.sol.fused_reduce) launch(fused_red_l.fn, fused_red_l.grid, dim3(256), 0, fused_red);
+        enqueue_solve(b0, &fused_sol);
         for (size_t b = 1; b < blocks.size(); ++b) enqueue_block(blocks[b]);
     }
     void enqueue_last() { enqueue_xupdate(); }
@@ -959,6 +980,7 @@ struct Solver : SolverBase {
         if (const char* e = getenv("IFCTN_TUNE_CTAS")) tune_ctas = atoi(e);  // experiments only
         pdl = (flags & IFCTN_FLAG_PDL) != 0;
         if (const char* e = getenv("IFCTN_TUNE_CHUNKS")) chunks_per_warp = std::max(1, atoi(e));
+        if (const char* e = getenv("IFCTN_TUNE_SOLVE_SLOTS")) solve_slots = atoi(e);
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
@@ -1311,7 +1333,7 @@ struct Solver : SolverBase {
         if (!bo || !wo) fail(IFCTN_E_ARG, "beta/omega must not be NULL");
         const auto& b = find_block(k, i);
         begin();
-        enqueue_contract(b);
+        enqueue_contract(b, true);
         const size_t bytes = (size_t)(s.ld[i] * s.ld[k]) * sizeof(double);
         CU(cudaMemcpyAsync(bo, beta, bytes, cudaMemcpyDefault, st));
         CU(cudaMemcpyAsync(wo, omega, bytes, cudaMemcpyDefault, st));

@@ -159,6 +159,36 @@ __device__ __forceinline__ double warp_sum(double x) {
 // summed across ranks (NCCL all-reduce), then SOLVE_FROM_PROJ adds ρI, ρc_old and solves.
 enum SolveMode : int { SOLVE_FULL = 0, SOLVE_PROJECT = 1, SOLVE_FROM_PROJ = 2 };
 
+// β(a,j), ω(a,j) of block (k,i) straight from the a2 partial slots (fixed slot order), for a
+// solve that absorbs the second-stage reduction: the inverse of out_index().
+template <typename T>
+__device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t j, int64_t a, double& b,
+                                              double& w) {
+    int64_t v, e;
+    if (Q.kept1) {
+        if (Q.kIsMode0) {
+            e = j;
+            v = a;
+        } else {
+            e = a;
+            v = j;
+        }
+    } else {
+        e = 0;
+        v = Q.kmode0IsK ? (j + Q.kdim0 * a) : (a + Q.kdim0 * j);
+    }
+    int64_t nslots;
+    const int64_t base = slot_base(Q, v, nslots) + e;
+    const int64_t stride = Q.VB * Q.Lv;
+    double sb = 0.0, sw = 0.0;
+    for (int64_t s = 0; s < nslots; ++s) {
+        sb += (double)Q.part_b[base + s * stride];
+        sw += (double)Q.part_w[base + s * stride];
+    }
+    b = sb;
+    w = sw;
+}
+
 template <typename T, int R, int SM>
 __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     pdl_trigger();
@@ -172,8 +202,13 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
     for (int64_t a = threadIdx.x; a < (SM == SOLVE_FROM_PROJ ? 0 : P.Ii); a += blockDim.x) {
-        const double b = P.beta[j * P.Ii + a];
-        const double w = P.omega[j * P.Ii + a];
+        double b, w;
+        if (P.fused_reduce) {
+            column_coeffs(P.red, j, a, b, w);
+        } else {
+            b = P.beta[j * P.Ii + a];
+            w = P.omega[j * P.Ii + a];
+        }
         double g[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) g[r] = (double)P.Gik[a * R + r];

