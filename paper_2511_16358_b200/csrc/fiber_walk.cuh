@@ -526,6 +526,11 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
         }
 
         Norms3<T> qn;
+        // contraction: the run-constant slow factor ws is applied once per run —
+        // Σ (ws·u)·x = ws·Σ u·x and Σ (ws·u)² = ws²·Σ u², u = H_{0,r0}·sf per entry
+        T rb[EPL], rw[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) rb[e] = rw[e] = T(0);
         for (int off = 0; off < len; off += F) {
             const int nf = min(F, len - off);
             const int s = (int)(cn % (uint32_t)D);
@@ -542,7 +547,8 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                     T h[EPL], w[EPL];
                     if constexpr (HRES) lds_vec<T, EPL>(hrun + (off + f) * hstep, h);
                     else lds_vec<T, EPL>(sh + f * SR + eb, h);
-                    weight<T, EPL>(ws, h, sf, w);
+                    if constexpr (MODE == PASS_KEPT1 || MODE == PASS_RED1) scale<T, EPL>(h, sf, w);
+                    else weight<T, EPL>(ws, h, sf, w);
                     if constexpr (kFused) {
                         T x[EPL], t[EPL], xn[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
                     } else if constexpr (kContract) {
                         T x[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
-                        accumulate<T, EPL>(w, x, sb, sw);
+                        accumulate<T, EPL>(w, x, rb, rw);
                     } else if constexpr (MODE == PASS_REFILL) {
                         T x[EPL], xn[EPL];
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
@@ -579,6 +585,13 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
             __syncwarp();
             ++cn;
             if (lane == 0) produce();
+        }
+        if constexpr (MODE == PASS_KEPT1 || MODE == PASS_RED1) {
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                sb[e] = fma(ws[e], rb[e], sb[e]);
+                sw[e] = fma(ws[e] * ws[e], rw[e], sw[e]);
+            }
         }
         if constexpr (kNorms) {
             n0 += qn.s0();
