@@ -70,6 +70,10 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NO_VBLOCK 8u /* diagnostic: plain fibre walk for every block (no v-blocking) */
 #define IFCTN_FLAG_NO_SOLVE_REDUCE 64u /* diagnostic: separate a2 reduce kernel even when the
                                         * small-rank solve can absorb it                     */
+#define IFCTN_FLAG_PERSISTENT 128u    /* run fixed-count sweeps (eps ≤ 0, no trace) in one
+                                       * persistent cooperative launch (sweep.cuh); default
+                                       * for single-GPU tensors of ≤ 64 Mi entries          */
+#define IFCTN_FLAG_NO_PERSISTENT 256u /* never use the persistent sweep kernel            */
 #define IFCTN_FLAG_PDL 32u      /* experimental: launch sweep kernels with programmatic
                                   * dependent launch (measured: no gain on C2-C5, a loss on
                                   * C2r — off by default)                                   */

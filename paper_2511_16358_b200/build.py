@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ifctn.cu")
-SRCS = [SRC, os.path.join(HERE, "csrc", "grid.cu")]
+SRCS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("sweep_kernels.cu", "sweep_kernels_f64.cu", "grid.cu")]
 OUT = os.path.join(HERE, "libifctn.so")
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
        [os.path.join(ROOT, "include", "ifctn.h")]
@@ -25,18 +25,39 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
-    """Compile libifctn.so.  `out`/`defines` build experiment variants (scripts/variants.sh)."""
+    """Compile libifctn.so: every translation unit to an object in parallel, then link.
+    `out`/`defines` build experiment variants (scripts/variants.sh)."""
     if out == OUT and not defines and not force and not needs_build():
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    tmp = out + f".tmp{os.getpid()}"
-    cmd = [nvcc] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", tmp] + SRCS + ["-ldl"]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    os.replace(tmp, out)
+    tag = f".tmp{os.getpid()}"
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
+    objs, procs = [], []
+    for src in SRCS:
+        obj = out + "." + os.path.splitext(os.path.basename(src))[0] + tag + ".o"
+        cmd = [nvcc] + flags + ["-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True), obj))
+        objs.append(obj)
+    errs = []
+    for p, obj in procs:
+        o, _ = p.communicate()
+        if p.returncode != 0:
+            errs.append(o)
+    try:
+        if errs:
+            raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
+        tmp = out + tag
+        link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs + ["-ldl"]
+        r = subprocess.run(link, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
+        os.replace(tmp, out)
+    finally:
+        for obj in objs:
+            if os.path.exists(obj):
+                os.remove(obj)
     return out
 
 

@@ -18,8 +18,7 @@
 namespace ifctn {
 
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
-__global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
-    fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
+__device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsigned char* smem_raw, int ncta) {
     static_assert(MODE == PASS_KEPT1 || MODE == PASS_RED1 || MODE == PASS_FUSED, "contraction passes only");
     static_assert(HRES, "the tiled pass keeps its H blocks resident");
     // PASS_FUSED: a5 refill of sweep s fused with block (0,1)'s a2 of sweep s+1 (K = {0,1}):
@@ -40,7 +39,6 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     const int I1p = P.I1p;
     const int RL = P.sf_cap / F;  // tile run capacity (stages per tile)
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * D;
     T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sfv_stride;
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);  // [H_{0,1} | H_{0,r0}]
@@ -389,12 +387,19 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
         chunk = __shfl_sync(0xffffffffu, nx, 0);
     }
     if (lane == 0) {
-        const unsigned total = gridDim.x * (unsigned)nwarps;
+        const unsigned total = (unsigned)ncta * (unsigned)nwarps;
         if (atomicAdd(P.sched + 1, 1u) == total - 1) {
             P.sched[0] = 0u;
             P.sched[1] = 0u;
         }
     }
+}
+
+template <typename T, int MODE, int EPL, int LPF, bool HRES>
+__global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
+    fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    fiber_pass_vb_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, gridDim.x);
 }
 
 }  // namespace ifctn

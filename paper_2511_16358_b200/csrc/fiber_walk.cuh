@@ -328,8 +328,10 @@ __device__ __forceinline__ bool walker_next(Walker& w, const PassParams<T>& P) {
     return true;
 }
 
+// The body of one pass for CTA `cta` of `ncta` (the __global__ wrapper below, or the
+// persistent sweep kernel of sweep.cuh, which runs every pass of a sweep in one launch).
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
-__global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
+__device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned char* smem_raw, int cta) {
     // PASS_FUSED = the a5 refill of sweep s fused with the a2 contraction of block (0,1) of
     // sweep s+1 (same G): X is read once and written once for both.
     constexpr bool kFused = (MODE == PASS_FUSED);
@@ -347,7 +349,6 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
     const int eb = (lane % LPF) * EPL;           // first mode-1 position of this lane
     const int I1p = P.I1p;
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * D;
     T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sfv_stride;
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
     fence_proxy_async_smem();
     __syncthreads();
 
-    const int group = blockIdx.x * nwarps + warp;
+    const int group = cta * nwarps + warp;
     if (group >= P.ngroups) return;
 
     const uint32_t bar0 = smem_u32(bars);
@@ -660,5 +661,10 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const
     }
 }
 
-}  // namespace ifctn
+template <typename T, int MODE, int EPL, int LPF, bool HRES>
+__global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    fiber_pass_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, blockIdx.x);
+}
 
+}  // namespace ifctn

@@ -21,6 +21,7 @@
 #include "fiber_tile.cuh"
 #include "solve.cuh"
 #include "metrics.cuh"
+#include "sweep.cuh"  // SweepOp / SweepProg (the kernels are in sweep_kernels.cu)
 #include "nccl_lite.h"
 
 namespace ifctn {
@@ -52,6 +53,7 @@ static int pow2ceil(int x) {
 }
 
 constexpr int64_t kGroupBoundThreads = 160LL * 2048;  // ≥ resident threads of any B200 part
+constexpr int64_t kPersistentMaxEntries = 64LL << 20;  // sweep_persistent up to this many entries
 constexpr int64_t kChunksPerWarp = 1;                  // tiled pass: dynamic chunks per warp (IFCTN_TUNE_CHUNKS)
 constexpr unsigned kFlagNoVBlock = IFCTN_FLAG_NO_VBLOCK;
 constexpr unsigned kFlagNoFuse = IFCTN_FLAG_NO_FUSE;
@@ -399,6 +401,15 @@ static PassKernel pick_pass(int epl, int lpf, bool hres) {
     return hres ? pick_pass_cfg<T, MODE, true>(epl, lpf) : pick_pass_cfg<T, MODE, false>(epl, lpf);
 }
 
+// sweep_persistent instances live in their own translation unit (sweep_kernels.cu, compiled
+// in parallel with this one)
+const void* persistent_kernel(int esize, int epl, int lpf);
+
+template <typename T>
+static const void* pick_persistent(int epl, int lpf) {
+    return persistent_kernel((int)sizeof(T), epl, lpf);
+}
+
 template <typename T>
 static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
     switch (mode) {
@@ -473,6 +484,13 @@ struct Solver : SolverBase {
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
     int64_t nlaunch_sweep = 0, last_launches = 0;
     int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
+    // persistent whole-sweep kernel (sweep.cuh; single GPU, small tensors)
+    bool persist = false;
+    const void* persist_fn = nullptr;
+    int persist_ncta = 0;
+    size_t persist_smem = 0;
+    SweepProg<T> prog{};
+    void* prog_mem = nullptr;
     int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
     bool pdl = false;                      // programmatic dependent launch (IFCTN_FLAG_PDL)
     int64_t chunks_per_warp = kChunksPerWarp;  // tiled-pass chunks per warp (env knob)
@@ -491,6 +509,10 @@ struct Solver : SolverBase {
     ~Solver() override {
         for (cudaGraphExec_t e : {gexec, gexec_first, gexec_mid, gexec_last})
             if (e) cudaGraphExecDestroy(e);
+        if (prog_mem) {
+            if (st) cudaStreamSynchronize(st);
+            cudaFree(prog_mem);
+        }
         if (comm && nccl) nccl->commDestroy(comm);
         if (st) cudaStreamSynchronize(st);
         if (own_ws && ws) cudaFree(ws);
@@ -887,6 +909,105 @@ struct Solver : SolverBase {
         }
     }
 
+    // The op list of one unfused sweep for sweep_persistent, its parameters copied to the
+    // device, and its launch shape (the pass one-wave grid; every pass grid must fit).
+    void build_persistent() {
+        persist = false;
+        // opt-in: measured slower than the graph path on C1–C4
+        const bool want = (flags & IFCTN_FLAG_PERSISTENT) && !(flags & IFCTN_FLAG_NO_PERSISTENT);
+        if (!want || s.dpath || (flags & IFCTN_FLAG_NO_GRAPH)) return;
+        for (const auto& b : blocks)  // validated for the register solve only (R ≤ 8)
+            if (b.sol.R > MAXR_SMALL) return;
+        std::vector<SweepOp> ops;
+        std::vector<PassParams<T>> pv;
+        std::vector<ReduceParams<T>> rv;
+        std::vector<SolveParams<T>> sv;
+        size_t smem = sweep_scratch_bytes(0);
+        int64_t max_pass_grid = 0;
+        auto add_pass = [&](const PassPlan<T>& pp, int mode, bool vblk) {
+            SweepOp op{};
+            op.kind = OP_PASS;
+            op.variant = mode * 4 + (vblk ? 2 : 0) + (pp.p.hres_elems > 0 ? 1 : 0);
+            op.idx = (int)pv.size();
+            pv.push_back(pp.p);
+            ops.push_back(op);
+            smem = std::max(smem, pp.smem);
+            max_pass_grid = std::max<int64_t>(max_pass_grid, pp.grid.x);
+        };
+        for (const auto& b : blocks) {
+            add_pass(b.pass, (b.k == 0 || b.i == 0) ? PASS_KEPT1 : PASS_RED1, b.vblk);
+            if (!b.sol.fused_reduce) {
+                SweepOp op{};
+                op.kind = OP_REDUCE;
+                op.variant = b.red_l.fn == (const void*)reduce_partials_warp<T> ? 0 : 1;
+                op.idx = (int)rv.size();
+                op.nvb = (int64_t)b.red_l.grid.x * b.red_l.grid.y * b.red_l.grid.z;
+                op.gy = (int)b.red_l.grid.y;
+                op.gz = (int)b.red_l.grid.z;
+                rv.push_back(b.red);
+                ops.push_back(op);
+            }
+            SweepOp op{};
+            op.kind = b.sol.R > MAXR_SMALL ? OP_SOLVE_BIG : OP_SOLVE;
+            op.variant = b.sol.R;
+            op.idx = (int)sv.size();
+            op.nvb = s.ld[b.k];
+            sv.push_back(b.sol);
+            ops.push_back(op);
+            if (op.kind == OP_SOLVE_BIG) smem = std::max(smem, sweep_scratch_bytes(b.sol_smem));
+        }
+        add_pass(refill, PASS_REFILL, false);
+        {
+            SweepOp op{};
+            op.kind = OP_FINALIZE;
+            ops.push_back(op);
+        }
+        const void* fn = pick_persistent<T>(s.epl, s.lpf);
+        cudaFuncAttributes fa;
+        CU(cudaFuncGetAttributes(&fa, fn));
+        if (smem + fa.sharedSizeBytes > smem_limit) return;
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPassThreads, smem));
+        const int ncta = nsm * std::min(occ, kPassMinBlocks);
+        if (occ < 1 || ncta < max_pass_grid) return;
+        // device copy of the program
+        const size_t bo = 0, bp = align_up((int64_t)(ops.size() * sizeof(SweepOp)), 256);
+        const size_t br = bp + align_up((int64_t)(pv.size() * sizeof(PassParams<T>)), 256);
+        const size_t bs = br + align_up((int64_t)(std::max<size_t>(rv.size(), 1) * sizeof(ReduceParams<T>)), 256);
+        const size_t total = bs + std::max<size_t>(sv.size(), 1) * sizeof(SolveParams<T>);
+        CU(cudaMalloc(&prog_mem, total));
+        unsigned char* base = (unsigned char*)prog_mem;
+        CU(cudaMemcpyAsync(base + bo, ops.data(), ops.size() * sizeof(SweepOp), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(base + bp, pv.data(), pv.size() * sizeof(PassParams<T>), cudaMemcpyHostToDevice, st));
+        if (!rv.empty())
+            CU(cudaMemcpyAsync(base + br, rv.data(), rv.size() * sizeof(ReduceParams<T>), cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(base + bs, sv.data(), sv.size() * sizeof(SolveParams<T>), cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+        prog.ops = (const SweepOp*)(base + bo);
+        prog.nops = (int)ops.size();
+        prog.pass = (const PassParams<T>*)(base + bp);
+        prog.red = (const ReduceParams<T>*)(base + br);
+        prog.sol = (const SolveParams<T>*)(base + bs);
+        prog.norms = norms;
+        prog.ngroups = refill.p.ngroups;
+        prog.delta = delta;
+        prog.ndelta = s.ndelta;
+        prog.p5 = p5;
+        prog.scal = scal;
+        prog.flags = dflags;
+        persist_fn = fn;
+        persist_ncta = ncta;
+        persist_smem = smem;
+        persist = true;
+    }
+
+    void launch_persistent(int nsweeps) {
+        void* args[] = {(void*)&prog, (void*)&nsweeps};
+        CU(cudaLaunchCooperativeKernel(persist_fn, dim3(persist_ncta), dim3(kPassThreads), args, persist_smem, st));
+        ++ctr;
+    }
+
     void build_all_H() {
         for (int a = 0; a < s.N; ++a)
             for (int b = a + 1; b < s.N; ++b) {
@@ -1047,6 +1168,7 @@ struct Solver : SolverBase {
         }
         plan();
         build_all_H();
+        build_persistent();
         CU(cudaStreamSynchronize(st));
         end();
     }
@@ -1105,6 +1227,13 @@ struct Solver : SolverBase {
         int s_done = 0;
         last_launches = 0;
         const int64_t c0 = ctr;
+        if (persist && !need_sync && t_max >= 1) {  // small tensor: every sweep in one launch
+            launch_persistent(t_max);
+            last_launches = 1;
+            if (done) *done = t_max;
+            end();
+            return;
+        }
         if (has_fused && !need_sync && t_max >= 2) {  // fixed sweep count: fused sequence
             if (use_graph && !gexec_mid) capture_fused();
             if (use_graph) {

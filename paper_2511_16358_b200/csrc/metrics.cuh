@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) ssim_whole(const T* truth, const T* X, in
 // Fixed-order combination of the partials of this rank into red[4 + 2·IN] (global band
 // indices; bands of other ranks stay 0 so that the all-reduce sums them):
 //   red[0..3] = [Σ d², Σ t², Σ_{Ω^c} d², |Ω^c|], red[4 + β] = Σ_band d², red[4 + IN + β] = Σ SSIM.
-__global__ void metric_reduce(const double* part, int64_t chunks, int64_t bl, int64_t boff, int64_t IN,
+static __global__ void metric_reduce(const double* part, int64_t chunks, int64_t bl, int64_t boff, int64_t IN,
                               const double* spart, int64_t ntiles, double* red) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int64_t q = 0; q < 4 + 2 * IN; ++q) red[q] = 0.0;
@@ -182,7 +182,7 @@ __global__ void metric_reduce(const double* part, int64_t chunks, int64_t bl, in
 
 // fin = [RSE, RMSE on Ω^c (NaN if Ω^c is empty), band-mean PSNR (+inf if a band is exact),
 //        mean SSIM (NaN when not computed), Σ t², |Ω^c|]
-__global__ void metric_finish(const double* red, int64_t IN, double band_n, double nwin_total, double* fin) {
+static __global__ void metric_finish(const double* red, int64_t IN, double band_n, double nwin_total, double* fin) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double d2 = red[0], t2 = red[1], m2 = red[2], mc = red[3];
     fin[0] = sqrt(d2) / sqrt(t2);

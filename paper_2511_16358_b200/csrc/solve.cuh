@@ -37,10 +37,8 @@ __device__ __forceinline__ int64_t out_index(const ReduceParams<T>& P, int64_t v
 // Lv = 1 (RED1 blocks, many v with few slots each): one warp per v, lanes stride the slots,
 // butterfly sum (fixed order).
 template <typename T>
-__global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
-    const int64_t v = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+__device__ __forceinline__ void reduce_partials_warp_body(const ReduceParams<T>& P, int64_t bx) {
+    const int64_t v = bx * 8 + (threadIdx.x >> 5);
     if (v >= P.NV) return;
     const int lane = threadIdx.x & 31;
     int64_t nslots;
@@ -66,20 +64,26 @@ __global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
+__global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T> P) {
     pdl_trigger();
     pdl_wait();
-    __shared__ double sb[256], sw[256];
-    const int64_t v = blockIdx.x;
+    reduce_partials_warp_body(P, blockIdx.x);
+}
+
+// CTA (v = bx, element tile = by, slot share z = bz); sb, sw: 256 doubles of shared scratch
+template <typename T>
+__device__ __forceinline__ void reduce_partials_body(const ReduceParams<T>& P, int64_t bx, int by, int bz,
+                                                     double* sb, double* sw, unsigned* last_flag) {
+    const int64_t v = bx;
     int64_t nslots;
     const int64_t base = slot_base(P, v, nslots);
     // this CTA: elements e = tile·ET + tx, slots [s0, s1) split over ny = 256/ET thread rows
     const int ET = P.ET, ny = 256 / ET;
     const int tx = threadIdx.x % ET, ty = threadIdx.x / ET;
-    const int z = blockIdx.z;
+    const int z = bz;
     const int64_t chunk = (nslots + P.Z - 1) / P.Z;
     const int64_t s0 = z * chunk, s1 = min(nslots, s0 + chunk);
-    const int64_t e = (int64_t)blockIdx.y * ET + tx;
+    const int64_t e = (int64_t)by * ET + tx;
     double b = 0.0, w = 0.0;
     if (e < P.Lv) {
         const int64_t stride = (int64_t)ny * P.VB * P.Lv;
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) 
     }
     if (P.Z > 1) {
         // publish this z-share, last CTA of (v, tile) to arrive sums the Z shares in z order
-        const int64_t id = (int64_t)blockIdx.y * P.NV + v;
+        const int64_t id = (int64_t)by * P.NV + v;
         double* my = P.scr + ((id * P.Z + z) * ET) * 2;
         if (ty == 0) {
             my[2 * tx] = sb[tx];
@@ -119,10 +123,9 @@ __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) 
         }
         __threadfence();
         __syncthreads();
-        __shared__ unsigned last;
-        if (threadIdx.x == 0) last = (atomicAdd(P.cnt + id, 1u) == (unsigned)(P.Z - 1));
+        if (threadIdx.x == 0) *last_flag = (atomicAdd(P.cnt + id, 1u) == (unsigned)(P.Z - 1));
         __syncthreads();
-        if (!last) return;
+        if (!*last_flag) return;
         __threadfence();
         if (ty == 0) {
             double bb = 0.0, ww = 0.0;
@@ -143,6 +146,15 @@ __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) 
             P.omega[o] = sw[tx];
         }
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ double sb[256], sw[256];
+    __shared__ unsigned last;
+    reduce_partials_body(P, blockIdx.x, blockIdx.y, blockIdx.z, sb, sw, &last);
 }
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -190,18 +202,16 @@ __device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t 
 }
 
 template <typename T, int R, int SM>
-__global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
+// nthr (a multiple of 32, ≤ blockDim.x) threads take part; the others only pass the barriers
+__device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_t j, int nthr,
+                                                 double* red /*(nthr/32)·NA*/, double* cs /*R*/) {
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
-    __shared__ double red[4][NA];
-    __shared__ double cs[R];
-    const int64_t j = blockIdx.x;
+    const int nw = nthr >> 5;
     double acc[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
-    for (int64_t a = threadIdx.x; a < (SM == SOLVE_FROM_PROJ ? 0 : P.Ii); a += blockDim.x) {
+    for (int64_t a = threadIdx.x; a < (SM == SOLVE_FROM_PROJ || (int)threadIdx.x >= nthr ? 0 : P.Ii); a += nthr) {
         double b, w;
         if (P.fused_reduce) {
             column_coeffs(P.red, j, a, b, w);
@@ -225,13 +235,15 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
 #pragma unroll
         for (int t = 0; t < NA; ++t) {
             const double s = warp_sum(acc[t]);
-            if (ln == 0) red[wid][t] = s;
+            if (ln == 0 && wid < nw) red[wid * NA + t] = s;
         }
         __syncthreads();
         if constexpr (SM == SOLVE_PROJECT) {
             if (threadIdx.x < NA) {
                 const int t = threadIdx.x;
-                P.proj[j * NA + t] = red[0][t] + red[1][t] + red[2][t] + red[3][t];
+                double v = 0.0;
+                for (int q = 0; q < nw; ++q) v += red[q * NA + t];
+                P.proj[j * NA + t] = v;
             }
             return;
         }
@@ -239,8 +251,13 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     if (threadIdx.x == 0) {
         double sum[NA];
 #pragma unroll
-        for (int t = 0; t < NA; ++t)
-            sum[t] = (SM == SOLVE_FROM_PROJ) ? P.proj[j * NA + t] : red[0][t] + red[1][t] + red[2][t] + red[3][t];
+        for (int t = 0; t < NA; ++t) {
+            double v = 0.0;
+            if constexpr (SM == SOLVE_FROM_PROJ) v = P.proj[j * NA + t];
+            else
+                for (int q = 0; q < nw; ++q) v += red[q * NA + t];
+            sum[t] = v;
+        }
         double A[R][R], L[R][R], y[R], c[R], cold[R];
         int t = 0;
 #pragma unroll
@@ -317,6 +334,16 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     }
 }
 
+template <typename T, int R, int SM>
+__global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
+    constexpr int NA = R * (R + 1) / 2 + R;
+    __shared__ double red[4 * NA];
+    __shared__ double cs[R];
+    block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs);
+}
+
 // ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------
 // Same mathematics as block_solve (Eq. 8) with the rank a runtime value ≤ 64.
 // One CTA (256 threads) per column j:
@@ -342,10 +369,8 @@ __host__ __device__ inline size_t big_solve_smem(int R, int ta, int esize) {
 }
 
 template <typename T, int SM>
-__global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
-    extern __shared__ __align__(16) double bsm[];
+__device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, int64_t j, double* bsm, int* okp,
+                                                     double* colb /*2·64*/, double* dinvp) {
     const int R = P.R, Rp = big_solve_rp(R), TA = P.ta;
     const int NG = R * (R + 1) / 2, NA = NG + R;
     T* gs = reinterpret_cast<T*>(bsm);  // G_{i,k}(:, a0 .. a0+ta), row stride R
@@ -356,9 +381,7 @@ __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams
     double* rhs = be + TA;
     double* cv = rhs + Rp;
     double* cold = cv + Rp;
-    __shared__ int ok;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
-    const int64_t j = blockIdx.x;
     const int nt = Rp / 4;
     const int ntiles = nt * (nt + 1) / 2;
     const int KS = max(1, min(8, nthr / ntiles));   // a-split per tile
@@ -476,7 +499,7 @@ __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams
         A[tid * Rp + tid] += P.rho;
         rhs[tid] += P.rho * co;
     }
-    if (tid == 0) ok = 1;
+    if (tid == 0) *okp = 1;
     __syncthreads();
     // Cholesky with the lower triangle in registers: thread t owns entries m = t + q·256 of
     // the packed lower triangle (row-major, (r, c) with c ≤ r), at most kBigEnt of them.
@@ -484,8 +507,6 @@ __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams
     // l_r = A_r,cc/sqrt(d) (parity-double-buffered column); every owner of (r, c), c > cc,
     // subtracts l_r·l_c.  Two barriers per step, no shared-memory read-modify-write chains.
     {
-        __shared__ double colb[2][64];
-        __shared__ double dinv;
         int er[kBigEnt], ec[kBigEnt];
         double ev[kBigEnt];
         const int NL = NG;  // lower-triangle entries
@@ -505,19 +526,19 @@ __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams
         }
         bool okl = true;
         for (int cc = 0; cc < R; ++cc) {
-            double* col = colb[cc & 1];
+            double* col = colb + (cc & 1) * 64;
 #pragma unroll
             for (int q = 0; q < kBigEnt; ++q)
                 if (er[q] == cc && ec[q] == cc) {
                     const double d = ev[q];
                     okl = d > 0.0;
                     const double inv = 1.0 / sqrt(d > 0.0 ? d : 1.0);
-                    dinv = inv;
+                    *dinvp = inv;
                     ev[q] = inv;  // the diagonal keeps 1/L_cc
-                    if (!okl) ok = 0;
+                    if (!okl) *okp = 0;
                 }
             __syncthreads();
-            const double inv = dinv;
+            const double inv = *dinvp;
 #pragma unroll
             for (int q = 0; q < kBigEnt; ++q)
                 if (ec[q] == cc && er[q] > cc) {
@@ -565,7 +586,7 @@ __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams
         if (lane < R) cv[lane] = x0;
         if (lane + 32 < R) cv[lane + 32] = x1;
         __syncwarp();
-        if (!ok) {
+        if (!*okp) {
             if (lane == 0) atomicOr(P.flags, 1);
             for (int r = lane; r < R; r += 32) cv[r] = cold[r];
         }
@@ -605,6 +626,17 @@ __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams
     }
 }
 
+template <typename T, int SM>
+__global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
+    extern __shared__ __align__(16) double bsm[];
+    __shared__ int ok;
+    __shared__ double colb[2 * 64];
+    __shared__ double dinv;
+    block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok, colb, &dinv);
+}
+
 // ---- a1: build H_{p,q} = G_{p,q}ᵀ G_{q,p} for one pair (K=R skinny product; FMA pipes) ---
 template <typename T>
 __global__ void pair_gram(const T* Gpq, const T* Gqp, int R, int64_t Ip, int64_t Iq, T* H,
@@ -637,43 +669,55 @@ __device__ __forceinline__ void combine_into(const double* p5, double* scal, int
     if (!isfinite(dx2) || !isfinite(x2) || !isfinite(f) || !isfinite(dg2)) atomicOr(flags + 1, 1);
 }
 
-__global__ void __launch_bounds__(1024) finalize_norms(const double* norms, int64_t ngroups,
+// Written for 1024 virtual threads (any blockDim.x dividing 1024 runs them in turn), so the
+// summation order is the same whatever the CTA size.  s: 5·1024 doubles of shared scratch.
+__device__ __forceinline__ void finalize_norms_body(const double* norms, int64_t ngroups, const double* delta,
+                                                    int64_t ndelta, int64_t sh_off, int64_t sh_len, double* p5,
+                                                    double* scal, int* flags, int obj_only, int combine,
+                                                    double* s) {
+    constexpr int VT = 1024;
+    for (int vt = threadIdx.x; vt < VT; vt += blockDim.x) {
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+        for (int64_t g = vt; g < ngroups; g += VT) {
+            a0 += norms[3 * g + 0];
+            a1 += norms[3 * g + 1];
+            a2 += norms[3 * g + 2];
+        }
+        if (!obj_only)
+            for (int64_t d = vt; d < ndelta; d += VT) {
+                if (d >= sh_off && d < sh_off + sh_len) a3 += delta[d];
+                else a4 += delta[d];
+            }
+        s[0 * VT + vt] = a0;
+        s[1 * VT + vt] = a1;
+        s[2 * VT + vt] = a2;
+        s[3 * VT + vt] = a3;
+        s[4 * VT + vt] = a4;
+    }
+    __syncthreads();
+    for (int st = VT >> 1; st > 0; st >>= 1) {
+        for (int vt = threadIdx.x; vt < st; vt += blockDim.x)
+            for (int q = 0; q < 5; ++q) s[q * VT + vt] += s[q * VT + vt + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 5; ++q) p5[q] = s[q * VT];
+        if (combine) combine_into(p5, scal, flags, obj_only);
+    }
+}
+
+static __global__ void __launch_bounds__(1024) finalize_norms(const double* norms, int64_t ngroups,
                                                        const double* delta, int64_t ndelta,
                                                        int64_t sh_off, int64_t sh_len, double* p5,
                                                        double* scal, int* flags, int obj_only,
                                                        int combine) {
     pdl_trigger();
     pdl_wait();
-    __shared__ double s[5][1024];
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-    for (int64_t g = threadIdx.x; g < ngroups; g += blockDim.x) {
-        a0 += norms[3 * g + 0];
-        a1 += norms[3 * g + 1];
-        a2 += norms[3 * g + 2];
-    }
-    if (!obj_only)
-        for (int64_t d = threadIdx.x; d < ndelta; d += blockDim.x) {
-            if (d >= sh_off && d < sh_off + sh_len) a3 += delta[d];
-            else a4 += delta[d];
-        }
-    s[0][threadIdx.x] = a0;
-    s[1][threadIdx.x] = a1;
-    s[2][threadIdx.x] = a2;
-    s[3][threadIdx.x] = a3;
-    s[4][threadIdx.x] = a4;
-    __syncthreads();
-    for (int st = blockDim.x >> 1; st > 0; st >>= 1) {
-        if ((int)threadIdx.x < st)
-            for (int q = 0; q < 5; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + st];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < 5; ++q) p5[q] = s[q][0];
-        if (combine) combine_into(p5, scal, flags, obj_only);
-    }
+    __shared__ double s[5 * 1024];
+    finalize_norms_body(norms, ngroups, delta, ndelta, sh_off, sh_len, p5, scal, flags, obj_only, combine, s);
 }
 
-__global__ void combine_norms(const double* p5, double* scal, int* flags, int obj_only) {
+static __global__ void combine_norms(const double* p5, double* scal, int* flags, int obj_only) {
     pdl_trigger();
     pdl_wait();
     if (threadIdx.x == 0 && blockIdx.x == 0) combine_into(p5, scal, flags, obj_only);
@@ -751,7 +795,7 @@ __global__ void __launch_bounds__(256) rse_partial(const T* truth, const T* X, i
     }
 }
 
-__global__ void sum_pairs(const double* part, int n, double* out) {
+static __global__ void sum_pairs(const double* part, int n, double* out) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double a = 0.0, b = 0.0;
         for (int i = 0; i < n; ++i) {

@@ -200,11 +200,11 @@ def test_trace_lemma2_and_feasibility(name):
 
 @pytest.mark.parametrize("name", ["C2s", "C5s"])
 def test_graph_and_plain_launches_bit_identical(name):
-    from paper_2511_16358_b200 import IFCTN_FLAG_NO_GRAPH
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_NO_PERSISTENT
     p = make_config(name)
-    a = make_solver(p)
+    a = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
     b = make_solver(p, flags=IFCTN_FLAG_NO_GRAPH)
-    c = make_solver(p)
+    c = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
     for x in (a, b, c):
         x.sweep(3)
     Xa, Xb, Xc = (x.reconstruct().cpu().numpy() for x in (a, b, c))
@@ -224,10 +224,10 @@ def test_graph_and_plain_launches_bit_identical(name):
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C2"])
 def test_fused_sweeps_match_plain_sweeps(name):
     """The fused a5(s) ⊕ a2(0,1)(s+1) pass reproduces the plain sweep sequence."""
-    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_PERSISTENT
     p = make_config(name)
-    a = make_solver(p)
-    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE)
+    a = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
+    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE | IFCTN_FLAG_NO_PERSISTENT)
     a.sweep(2)   # sweep 1's blocks, [a5(1) ⊕ a2(0,1)(2)], sweep 2's other blocks, a5(2)
     b.sweep(2)
     tol = tol_for(p, 1e-5, 1e-12)
@@ -241,8 +241,9 @@ def test_fused_sweeps_match_plain_sweeps(name):
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C3"])
 def test_fused_three_sweeps_vs_oracle(name):
     """Three sweeps through the fused sequence against three oracle sweeps (north-star bar)."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_PERSISTENT
     p = make_config(name)
-    s = make_solver(p)
+    s = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
     s.sweep(3)
     sh, G, X = oracle_state(p)
     F = O.objective(sh, G, X)
@@ -252,6 +253,24 @@ def test_fused_three_sweeps_vs_oracle(name):
     tol = tol_for(p)
     assert rel(s.factors().cpu().numpy(), G) <= tol
     assert rel(s.reconstruct().cpu().numpy(), X) <= tol
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C2", "C4"])
+def test_persistent_sweeps_bit_identical_to_launch_sequence(name):
+    """the persistent whole-sweep kernel (one cooperative launch for all
+    sweeps) runs the same op bodies with the same work split as the unfused launch sequence,
+    so factors and X agree bit for bit."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_PERSISTENT, IFCTN_FLAG_PERSISTENT
+    p = make_config(name)
+    a = make_solver(p, flags=IFCTN_FLAG_PERSISTENT)
+    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE | IFCTN_FLAG_NO_PERSISTENT)
+    a.sweep(3)
+    b.sweep(3)
+    assert a.launch_count() == 1
+    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
+    assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
+    assert a.objective() == b.objective()
 
 
 @pytest.mark.parametrize("name,sweeps", [("C1", 10), ("C2s", 20), ("C3s", 20), ("C4s", 20), ("C5s", 10),
