@@ -12,7 +12,7 @@ constexpr int MAXN = 6;                        // IFCTN_MAX_ORDER
 constexpr int MAXP = MAXN * (MAXN - 1) / 2;    // pairs p<q
 constexpr int MAXSF = MAXN - 2;                // pairs involving the fast mode r0 (outer)
 constexpr int MAXR = 64;                       // IFCTN_MAX_RANK
-constexpr int MAXR_SMALL = 8;                  // block_solve (registers) up to here, then block_solve_big (warp per column)
+constexpr int MAXR_SMALL = 9;                   // block_solve (registers) up to here, then block_solve_big
 constexpr int kPassThreads = 256;              // fiber-pass CTA size
 constexpr int kPassMinBlocks = 2;              // ≤ 128 registers: ≥ 16 warps per SM
 #ifndef IFCTN_RING_D

@@ -435,7 +435,8 @@ static const void* pick_solve_sm(int R) {
         case 5: return (const void*)block_solve<T, 5, SM>;
         case 6: return (const void*)block_solve<T, 6, SM>;
         case 7: return (const void*)block_solve<T, 7, SM>;
-        default: return (const void*)block_solve<T, 8, SM>;
+        case 8: return (const void*)block_solve<T, 8, SM>;
+        default: return (const void*)block_solve<T, 9, SM>;
     }
 }
 
@@ -916,7 +917,7 @@ struct Solver : SolverBase {
         // opt-in: measured slower than the graph path on C1–C4
         const bool want = (flags & IFCTN_FLAG_PERSISTENT) && !(flags & IFCTN_FLAG_NO_PERSISTENT);
         if (!want || s.dpath || (flags & IFCTN_FLAG_NO_GRAPH)) return;
-        for (const auto& b : blocks)  // validated for the register solve only (R ≤ 8)
+        for (const auto& b : blocks)  // validated for the register solve only (R ≤ 9)
             if (b.sol.R > MAXR_SMALL) return;
         std::vector<SweepOp> ops;
         std::vector<PassParams<T>> pv;

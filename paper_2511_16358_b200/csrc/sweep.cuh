@@ -72,7 +72,8 @@ __device__ __forceinline__ void run_solve(int R, const SolveParams<T>& P, int64_
         case 5: block_solve_body<T, 5, SOLVE_FULL>(P, j, 128, red, cs); break;
         case 6: block_solve_body<T, 6, SOLVE_FULL>(P, j, 128, red, cs); break;
         case 7: block_solve_body<T, 7, SOLVE_FULL>(P, j, 128, red, cs); break;
-        default: block_solve_body<T, 8, SOLVE_FULL>(P, j, 128, red, cs); break;
+        case 8: block_solve_body<T, 8, SOLVE_FULL>(P, j, 128, red, cs); break;
+        default: block_solve_body<T, 9, SOLVE_FULL>(P, j, 128, red, cs); break;
     }
 }
 
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
             } else if (op.kind == OP_SOLVE) {
                 const SolveParams<T>& P = G.sol[op.idx];
                 for (int64_t j = cta; j < op.nvb; j += ncta) {
-                    run_solve<T>(op.variant, P, j, scratch, scratch + 8 * 64);
+                    run_solve<T>(op.variant, P, j, scratch, scratch + 4 * 64);
                     __syncthreads();
                 }
             } else if (op.kind == OP_SOLVE_BIG) {
