@@ -510,6 +510,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         int er[kBigEnt], ec[kBigEnt];
         double ev[kBigEnt];
         const int NL = NG;  // lower-triangle entries
+        const int nent = (NL + kBigThreads - 1) / kBigThreads;  // entries per thread (≤ kBigEnt)
 #pragma unroll
         for (int q = 0; q < kBigEnt; ++q) {
             const int m = tid + q * kBigThreads;
@@ -528,7 +529,8 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         for (int cc = 0; cc < R; ++cc) {
             double* col = colb + (cc & 1) * 64;
 #pragma unroll
-            for (int q = 0; q < kBigEnt; ++q)
+            for (int q = 0; q < kBigEnt; ++q) {
+                if (q >= nent) break;
                 if (er[q] == cc && ec[q] == cc) {
                     const double d = ev[q];
                     okl = d > 0.0;
@@ -537,18 +539,23 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
                     ev[q] = inv;  // the diagonal keeps 1/L_cc
                     if (!okl) *okp = 0;
                 }
+            }
             __syncthreads();
             const double inv = *dinvp;
 #pragma unroll
-            for (int q = 0; q < kBigEnt; ++q)
+            for (int q = 0; q < kBigEnt; ++q) {
+                if (q >= nent) break;
                 if (ec[q] == cc && er[q] > cc) {
                     ev[q] *= inv;
                     col[er[q]] = ev[q];
                 }
+            }
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < kBigEnt; ++q)
+            for (int q = 0; q < kBigEnt; ++q) {
+                if (q >= nent) break;
                 if (ec[q] > cc) ev[q] = fma(-col[er[q]], col[ec[q]], ev[q]);
+            }
         }
 #pragma unroll
         for (int q = 0; q < kBigEnt; ++q)
