@@ -145,9 +145,12 @@ ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims,
  * t_max sweeps and, with trace == NULL, returns without synchronising (device errors are
  * then reported by ifctn_sync).  eps > 0 stops after the first sweep with rel_change < eps.
  * trace (host, t_max rows) is filled when non-NULL.  *sweeps_done (may be NULL).
- * With eps ≤ 0, no trace and t_max ≥ 2 the X update of sweep s and the first block of
- * sweep s+1 run as one pass over X (they use the same factors); results are the same
- * sweeps up to floating-point summation order.                                           */
+ * With eps ≤ 0 and t_max ≥ 2 the X update of sweep s and the first block of sweep s+1
+ * run as one pass over X (they use the same factors); results are the same sweeps up to
+ * floating-point summation order.  With a trace on that path the rows are gathered on the
+ * device and read back once, after the last sweep (a single synchronisation).
+ * IFCTN_FLAG_PERSISTENT: eps ≤ 0 without trace runs all t_max sweeps in one cooperative
+ * launch (unfused order, bit-identical to the unfused launch sequence).                  */
 ifctn_status ifctn_sweep(ifctn_ctx* ctx, int t_max, double eps, int* sweeps_done,
                          ifctn_trace_row* trace);
 

@@ -237,6 +237,7 @@ struct PassParams {
     int64_t tc_off, tc_ld;
     int64_t sfv_stride;            // per-warp elements of the sf scratch
     unsigned* sched;               // tiled pass: [next chunk, retired warps], zero between launches
+    int full_norms;                // fused pass: all three norms (traced sweeps), else ‖X_new‖² only
 };
 
 template <typename T>

@@ -301,7 +301,8 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
                             const int sl = (int)((uint32_t)(xw - P.Xw) & 127u);
                             const uint32_t bits = (SR == I1p) ? mask_bits_l(smw, sl + fo + eb)
                                                               : mask_bits_l(smw + f * MWF, ((sl + fo) & 127) + eb);
-                            refill_lite<T, EPL>(x, tt, bits, P.rho, P.inv1p, xn, qn);
+                            if (P.full_norms) refill_chunk<T, EPL>(x, tt, bits, P.rho, P.inv1p, xn, qn);
+                            else refill_lite<T, EPL>(x, tt, bits, P.rho, P.inv1p, xn, qn);
                             store_chunk<T, EPL>(xw + fo + eb, xn, lane_full, ev);
                             accumulate<T, EPL>(w, xn, sb[st], sw[st]);
                         } else {

@@ -557,7 +557,8 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
                         for (int e = 0; e < EPL; ++e) t[e] = w[e] * h01v[e];
                         const int64_t gf = sg0 + (int64_t)f * xstep, ge = gf + eb;
                         const uint32_t bits = xmerge ? mask_bits_s(smw, sg0, ge) : mask_bits_s(smw + f * MWF, gf, ge);
-                        refill_lite<T, EPL>(x, t, bits, P.rho, P.inv1p, xn, qn);
+                        if (P.full_norms) refill_chunk<T, EPL>(x, t, bits, P.rho, P.inv1p, xn, qn);
+                        else refill_lite<T, EPL>(x, t, bits, P.rho, P.inv1p, xn, qn);
                         store_chunk<T, EPL>(P.Xw + ge, xn, lane_full, ev);
                         accumulate<T, EPL>(w, xn, sb, sw);
                     } else if constexpr (kContract) {

@@ -483,6 +483,11 @@ struct Solver : SolverBase {
     bool has_fused = false;
     cudaGraphExec_t gexec = nullptr;                                    // one plain sweep
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
+    cudaGraphExec_t gexec_mid_t = nullptr, gexec_last_t = nullptr;  // traced fused sweeps
+    double* trace_rows = nullptr;  // device: 5 doubles per traced sweep
+    int* trace_count = nullptr;
+    int trace_cap = 0;
+    int64_t n_mid_t = 0, n_last_t = 0;
     int64_t nlaunch_sweep = 0, last_launches = 0;
     int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
     // persistent whole-sweep kernel (sweep.cuh; single GPU, small tensors)
@@ -508,8 +513,9 @@ struct Solver : SolverBase {
     void* comm = nullptr;
 
     ~Solver() override {
-        for (cudaGraphExec_t e : {gexec, gexec_first, gexec_mid, gexec_last})
+        for (cudaGraphExec_t e : {gexec, gexec_first, gexec_mid, gexec_last, gexec_mid_t, gexec_last_t})
             if (e) cudaGraphExecDestroy(e);
+        if (trace_rows) cudaFree(trace_rows);
         if (prog_mem) {
             if (st) cudaStreamSynchronize(st);
             cudaFree(prog_mem);
@@ -1080,15 +1086,26 @@ struct Solver : SolverBase {
     void enqueue_first() {
         for (const auto& b : blocks) enqueue_block(b);
     }
-    void enqueue_mid() {
+    // traced: the fused pass keeps all three norms and every finaliser appends its row
+    void enqueue_trace_push() {
+        void* args[] = {&scal, &trace_rows, &trace_count};
+        launch_raw((const void*)trace_push, dim3(1), dim3(32), 0, args);
+    }
+    void enqueue_mid(bool traced = false) {
         const BlockPlan<T>& b0 = blocks[0];
-        launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fused.p);
+        PassParams<T> fp = fused.p;
+        fp.full_norms = traced ? 1 : 0;
+        launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fp);
         enqueue_finalize(fused.p.ngroups, 0);
+        if (traced) enqueue_trace_push();
         if (!b0.sol.fused_reduce) launch(fused_red_l.fn, fused_red_l.grid, dim3(256), 0, fused_red);
         enqueue_solve(b0, &fused_sol);
         for (size_t b = 1; b < blocks.size(); ++b) enqueue_block(blocks[b]);
     }
-    void enqueue_last() { enqueue_xupdate(); }
+    void enqueue_last(bool traced = false) {
+        enqueue_xupdate();
+        if (traced) enqueue_trace_push();
+    }
 
     void init(const void* observed, const uint8_t* mask, const void* G0, void* workspace,
               size_t wbytes, cudaStream_t stream) {
@@ -1209,6 +1226,10 @@ struct Solver : SolverBase {
         gexec_mid = capture_counted([&] { enqueue_mid(); }, n_mid);
         gexec_last = capture_counted([&] { enqueue_last(); }, n_last);
     }
+    void capture_fused_traced() {
+        gexec_mid_t = capture_counted([&] { enqueue_mid(true); }, n_mid_t);
+        gexec_last_t = capture_counted([&] { enqueue_last(true); }, n_last_t);
+    }
 
     void check_flags_sync() {
         CU(cudaMemcpyAsync(hflags, dflags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1231,6 +1252,44 @@ struct Solver : SolverBase {
         if (persist && !need_sync && t_max >= 1) {  // small tensor: every sweep in one launch
             launch_persistent(t_max);
             last_launches = 1;
+            if (done) *done = t_max;
+            end();
+            return;
+        }
+        if (has_fused && trace && !(eps > 0.0) && use_graph && t_max >= 2) {
+            // traced, fixed sweep count: the fused sequence with full norms; every sweep's row
+            // is appended on the device and read back once
+            if (t_max > trace_cap) {
+                if (trace_rows) {
+                    CU(cudaStreamSynchronize(st));
+                    CU(cudaFree(trace_rows));
+                }
+                CU(cudaMalloc(&trace_rows, sizeof(double) * 5 * (size_t)t_max + 64));
+                trace_count = (int*)(trace_rows + 5 * (size_t)t_max);
+                trace_cap = t_max;
+                if (gexec_mid_t) {  // the captured graphs hold the old buffer
+                    cudaGraphExecDestroy(gexec_mid_t);
+                    cudaGraphExecDestroy(gexec_last_t);
+                    gexec_mid_t = gexec_last_t = nullptr;
+                }
+            }
+            if (!gexec_mid) capture_fused();
+            if (!gexec_mid_t) capture_fused_traced();
+            CU(cudaMemsetAsync(trace_count, 0, sizeof(int), st));
+            CU(cudaGraphLaunch(gexec_first, st));
+            for (int sw = 1; sw < t_max; ++sw) CU(cudaGraphLaunch(gexec_mid_t, st));
+            CU(cudaGraphLaunch(gexec_last_t, st));
+            last_launches = n_first + (int64_t)(t_max - 1) * n_mid_t + n_last_t;
+            std::vector<double> rows((size_t)5 * t_max);
+            CU(cudaMemcpyAsync(rows.data(), trace_rows, rows.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+            check_flags_sync();
+            for (int sw = 0; sw < t_max; ++sw) {
+                trace[sw].sweep = (int)rows[5 * sw + 0];
+                trace[sw].rel_change = rows[5 * sw + 1];
+                trace[sw].objective = rows[5 * sw + 2];
+                trace[sw].dx2 = rows[5 * sw + 3];
+                trace[sw].dg2 = rows[5 * sw + 4];
+            }
             if (done) *done = t_max;
             end();
             return;

@@ -724,6 +724,20 @@ static __global__ void __launch_bounds__(1024) finalize_norms(const double* norm
     finalize_norms_body(norms, ngroups, delta, ndelta, sh_off, sh_len, p5, scal, flags, obj_only, combine, s);
 }
 
+// traced fused sweeps: append this sweep's row {sweep, rel_change, objective, dx2, dg2} of
+// scal to the device trace (read back once after the last sweep)
+static __global__ void trace_push(const double* scal, double* rows, int* count) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int c = *count;
+    double* r = rows + 5 * (int64_t)c;
+    r[0] = scal[5];
+    r[1] = scal[4];
+    r[2] = scal[2];
+    r[3] = scal[0];
+    r[4] = scal[3];
+    *count = c + 1;
+}
+
 static __global__ void combine_norms(const double* p5, double* scal, int* flags, int obj_only) {
     pdl_trigger();
     pdl_wait();

@@ -238,6 +238,24 @@ def test_fused_sweeps_match_plain_sweeps(name):
     assert np.array_equal(Xa[obs].view(np.uint8), p.observed[obs].view(np.uint8))
 
 
+@pytest.mark.parametrize("name", ["C1", "C2s", "C4s"])
+def test_traced_fused_rows_match_unfused_trace(name):
+    """eps ≤ 0 with a trace runs the fused sequence with full norms and device-appended rows;
+    the rows match the unfused traced sweeps (same quantities, another summation order)."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE
+    p = make_config(name)
+    a = make_solver(p)
+    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE)
+    da, ra = a.sweep(4, trace=True)
+    db, rb = b.sweep(4, trace=True)
+    assert da == db == 4
+    assert [r["sweep"] for r in ra] == [r["sweep"] for r in rb] == [1, 2, 3, 4]
+    tol = tol_for(p, 1e-4, 1e-10)
+    for x, y in zip(ra, rb):
+        for key in ("objective", "rel_change", "dx2", "dg2"):
+            assert abs(x[key] - y[key]) <= tol * abs(y[key]) + 1e-12, (key, x[key], y[key])
+
+
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C3"])
 def test_fused_three_sweeps_vs_oracle(name):
     """Three sweeps through the fused sequence against three oracle sweeps (north-star bar)."""
