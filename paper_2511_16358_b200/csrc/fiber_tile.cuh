@@ -213,25 +213,24 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
             const int seg_end = min(q1, (vb + 1) * FR);           // end of this kept block
             const int rl = min(min(seg_end - q, rdim0 - ridx[0]), RL);  // tile: r0 run
             // ---- tile setup: slow factors and the (v, i_{r0}) scalar table --------------------
-            int idx[MAXN];
-#pragma unroll
-            for (int m = 0; m < MAXN; ++m) idx[m] = 0;
-            if (P.nkept >= 2) idx[P.kmode[1]] = vb / nb0;
+            int midx = 0;  // index of outer mode m held by lane m (see fiber_walk.cuh)
+            if (P.nkept >= 2 && lane == P.kmode[1]) midx = vb / nb0;
 #pragma unroll
             for (int j = 0; j < MAXN; ++j)
-                if (j < P.nred) idx[P.rmode[j]] = ridx[j];
+                if (j < P.nred && lane == P.rmode[j]) midx = ridx[j];
+            auto idx = [&](int m) { return __shfl_sync(0xffffffffu, midx, m); };
             T ws[EPL];
 #pragma unroll
             for (int e = 0; e < EPL; ++e) ws[e] = ev[e] ? T(1) : T(0);
             for (int t = 0; t < P.nvs; ++t) {
-                const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * I1p + eb;
+                const T* base = Hb + P.vs_off[t] + (int64_t)idx(P.vs_mode[t]) * I1p + eb;
 #pragma unroll
                 for (int e = 0; e < EPL; ++e)
                     if (ev[e]) ws[e] *= base[e];
             }
             T ss = T(1);
             for (int t = 0; t < P.nss; ++t)
-                ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
+                ss *= Hb[P.ss_off[t] + (int64_t)idx(P.ss_q[t]) * P.ss_ld[t] + idx(P.ss_p[t])];
 #pragma unroll
             for (int e = 0; e < EPL; ++e) ws[e] *= ss;
             // scalar factors touching mode 1 or r0, factorised: sf(f,t) = A(v_f)·B(i_{r0,t})·C(v_f, i_{r0,t})
@@ -239,17 +238,29 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
             //   C = H_{1,r0}(v, i_{r0}) unless {1, r0} is the kept pair.
             T* At = sfv + P.sf_cap;
             T* Bt = At + F;
+            // table bases (uniform: the index shuffles need the whole warp)
+            const T* ab[MAXSF];
+            const T* bb[MAXSF];
+#pragma unroll
+            for (int u = 0; u < MAXSF; ++u) {
+                ab[u] = Hb;
+                bb[u] = Hb;
+                if (u < P.nta) ab[u] = Hb + P.ta_off[u] + (int64_t)idx(P.ta_fix[u]) * P.ta_mul[u];
+                if (u < P.nsf) bb[u] = Hb + P.sf_off[u] + (int64_t)idx(P.sf_fixmode[u]) * P.sf_fixmul[u];
+            }
             if (lane < F) {
                 T a = T(1);
                 const int v = b0 + min(lane, nvalid - 1);
-                for (int u = 0; u < P.nta; ++u)
-                    a *= Hb[P.ta_off[u] + (int64_t)idx[P.ta_fix[u]] * P.ta_mul[u] + (int64_t)v * P.ta_inc[u]];
+#pragma unroll
+                for (int u = 0; u < MAXSF; ++u)
+                    if (u < P.nta) a *= ab[u][(int64_t)v * P.ta_inc[u]];
                 At[lane] = a;
             }
             for (int t = lane; t < rl; t += 32) {
                 T b = T(1);
-                for (int u = 0; u < P.nsf; ++u)
-                    b *= Hb[P.sf_off[u] + (int64_t)idx[P.sf_fixmode[u]] * P.sf_fixmul[u] + (int64_t)(ridx[0] + t) * P.sf_inc[u]];
+#pragma unroll
+                for (int u = 0; u < MAXSF; ++u)
+                    if (u < P.nsf) b *= bb[u][(int64_t)(ridx[0] + t) * P.sf_inc[u]];
                 Bt[t] = b;
             }
             __syncwarp();

@@ -471,26 +471,27 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
             for (int e = 0; e < EPL; ++e) sb[e] = sw[e] = T(0);
         }
         // run setup (rare path): indices of every outer mode, slow factors, sf vector
-        int idx[MAXN];
-#pragma unroll
-        for (int m = 0; m < MAXN; ++m) idx[m] = 0;
-        if (P.nkept >= 1) idx[P.kmode[0]] = C.v % (int)P.kdim[0];
-        if (P.nkept >= 2) idx[P.kmode[1]] = C.v / (int)P.kdim[0];
+        // index of outer mode m held by lane m, read with a shuffle (a runtime-indexed local
+        // array would live in local memory)
+        int midx = 0;
+        if (P.nkept >= 1 && lane == P.kmode[0]) midx = C.v % (int)P.kdim[0];
+        if (P.nkept >= 2 && lane == P.kmode[1]) midx = C.v / (int)P.kdim[0];
 #pragma unroll
         for (int j = 0; j < MAXN; ++j)
-            if (j < P.nred) idx[P.rmode[j]] = C.ridx[j];
+            if (j < P.nred && lane == P.rmode[j]) midx = C.ridx[j];
+        auto idx = [&](int m) { return __shfl_sync(0xffffffffu, midx, m); };
         T ws[EPL];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) ws[e] = ev[e] ? T(1) : T(0);
         for (int t = 0; t < P.nvs; ++t) {
-            const T* base = Hb + P.vs_off[t] + (int64_t)idx[P.vs_mode[t]] * I1p + eb;
+            const T* base = Hb + P.vs_off[t] + (int64_t)idx(P.vs_mode[t]) * I1p + eb;
 #pragma unroll
             for (int e = 0; e < EPL; ++e)
                 if (ev[e]) ws[e] *= base[e];
         }
         T ss = T(1);
         for (int t = 0; t < P.nss; ++t)
-            ss *= Hb[P.ss_off[t] + (int64_t)idx[P.ss_q[t]] * P.ss_ld[t] + idx[P.ss_p[t]]];
+            ss *= Hb[P.ss_off[t] + (int64_t)idx(P.ss_q[t]) * P.ss_ld[t] + idx(P.ss_p[t])];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) ws[e] *= ss;
         const int len = C.run_len, ri0 = C.ri0;
@@ -503,7 +504,7 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
                 sfb[t] = Hb;
                 sfi[t] = 0;
                 if (t < P.nsf) {
-                    sfb[t] = Hb + P.sf_off[t] + (int64_t)idx[P.sf_fixmode[t]] * P.sf_fixmul[t] +
+                    sfb[t] = Hb + P.sf_off[t] + (int64_t)idx(P.sf_fixmode[t]) * P.sf_fixmul[t] +
                              (int64_t)ri0 * P.sf_inc[t];
                     sfi[t] = (int)P.sf_inc[t];
                 }
@@ -521,7 +522,7 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
         const T* hrun = hres + (HRES && has_fast ? ri0 * I1p : 0) + ebc;
         T h01v[EPL];  // fused: the excluded pair's column H_{0,1}(·, i_1) completes t = M·H_{0,1}
         if constexpr (kFused) {
-            const T* hb = Hb + P.h01_off + (int64_t)idx[1] * I1p + eb;
+            const T* hb = Hb + P.h01_off + (int64_t)idx(1) * I1p + eb;
 #pragma unroll
             for (int e = 0; e < EPL; ++e) h01v[e] = ev[e] ? hb[e] : T(0);
         }
