@@ -309,7 +309,12 @@ def run_ours(args):
                          "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": k2_gbs / hbm,
                          "traffic": traffic,
                          "bytes_per_launch": k2_bytes, "avg_launch_ms": statistics.mean(k2),
-                         "launches_per_step": len(k2)},
+                         "launches_per_step": len(k2),
+                         # the a2 pass only reads; `peak` is a copy (read + write) peak.  The
+                         # measured read-only ceiling of the same data movement (per-warp TMA
+                         # ring, scripts/readbw.cu) is 7.18 TB/s on this B200 pool.
+                         "read_ceiling_gbs": READ_CEILING_GBS,
+                         "frac_of_read_ceiling": k2_gbs / READ_CEILING_GBS},
             "refill": {"achieved": refill_gbs, "frac": refill_gbs / hbm, "ms": refill_ms,
                        "bytes": refill_bytes},
             "a2_ms_by_block": {f"{k},{i}": round(k2[b], 4) for b, (k, i) in enumerate(
@@ -430,6 +435,9 @@ def rank_grid_extra(torch):
                                       "sweeps_per_s": len(inst) * p.sweeps / el,
                                       "best_rse": res[best]["rse"], "best_ranks": list(MSI_GRID[best])}
     return out
+
+
+READ_CEILING_GBS = 7180.0   # scripts/readbw.cu: TMA ring, 2 KB stages, 1 CTA/SM
 
 
 def main():

@@ -26,15 +26,24 @@ constexpr int kRingStages = IFCTN_RING_D;      // TMA ring depth per warp (stage
 // MASK (refill passes): each stage also carries the Ω bit words of its fibres, MWF 32-bit
 // words per fibre slot (16-B aligned copies that cover the fibre's bits plus the funnel
 // word), or the whole stage's bits in one copy when its fibres are contiguous.
-template <typename T, int EPL, int LPF, bool HRES, bool LOADX, bool MASK = false>
+#ifndef IFCTN_PLAIN_STAGE
+#define IFCTN_PLAIN_STAGE 4096
+#endif
+#ifndef IFCTN_PLAIN_D
+#define IFCTN_PLAIN_D 2
+#endif
+// PLAIN: the plain fibre walk (its accumulators do not grow with F, so its stage size and
+// ring depth are set separately: IFCTN_PLAIN_STAGE bytes, IFCTN_PLAIN_D stages)
+template <typename T, int EPL, int LPF, bool HRES, bool LOADX, bool MASK = false, bool PLAIN = false>
 struct PassCfg {
     static constexpr int FP = 32 / LPF;
     static constexpr int SR = LPF * EPL;  // shared-memory row stride (elements)
     static constexpr int NROW = (LOADX ? 1 : 0) + (HRES ? 0 : 1);
     static constexpr int ROWB = SR * (int)sizeof(T);
-    static constexpr int FK = (2048 / (NROW > 0 ? NROW : 1) / ROWB) / FP;
+    static constexpr int SB = PLAIN ? IFCTN_PLAIN_STAGE : 2048;
+    static constexpr int FK = (SB / (NROW > 0 ? NROW : 1) / ROWB) / FP;
     static constexpr int F = FP * (FK > 1 ? FK : 1);
-    static constexpr int D = kRingStages;
+    static constexpr int D = PLAIN ? IFCTN_PLAIN_D : kRingStages;
     static constexpr int XH = NROW * F * SR;                       // X/H elements per stage
     static constexpr int MWF = MASK ? ((SR / 32 + 9 + 3) & ~3) : 0;  // mask words per fibre
     static constexpr int MW = F * MWF;                             // mask words per stage

@@ -339,7 +339,7 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
     constexpr bool kNorms = (MODE == PASS_REFILL || MODE == PASS_OBJ || kFused);
     constexpr bool kLoadX = (MODE != PASS_MODEL);
     constexpr bool kMask = (MODE == PASS_REFILL || kFused);
-    using Cfg = PassCfg<T, EPL, LPF, HRES, kLoadX, kMask>;
+    using Cfg = PassCfg<T, EPL, LPF, HRES, kLoadX, kMask, true>;
     constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR, NROW = Cfg::NROW;
     constexpr int STAGE = Cfg::STAGE;  // elements per ring stage (X, H rows, Ω words)
     constexpr int MWF = Cfg::MWF;

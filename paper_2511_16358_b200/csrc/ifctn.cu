@@ -372,7 +372,7 @@ struct PassKernel {
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 static PassKernel pk() {
     constexpr int M0 = MODE % 100;
-    using Cfg = PassCfg<T, EPL, LPF, HRES, M0 != PASS_MODEL, M0 == PASS_REFILL || M0 == PASS_FUSED>;
+    using Cfg = PassCfg<T, EPL, LPF, HRES, M0 != PASS_MODEL, M0 == PASS_REFILL || M0 == PASS_FUSED, (MODE < 100)>;
     if constexpr (MODE >= 100) {
         constexpr int M = MODE - 100;
         if constexpr ((M == PASS_KEPT1 || M == PASS_RED1 || M == PASS_FUSED) && HRES)

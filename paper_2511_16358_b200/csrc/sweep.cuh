@@ -94,8 +94,11 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
                 __syncthreads();
                 // retire this pass's stage barriers before the shared memory is reused
                 if (lane == 0) {
-                    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * kRingStages;
-                    for (int s = 0; s < kRingStages; ++s) mbar_inval(bars + s);
+                    // (8 barrier slots per warp are reserved; invalidate the ones a pass uses)
+                    constexpr int DB = IFCTN_PLAIN_D > kRingStages ? IFCTN_PLAIN_D : kRingStages;
+                    const int d = (op.variant & 2) ? kRingStages : IFCTN_PLAIN_D;
+                    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw) + warp * d;
+                    for (int s = 0; s < d && s < DB; ++s) mbar_inval(bars + s);
                 }
             } else if (op.kind == OP_REDUCE) {
                 const ReduceParams<T>& P = G.red[op.idx];
