@@ -24,9 +24,8 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
     // PASS_FUSED: a5 refill of sweep s fused with block (0,1)'s a2 of sweep s+1 (K = {0,1}):
     // t = M·H_{0,1}(i_0, v), X_new written back and used for β.
     constexpr bool kFused = (MODE == PASS_FUSED);
-    // KEPT1/FUSED tiles keep modes {1, 2} (code 0, 1): H_{0,1} is the excluded pair, so only
-    // RED1 tiles multiply by an H_{0,1} column
-    constexpr bool kH1 = (MODE == PASS_RED1);
+    // KEPT1/FUSED tiles keep modes {1, 2} (code 0, 1): H_{0,1} is the excluded pair; RED1
+    // tiles apply their H_{0,1} column at the flush
     using Cfg = PassCfg<T, EPL, LPF, true, true, kFused>;
     constexpr int D = Cfg::D, F = Cfg::F, FP = Cfg::FP, SR = Cfg::SR;
     constexpr int STAGE = Cfg::STAGE;
@@ -294,13 +293,10 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
                     const int f = st * FP + fsub;
                     if (f < nvalid) {
                         T w[EPL], x[EPL];
-                        if constexpr (kH1) {
-                            T h[EPL];
-                            lds_vec<T, EPL>(h1 + (b0 + f) * h1step, h);
-                            weight<T, EPL>(wr, h, sfv[t * F + f], w);
-                        } else {  // H_{0,1} is the excluded pair: M = wr · sf
-                            scale<T, EPL>(wr, sfv[t * F + f], w);
-                        }
+                        // RED1: the column H_{0,1}(·, v_f) is constant over the kept block, so it
+                        // is applied to the accumulators at the flush (Σ h·u·x = h·Σ u·x,
+                        // Σ (h·u)² = h²·Σ u²); KEPT1/FUSED: H_{0,1} is the excluded pair
+                        scale<T, EPL>(wr, sfv[t * F + f], w);
                         lds_vec<T, EPL>(sx + f * SR + eb, x);
                         if constexpr (kFused) {
                             T h01[EPL], tt[EPL], xn[EPL];
@@ -355,11 +351,13 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
                             }
                         }
                     } else {
+                        T hf[EPL];
+                        lds_vec<T, EPL>(h1 + (b0 + min(f, nvalid - 1)) * h1step, hf);
                         T tb = T(0), tw = T(0);
 #pragma unroll
                         for (int e = 0; e < EPL; ++e) {
-                            tb += sb[st][e];
-                            tw += sw[st][e];
+                            tb = fma(hf[e], sb[st][e], tb);
+                            tw = fma(hf[e] * hf[e], sw[st][e], tw);
                         }
 #pragma unroll
                         for (int o = LPF / 2; o > 0; o >>= 1) {  // the fibre's LPF lanes
