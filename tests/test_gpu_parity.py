@@ -273,6 +273,20 @@ def test_fused_three_sweeps_vs_oracle(name):
     assert rel(s.reconstruct().cpu().numpy(), X) <= tol
 
 
+@pytest.mark.parametrize("name", ["C2s", "C4s", "C2rs"])
+def test_pdl_launches_bit_identical(name):
+    """IFCTN_FLAG_PDL (programmatic dependent launch: kernels start early and wait in
+    griddepcontrol.wait) changes only launch timing, never results."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_PDL
+    p = make_config(name)
+    a = make_solver(p, flags=IFCTN_FLAG_PDL)
+    b = make_solver(p)
+    for x in (a, b):
+        x.sweep(3)
+    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
+    assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
+
+
 @pytest.mark.timeout(120)
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C2", "C4"])
 def test_persistent_sweeps_bit_identical_to_launch_sequence(name):
