@@ -1,5 +1,6 @@
-// fiber_pass.cuh — K2 (coefficient contraction, step a2) and K4 (model rebuild + masked
-// refill + norms, step a5) as one streaming kernel family over X in fibre order.
+// fiber_walk.cuh — K2 (coefficient contraction, step a2) and K4 (model rebuild + masked
+// refill + norms, step a5) as one streaming kernel family over X in fibre order (the plain
+// walk; fiber_tile.cuh is the tiled walk for blocks keeping mode 2).
 //
 // Paper: Prop. 1 gives the mode-k coefficient matrix Z_k = diag(vec S_k)·⊗G;
 // Eq. 8 solves column j of G_{k,i} from (y_j ⊗ G_{i,k}) D.  Written out per
@@ -20,10 +21,11 @@
 // (16-B shared-memory vectors; fp32 math in packed FMUL2/FFMA2 pairs).
 // Data movement is a TMA pipeline that runs ahead across run and segment boundaries: lane 0
 // (the producer, with its own copy of the fibre walker) issues cp.async.bulk copies of F
-// fibres of X (and their H columns when !HRES) per stage into a D-stage shared-memory ring
-// guarded by mbarriers; all 32 lanes consume.  Reductions are deterministic: lane-local
-// accumulation, one partial slot per (warp, v) pair, and a fixed-order fp64 second stage
-// (reduce_partials).
+// fibres of X (and their H columns when !HRES; the Ω words for refills) per stage into a
+// D-stage shared-memory ring guarded by mbarriers (4 KB × 2 stages, PassCfg PLAIN); all 32
+// lanes consume.  The run-constant slow factor ws is applied once per run.  Reductions are
+// deterministic: lane-local accumulation, one partial slot per (warp, v) pair, and a
+// fixed-order fp64 second stage (reduce_partials, or the solve itself: block_solve).
 #pragma once
 
 #include "common.cuh"
