@@ -18,7 +18,21 @@ ncu --set full --clock-control none --import-source on -k regex:"fiber_pass|redu
     -c 62 -o $OUT/sweep -f python scripts/ncu_target.py --config C5 --sweeps 1 > $OUT/ncu_sweep.log 2>&1
 python scripts/ncu_summary.py $OUT/sweep.ncu-rep 0 > $OUT/ncu_sweep_summary.txt 2>&1
 python scripts/ncu_per_launch.py $OUT/sweep.ncu-rep > $OUT/ncu_sweep_per_launch.txt 2>&1
-for l in 0 1 5 60; do
+# source hot spots of: the first tiled pass, the first plain pass, the first solve, the refill
+PICK=$(python - "$OUT/ncu_sweep_per_launch.txt" << 'PY'
+import sys
+rows = [l.split() for l in open(sys.argv[1]) if l[:4].strip().isdigit()]
+def first(pred):
+    for r in rows:
+        if pred(r[1] + " " + r[2]):
+            return r[0]
+    return None
+picks = [first(lambda n: n.startswith("fiber_pass_vb")), first(lambda n: n.startswith("fiber_pass<") and "2," not in n),
+         first(lambda n: n.startswith("block_solve")), first(lambda n: n.startswith("fiber_pass<float, 2"))]
+print(" ".join(p for p in picks if p is not None))
+PY
+)
+for l in $PICK; do
   python scripts/ncu_summary.py $OUT/sweep.ncu-rep $l > $OUT/ncu_src_launch$l.txt 2>&1
 done
 rm -f $OUT/sweep.ncu-rep
