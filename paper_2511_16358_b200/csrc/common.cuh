@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <type_traits>
 
@@ -95,6 +96,24 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
                  : "=d"(r.x), "=d"(r.y) : "l"(p));
     return r;
 }
+
+// ---- debug builds (IFCTN_DEBUG_CHECKS): device-side bounds checks on the computed indices
+// of partial slots, TMA source ranges and mask words (compute-sanitizer is not available on
+// the B200 pool); a failed check prints and traps the kernel.
+#ifdef IFCTN_DEBUG_CHECKS
+#define IFCTN_CHECK(cond, what)                                                              \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("IFCTN_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__,     \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define IFCTN_CHECK(cond, what) \
+    do {                        \
+    } while (0)
+#endif
 
 // ---- programmatic dependent launch (sweep kernels are launched with programmatic stream
 // serialization: the next kernel's CTAs may start while this one runs; each kernel lets its
@@ -247,6 +266,7 @@ struct PassParams {
     int64_t sfv_stride;            // per-warp elements of the sf scratch
     unsigned* sched;               // tiled pass: [next chunk, retired warps], zero between launches
     int full_norms;                // fused pass: all three norms (traced sweeps), else ‖X_new‖² only
+    int64_t part_cap, x_cap, mask_cap;  // element / word capacities (IFCTN_DEBUG_CHECKS)
 };
 
 template <typename T>
@@ -267,6 +287,7 @@ struct ReduceParams {
     // its z-th share of the slots; Z > 1 combines the Z partials in z order in the last CTA
     // to arrive (scr/cnt), so the sum order is fixed for a given Z.
     int ET, ntile, Z;
+    int64_t part_cap;    // partial-slot capacity (IFCTN_DEBUG_CHECKS)
     double* scr;         // ≥ NV·ntile·Z·ET·2 doubles when Z > 1
     unsigned* cnt;       // ≥ NV·ntile counters, zero between launches
 };

@@ -157,10 +157,13 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
             } else {
                 for (int f = 0; f < nvalid; ++f) {
                     const uint32_t b = mask_span(pg0 + (int64_t)f * I1p, I1p, ma0);
+                    IFCTN_CHECK(ma0 + (int64_t)(b / 4) <= P.mask_cap && b <= (uint32_t)(MWF * 4), "tiled fibre mask words");
                     tma_g2s_a(sm + (uint32_t)(f * MWF * 4), P.mask + ma0, b, bar);
                 }
             }
         }
+        IFCTN_CHECK(((int64_t)fib + nvalid) * I1p <= P.x_cap, "tiled X range");
+        IFCTN_CHECK(!kFused || SR != I1p || ma0 + (int64_t)(mbytes / 4) <= P.mask_cap, "tiled mask words");
         const T* xs = P.X + (int64_t)fib * I1p;
         if (SR == I1p) {
             tma_g2s_a(sx, xs, (uint32_t)nvalid * rowbytes, bar);
@@ -334,6 +337,7 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
                 for (int st = 0; st < NS; ++st) {
                     const int f = st * FP + fsub;
                     const int64_t slot = ((int64_t)group + vb) * F + f;
+                    IFCTN_CHECK(f >= nvalid || (slot + 1) * P.Lv <= P.part_cap, "tiled slot");
                     if constexpr (MODE == PASS_KEPT1 || kFused) {
                         if (f < nvalid) {
                             T* pbd = P.part_b + slot * P.Lv + eb;

@@ -432,10 +432,13 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
             } else {
                 for (int f = 0; f < nf; ++f) {
                     const uint32_t b = mask_span(pg0 + (int64_t)f * xstep, I1p, ma0);
+                    IFCTN_CHECK(ma0 + (int64_t)(b / 4) <= P.mask_cap && b <= (uint32_t)(MWF * 4), "plain fibre mask words");
                     tma_g2s_a(sm + (uint32_t)(f * MWF * 4), P.mask + ma0, b, bar);
                 }
             }
         }
+        IFCTN_CHECK(!kLoadX || (p_x - P.X) + (int64_t)(nf - 1) * xstep + I1p <= P.x_cap, "plain X range");
+        IFCTN_CHECK(!kMask || !xmerge || ma0 + (int64_t)(mbytes / 4) <= P.mask_cap, "plain mask words");
         if constexpr (kLoadX) {
             if (xmerge) {
                 tma_g2s_a(sx, p_x, (uint32_t)nf * rowbytes, bar);
@@ -616,6 +619,7 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
                         sw[e] += __shfl_xor_sync(0xffffffffu, sw[e], o);
                     }
                 if (fsub == 0) {
+                    IFCTN_CHECK(((int64_t)group + C.v + 1) * P.Lv <= P.part_cap, "plain KEPT1 slot");
                     T* pbd = P.part_b + ((int64_t)group + C.v) * P.Lv + eb;
                     T* pwd = P.part_w + ((int64_t)group + C.v) * P.Lv + eb;
                     if (lane_full) {
@@ -644,6 +648,7 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
                 }
                 if (lane == 0) {
                     const int64_t slot = (int64_t)group + C.v;
+                    IFCTN_CHECK(slot < P.part_cap, "plain RED1 slot");
                     P.part_b[slot] = tb;
                     P.part_w[slot] = tw;
                 }

@@ -590,6 +590,9 @@ struct Solver : SolverBase {
         p.Xw = X;
         p.mask = bits;
         p.part_b = pb;
+        p.part_cap = s.part_elems;
+        p.x_cap = s.npad;
+        p.mask_cap = (align_up((s.npad + 31) / 32, 8) + 8);
         p.part_w = pw;
         p.norms = norms;
         p.rho = (T)rho;
@@ -819,6 +822,7 @@ struct Solver : SolverBase {
                 b.pass = make_pass(mode, k, i, vblk);
                 ReduceParams<T>& r = b.red;
                 r.part_b = pb;
+                r.part_cap = s.part_elems;
                 r.part_w = pw;
                 r.beta = beta;
                 r.omega = omega;

@@ -44,6 +44,7 @@ __device__ __forceinline__ void reduce_partials_warp_body(const ReduceParams<T>&
     int64_t nslots;
     const int64_t base = slot_base(P, v, nslots);
     const int64_t stride = P.VB;  // Lv = 1: consecutive slots are VB elements apart
+    IFCTN_CHECK(nslots < 1 || base + (nslots - 1) * stride < P.part_cap, "reduce_warp slots");
     double b = 0.0, w = 0.0;
     for (int64_t s = lane; s < nslots; s += 32) {
         b += (double)P.part_b[base + s * stride];
@@ -192,6 +193,7 @@ __device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t 
     int64_t nslots;
     const int64_t base = slot_base(Q, v, nslots) + e;
     const int64_t stride = Q.VB * Q.Lv;
+    IFCTN_CHECK(nslots < 1 || base + (nslots - 1) * stride < Q.part_cap, "solve gather slots");
     double sb = 0.0, sw = 0.0;
     for (int64_t s = 0; s < nslots; ++s) {
         sb += (double)Q.part_b[base + s * stride];
