@@ -353,6 +353,7 @@ struct BlockPlan {
     SolveParams<T> sol;
     dim3 sol_grid;
     unsigned sol_threads = 128;
+    bool sol_warp = false;     // block_solve_w: a warp per column
     size_t sol_smem = 0;
     const void* sol_fn = nullptr;
     // multi-GPU, k ≠ shard mode: project → all-reduce → solve
@@ -426,6 +427,21 @@ static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
 }
 
 template <typename T, int SM>
+static const void* pick_solve_w(int R) {
+    switch (R) {
+        case 1: return (const void*)block_solve_w<T, 1, SM>;
+        case 2: return (const void*)block_solve_w<T, 2, SM>;
+        case 3: return (const void*)block_solve_w<T, 3, SM>;
+        case 4: return (const void*)block_solve_w<T, 4, SM>;
+        case 5: return (const void*)block_solve_w<T, 5, SM>;
+        case 6: return (const void*)block_solve_w<T, 6, SM>;
+        case 7: return (const void*)block_solve_w<T, 7, SM>;
+        case 8: return (const void*)block_solve_w<T, 8, SM>;
+        default: return (const void*)block_solve_w<T, 9, SM>;
+    }
+}
+
+template <typename T, int SM>
 static const void* pick_solve_sm(int R) {
     switch (R) {
         case 1: return (const void*)block_solve<T, 1, SM>;
@@ -441,7 +457,12 @@ static const void* pick_solve_sm(int R) {
 }
 
 template <typename T>
-static const void* pick_solve(int R, int sm = SOLVE_FULL) {
+static const void* pick_solve(int R, int sm = SOLVE_FULL, bool warp = false) {
+    if (warp && R <= MAXR_SMALL) {
+        if (sm == SOLVE_PROJECT) return pick_solve_w<T, SOLVE_PROJECT>(R);
+        if (sm == SOLVE_FROM_PROJ) return pick_solve_w<T, SOLVE_FROM_PROJ>(R);
+        return pick_solve_w<T, SOLVE_FULL>(R);
+    }
     if (R > MAXR_SMALL) {
         const void* fn = sm == SOLVE_PROJECT     ? (const void*)block_solve_big<T, SOLVE_PROJECT>
                          : sm == SOLVE_FROM_PROJ ? (const void*)block_solve_big<T, SOLVE_FROM_PROJ>
@@ -500,6 +521,8 @@ struct Solver : SolverBase {
     int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
     bool pdl = false;                      // programmatic dependent launch (IFCTN_FLAG_PDL)
     int64_t chunks_per_warp = kChunksPerWarp;  // tiled-pass chunks per warp (env knob)
+    bool solve_warp = false;               // warp-per-system small-rank solve (env IFCTN_TUNE_SOLVE_WARP=1;
+                                           // measured slower on C2–C5, faster on C1)
     int64_t solve_slots = 64;              // max serial slot chain for the solve to absorb
                                            // the reduce (env IFCTN_TUNE_SOLVE_SLOTS)
     int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
@@ -867,6 +890,8 @@ struct Solver : SolverBase {
                 const bool gather_ok = r.kept1 ? (i == 0 && chain <= solve_slots) : (slots_per_v <= 16 && s.ld[i] >= 16);
                 q.fused_reduce = (q.R <= MAXR_SMALL && gather_ok && !(flags & IFCTN_FLAG_NO_SOLVE_REDUCE)) ? 1 : 0;
                 b.sol_grid = dim3((unsigned)s.ld[k]);
+                b.sol_warp = solve_warp && q.R <= MAXR_SMALL;
+                if (b.sol_warp) b.sol_grid = dim3((unsigned)((s.ld[k] + 3) / 4));
                 if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): a CTA per column
                     b.sol_threads = kBigThreads;
                     // stage all of G_{i,k} at once when it fits in ≈ 96 KB, else 32-column tiles
@@ -886,11 +911,11 @@ struct Solver : SolverBase {
                 b.dist = s.dpath && k != s.shard;
                 if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
                     const int R = s.R(k, i);
-                    b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT);
-                    b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ);
+                    b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT, b.sol_warp);
+                    b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ, b.sol_warp);
                     b.proj_count = s.ld[k] * (R * (R + 1) / 2 + R);
                 } else {
-                    b.sol_fn = pick_solve<T>(s.R(k, i));
+                    b.sol_fn = pick_solve<T>(s.R(k, i), SOLVE_FULL, b.sol_warp);
                 }
                 blocks.push_back(b);
             }
@@ -960,9 +985,9 @@ struct Solver : SolverBase {
             }
             SweepOp op{};
             op.kind = b.sol.R > MAXR_SMALL ? OP_SOLVE_BIG : OP_SOLVE;
-            op.variant = b.sol.R;
+            op.variant = b.sol.R + (b.sol_warp ? 16 : 0);
             op.idx = (int)sv.size();
-            op.nvb = s.ld[b.k];
+            op.nvb = b.sol_warp ? (s.ld[b.k] + 3) / 4 : s.ld[b.k];
             sv.push_back(b.sol);
             ops.push_back(op);
             if (op.kind == OP_SOLVE_BIG) smem = std::max(smem, sweep_scratch_bytes(b.sol_smem));
@@ -1124,6 +1149,7 @@ struct Solver : SolverBase {
         pdl = (flags & IFCTN_FLAG_PDL) != 0;
         if (const char* e = getenv("IFCTN_TUNE_CHUNKS")) chunks_per_warp = std::max(1, atoi(e));
         if (const char* e = getenv("IFCTN_TUNE_SOLVE_SLOTS")) solve_slots = atoi(e);
+        if (const char* e = getenv("IFCTN_TUNE_SOLVE_WARP")) solve_warp = atoi(e) != 0;
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));

@@ -203,17 +203,24 @@ __device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t 
     w = sw;
 }
 
-template <typename T, int R, int SM>
+template <typename T, int R, int SM, bool W = false>
 // nthr (a multiple of 32, ≤ blockDim.x) threads take part; the others only pass the barriers
 __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_t j, int nthr,
                                                  double* red /*(nthr/32)·NA*/, double* cs /*R*/) {
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
     const int nw = nthr >> 5;
+    // W: the "CTA" is one warp (warp-per-system: lane ids, __syncwarp, nthr = 32)
+    const int tid = W ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+    const int ntot = W ? 32 : (int)blockDim.x;
+    auto sync = [&]() {
+        if constexpr (W) __syncwarp();
+        else __syncthreads();
+    };
     double acc[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
-    for (int64_t a = threadIdx.x; a < (SM == SOLVE_FROM_PROJ || (int)threadIdx.x >= nthr ? 0 : P.Ii); a += nthr) {
+    for (int64_t a = tid; a < (SM == SOLVE_FROM_PROJ || tid >= nthr ? 0 : P.Ii); a += nthr) {
         double b, w;
         if (P.fused_reduce) {
             column_coeffs(P.red, j, a, b, w);
@@ -232,17 +239,16 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[NG + r] += b * g[r];
     }
-    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const int wid = tid >> 5, ln = tid & 31;
     if constexpr (SM != SOLVE_FROM_PROJ) {
 #pragma unroll
         for (int t = 0; t < NA; ++t) {
             const double s = warp_sum(acc[t]);
             if (ln == 0 && wid < nw) red[wid * NA + t] = s;
         }
-        __syncthreads();
+        sync();
         if constexpr (SM == SOLVE_PROJECT) {
-            if (threadIdx.x < NA) {
-                const int t = threadIdx.x;
+            for (int t = tid; t < NA; t += ntot) {
                 double v = 0.0;
                 for (int q = 0; q < nw; ++q) v += red[q * NA + t];
                 P.proj[j * NA + t] = v;
@@ -250,7 +256,7 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
             return;
         }
     }
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double sum[NA];
 #pragma unroll
         for (int t = 0; t < NA; ++t) {
@@ -325,9 +331,9 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
         }
         P.delta[j] = d2;
     }
-    __syncthreads();
+    sync();
     // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a)
-    for (int64_t a = threadIdx.x; a < P.Ii; a += blockDim.x) {
+    for (int64_t a = tid; a < P.Ii; a += ntot) {
         double h = 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) h += cs[r] * (double)P.Gik[a * R + r];
@@ -344,6 +350,19 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     __shared__ double red[4 * NA];
     __shared__ double cs[R];
     block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs);
+}
+
+// warp per system: 4 columns per 128-thread CTA, no CTA-wide barrier (north-star design)
+template <typename T, int R, int SM>
+__global__ void __launch_bounds__(128) block_solve_w(const SolveParams<T> P) {
+    pdl_trigger();
+    pdl_wait();
+    constexpr int NA = R * (R + 1) / 2 + R;
+    __shared__ double red[4][NA];
+    __shared__ double cs[4][R];
+    const int w = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 4 + w;
+    if (j < P.Ik) block_solve_body<T, R, SM, true>(P, j, 32, red[w], cs[w]);
 }
 
 // ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------

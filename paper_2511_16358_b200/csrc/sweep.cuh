@@ -62,6 +62,27 @@ __device__ __forceinline__ void run_pass(int variant, const PassParams<T>& P, un
     }
 }
 
+// variant ≥ 16: warp per column (block_solve_w): warps 0–3 take columns 4·vb + warp
+template <typename T>
+__device__ __forceinline__ void run_solve_w(int R, const SolveParams<T>& P, int64_t vb, double* red, double* cs) {
+    const int w = threadIdx.x >> 5;
+    const int64_t j = vb * 4 + w;
+    if (w >= 4 || j >= P.Ik) return;
+    double* rw = red + w * 64;
+    double* cw = cs + w * 16;
+    switch (R) {
+        case 1: block_solve_body<T, 1, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 2: block_solve_body<T, 2, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 3: block_solve_body<T, 3, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 4: block_solve_body<T, 4, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 5: block_solve_body<T, 5, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 6: block_solve_body<T, 6, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 7: block_solve_body<T, 7, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        case 8: block_solve_body<T, 8, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+        default: block_solve_body<T, 9, SOLVE_FULL, true>(P, j, 32, rw, cw); break;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void run_solve(int R, const SolveParams<T>& P, int64_t j, double* red, double* cs) {
     switch (R) {
@@ -116,7 +137,8 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
             } else if (op.kind == OP_SOLVE) {
                 const SolveParams<T>& P = G.sol[op.idx];
                 for (int64_t j = cta; j < op.nvb; j += ncta) {
-                    run_solve<T>(op.variant, P, j, scratch, scratch + 4 * 64);
+                    if (op.variant >= 16) run_solve_w<T>(op.variant - 16, P, j, scratch, scratch + 4 * 64);
+                    else run_solve<T>(op.variant, P, j, scratch, scratch + 4 * 64);
                     __syncthreads();
                 }
             } else if (op.kind == OP_SOLVE_BIG) {
