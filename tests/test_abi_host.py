@@ -122,3 +122,28 @@ def test_python_package_has_no_fallback():
     for f in os.listdir(os.path.join(ROOT, "paper_2511_16358_b200")):
         if f.endswith(".py"):
             assert "import oracle" not in open(os.path.join(ROOT, "paper_2511_16358_b200", f)).read()
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/ifctn.h is a C-ABI header: it compiles as C99 (no C++ or CUDA types) and a C
+    program can link against libifctn.so with it."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "use.c"
+    src.write_text('#include "include/ifctn.h"\n#include <stdio.h>\n'
+                   'int main(void) {\n'
+                   '  int64_t dims[3] = {4, 5, 6}; int32_t r[9] = {0,2,2, 2,0,2, 2,2,0}; size_t b = 0;\n'
+                   '  ifctn_status s = ifctn_workspace_bytes(3, dims, r, IFCTN_F32, NULL, &b);\n'
+                   '  printf("%s %zu\\n", ifctn_status_string(s), b);\n'
+                   '  return s == IFCTN_OK && b > 0 ? 0 : 1;\n}\n')
+    lib = os.path.join(root, "paper_2511_16358_b200")
+    exe = tmp_path / "use"
+    subprocess.check_call([gcc, "-std=c99", "-Wall", "-Werror", "-I", root, str(src), "-o", str(exe),
+                           "-L", lib, "-lifctn", f"-Wl,-rpath,{lib}"])
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("IFCTN_OK")
