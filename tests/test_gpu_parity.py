@@ -321,6 +321,22 @@ def test_full_run_rse_parity(name, sweeps):
     assert abs(rg - ro) <= 1e-3 * ro + floor, (rg, ro)
 
 
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C2r"])
+def test_full_size_full_run_rse_parity(name):
+    """North star: final RSE within 1e-3 relative after the FULL configured run, at full size
+    (C2 100, C3 100, C4 200, C2r 100 sweeps; the oracle takes ≈ 1–16 s each on 16 cores).
+    C5's 50-sweep run (595 s of oracle time) is in profiles/r1/c5_full_parity.json."""
+    p = make_config(name)
+    s = make_solver(p)
+    s.sweep(p.sweeps)
+    e_gpu = s.rse(dev(p.truth))
+    sh, G, X = oracle_state(p)
+    r, _ = O.solve(sh, G, X, p.mask, p.rho, p.sweeps, 0.0, False)
+    assert r == p.sweeps
+    e = O.rse(p.truth.astype(np.float64), X)
+    assert abs(e_gpu - e) <= 1e-3 * e + 1e-5, (e_gpu, e)
+
+
 def test_objective_and_rse_against_oracle():
     p = make_config("C3s")
     s = make_solver(p)
