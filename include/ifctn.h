@@ -74,6 +74,9 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
                                        * persistent cooperative launch (sweep.cuh); default
                                        * for single-GPU tensors of ≤ 64 Mi entries          */
 #define IFCTN_FLAG_NO_PERSISTENT 256u /* never use the persistent sweep kernel            */
+#define IFCTN_FLAG_PASS_FINALIZE 512u   /* experimental: the norm passes run the sweep
+                                          * finaliser in their last CTA (one launch fewer;
+                                          * measured no faster — off by default)         */
 #define IFCTN_FLAG_PDL 32u      /* experimental: launch sweep kernels with programmatic
                                   * dependent launch (measured: no gain on C2-C5, a loss on
                                   * C2r — off by default)                                   */

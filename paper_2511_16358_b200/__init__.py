@@ -16,7 +16,8 @@ import numpy as np
 
 from . import _abi
 from ._abi import (IFCTN_F32, IFCTN_F64, IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_PDL,  # noqa: F401
-                   IFCTN_FLAG_NO_PERSISTENT, IFCTN_FLAG_NO_SOLVE_REDUCE, IFCTN_FLAG_NO_VBLOCK, IFCTN_FLAG_PERSISTENT,
+                   IFCTN_FLAG_PASS_FINALIZE, IFCTN_FLAG_NO_PERSISTENT, IFCTN_FLAG_NO_SOLVE_REDUCE,
+                   IFCTN_FLAG_NO_VBLOCK, IFCTN_FLAG_PERSISTENT,
                    IFCTN_FLAG_NONE, IFCTN_FLAG_X_FULL, IFCTN_MODEL, IFCTN_X, IfctnError,
                    ifctn_dist, ifctn_trace_row)
 

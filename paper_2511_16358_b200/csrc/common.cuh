@@ -267,6 +267,16 @@ struct PassParams {
     unsigned* sched;               // tiled pass: [next chunk, retired warps], zero between launches
     int full_norms;                // fused pass: all three norms (traced sweeps), else ‖X_new‖² only
     int64_t part_cap, x_cap, mask_cap;  // element / word capacities (IFCTN_DEBUG_CHECKS)
+    // norm passes: the last CTA to finish runs the sweep finaliser (finalize_norms_body) —
+    // one launch fewer per sweep; fin_cnt is the arrival counter (self-resetting)
+    int fin;
+    unsigned* fin_cnt;
+    const double* fin_delta;
+    int64_t fin_ndelta, fin_sh_off, fin_sh_len;
+    double* fin_p5;
+    double* fin_scal;
+    int* fin_flags;
+    int fin_obj_only, fin_combine;
 };
 
 template <typename T>

@@ -414,6 +414,8 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     fiber_pass_vb_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, gridDim.x);
+    if constexpr (MODE == PASS_FUSED)
+        if (P.fin) pass_finalize(P, smem_raw);
 }
 
 }  // namespace ifctn

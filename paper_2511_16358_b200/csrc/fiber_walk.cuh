@@ -29,6 +29,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "solve.cuh"  // finalize_norms_body (last-CTA finaliser of the norm passes)
 
 namespace ifctn {
 
@@ -670,10 +671,32 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
     }
 }
 
+// Last-CTA sweep finaliser of a norm pass (PassParams::fin): after the body, every CTA
+// arrives on fin_cnt; the last one sums the norm partials and ΔG² (finalize_norms_body, the
+// same fixed order as the standalone finalize_norms launch) in its now idle shared memory.
+template <typename T>
+__device__ __forceinline__ void pass_finalize(const PassParams<T>& P, unsigned char* smem_raw) {
+    __shared__ unsigned last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = (atomicAdd(P.fin_cnt, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    finalize_norms_body(P.norms, P.ngroups, P.fin_delta, P.fin_ndelta, P.fin_sh_off, P.fin_sh_len, P.fin_p5,
+                        P.fin_scal, P.fin_flags, P.fin_obj_only, P.fin_combine,
+                        reinterpret_cast<double*>(smem_raw));
+    if (threadIdx.x == 0) *P.fin_cnt = 0u;
+}
+
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     fiber_pass_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, blockIdx.x);
+    if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ || MODE == PASS_FUSED)
+        if (P.fin) pass_finalize(P, smem_raw);
 }
 
 }  // namespace ifctn

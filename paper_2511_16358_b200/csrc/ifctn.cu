@@ -764,7 +764,13 @@ struct Solver : SolverBase {
         pp.fn = kern.fn;
         if (smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "fibre-pass shared memory exceeds the device limit");
         // one kernel serves several passes with different sizes: allow the device maximum
-        CU(cudaFuncSetAttribute(pp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit));
+        {
+            cudaFuncAttributes fa;
+            CU(cudaFuncGetAttributes(&fa, pp.fn));
+            if (smem + fa.sharedSizeBytes > smem_limit) fail(IFCTN_E_UNSUPPORTED, "fibre-pass shared memory exceeds the device limit");
+            CU(cudaFuncSetAttribute(pp.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(smem_limit - fa.sharedSizeBytes)));
+        }
         int nb = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pp.fn, kPassThreads, smem));
         if (nb < 1) nb = 1;
@@ -943,6 +949,44 @@ struct Solver : SolverBase {
             fused_sol.red = fused_red;
             has_fused = true;
         }
+        set_fin(refill, 0);
+        set_fin(obj, 1);
+        if (has_fused) set_fin(fused, 0);
+    }
+
+    // IFCTN_FLAG_PASS_FINALIZE: the norm passes run the sweep finaliser in their last CTA
+    // (needs 40 KB of their shared memory as scratch; bit-identical to the finalize_norms
+    // launch, measured no faster — the 1024-thread finaliser kernel is quicker than one
+    // 256-thread CTA at the end of a pass)
+    void set_fin(PassPlan<T>& pp, int obj_only) {
+        PassParams<T>& p = pp.p;
+        p.fin = ((flags & IFCTN_FLAG_PASS_FINALIZE) && pp.smem >= sizeof(double) * 5 * 1024) ? 1 : 0;
+        p.fin_cnt = sched + 4;
+        p.fin_delta = delta;
+        p.fin_ndelta = obj_only ? 0 : s.ndelta;
+        p.fin_sh_off = sh_off;
+        p.fin_sh_len = sh_len;
+        p.fin_p5 = p5;
+        p.fin_scal = scal;
+        p.fin_flags = dflags;
+        p.fin_obj_only = obj_only;
+        p.fin_combine = s.dpath ? 0 : 1;
+    }
+
+    // after a norm pass: its finaliser (in-pass or a launch), then the cross-rank combine
+    void finish_norm_pass(const PassParams<T>& p, int obj_only) {
+        if (!p.fin) {
+            enqueue_finalize(p.ngroups, obj_only);
+            return;
+        }
+        prof_mark();  // the finaliser ran inside the pass: empty interval in ifctn_profile_sweep
+        if (s.dpath) {
+            allreduce_dev(p5, 4);
+            prof_mark();
+            int a3 = obj_only;
+            void* args[] = {&p5, &scal, &dflags, &a3};
+            launch_raw((const void*)combine_norms, dim3(1), dim3(32), 0, args);
+        }
     }
 
     // The op list of one unfused sweep for sweep_persistent, its parameters copied to the
@@ -966,6 +1010,7 @@ struct Solver : SolverBase {
             op.variant = mode * 4 + (vblk ? 2 : 0) + (pp.p.hres_elems > 0 ? 1 : 0);
             op.idx = (int)pv.size();
             pv.push_back(pp.p);
+            pv.back().fin = 0;  // the program has its own OP_FINALIZE
             ops.push_back(op);
             smem = std::max(smem, pp.smem);
             max_pass_grid = std::max<int64_t>(max_pass_grid, pp.grid.x);
@@ -1101,7 +1146,7 @@ struct Solver : SolverBase {
 
     void enqueue_xupdate() {
         launch(refill.fn, refill.grid, dim3(kPassThreads), refill.smem, refill.p);
-        enqueue_finalize(refill.p.ngroups, 0);
+        finish_norm_pass(refill.p, 0);
     }
 
     void enqueue_sweep() {
@@ -1125,7 +1170,7 @@ struct Solver : SolverBase {
         PassParams<T> fp = fused.p;
         fp.full_norms = traced ? 1 : 0;
         launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fp);
-        enqueue_finalize(fused.p.ngroups, 0);
+        finish_norm_pass(fp, 0);
         if (traced) enqueue_trace_push();
         if (!b0.sol.fused_reduce) launch(fused_red_l.fn, fused_red_l.grid, dim3(256), 0, fused_red);
         enqueue_solve(b0, &fused_sol);
@@ -1533,7 +1578,7 @@ struct Solver : SolverBase {
     double objective() override {
         begin();
         launch(obj.fn, obj.grid, dim3(kPassThreads), obj.smem, obj.p);
-        enqueue_finalize(obj.p.ngroups, 1);
+        finish_norm_pass(obj.p, 1);
         CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         end();

@@ -706,10 +706,10 @@ __device__ __forceinline__ void finalize_norms_body(const double* norms, int64_t
     constexpr int VT = 1024;
     for (int vt = threadIdx.x; vt < VT; vt += blockDim.x) {
         double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-        for (int64_t g = vt; g < ngroups; g += VT) {
-            a0 += norms[3 * g + 0];
-            a1 += norms[3 * g + 1];
-            a2 += norms[3 * g + 2];
+        for (int64_t g = vt; g < ngroups; g += VT) {  // L2 loads: written by other CTAs just now
+            a0 += __ldcg(norms + 3 * g + 0);
+            a1 += __ldcg(norms + 3 * g + 1);
+            a2 += __ldcg(norms + 3 * g + 2);
         }
         if (!obj_only)
             for (int64_t d = vt; d < ndelta; d += VT) {

@@ -273,6 +273,26 @@ def test_fused_three_sweeps_vs_oracle(name):
     assert rel(s.reconstruct().cpu().numpy(), X) <= tol
 
 
+@pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "C2"])
+def test_in_pass_finaliser_bit_identical(name):
+    """IFCTN_FLAG_PASS_FINALIZE: the norm passes run the sweep finaliser in their last CTA
+    (same fixed summation order as the finalize_norms launch): traces, objective and state
+    are bit-identical."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_PASS_FINALIZE
+    p = make_config(name)
+    a = make_solver(p, flags=IFCTN_FLAG_PASS_FINALIZE)
+    b = make_solver(p)
+    ra = a.sweep(3, trace=True)[1] + a.sweep(1, trace=True)[1]
+    rb = b.sweep(3, trace=True)[1] + b.sweep(1, trace=True)[1]
+    assert ra == rb
+    a.sweep(2)
+    b.sweep(2)
+    assert a.objective() == b.objective()
+    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
+    na, nb = a.x_update(), b.x_update()
+    assert list(na) == list(nb)
+
+
 @pytest.mark.parametrize("name", ["C2s", "C4s", "C2rs"])
 def test_pdl_launches_bit_identical(name):
     """IFCTN_FLAG_PDL (programmatic dependent launch: kernels start early and wait in
