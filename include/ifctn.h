@@ -222,6 +222,30 @@ int64_t ifctn_launch_count(const ifctn_ctx* ctx);
  * Errors: E_ARG for NULL pointers or ‖T‖ = 0.                                              */
 ifctn_status ifctn_metrics(ifctn_ctx* ctx, const void* truth, double* out);
 
+/* ---- Sampling-set generators on the device -------------
+ * The paper's two missingness protocols, random missing (RM) and fibre missing (FM), as
+ * exact-count draws without replacement (reading R12): the selected set is the k
+ * indices u with the smallest keys key(u) = fmix64(seed + (u+1)·0x9E3779B97F4A7C15), i.e. the
+ * u-th output of the splitmix64 generator started at state `seed` (fmix64: z ^= z>>30,
+ * z *= 0xBF58476D1CE4E5B9, z ^= z>>27, z *= 0x94D049BB133111EB, z ^= z>>31; all mod 2^64).
+ * The keys are distinct (a bijection of u), so the set is unique; the result is
+ * deterministic and bit-identical on every GPU.  Found by an on-device 8-bit radix select
+ * (no host synchronisation); all work is enqueued on `stream` (cudaStream_t, NULL = legacy
+ * default).  A 2 KB scratch is taken with cudaMallocAsync on that stream and freed on it.
+ *
+ * ifctn_mask_uniform: mask[u] = 1 for the `observed` selected indices of u ∈ [0, n), else 0.
+ *   mask    DEVICE, n bytes, caller-owned (written in full)
+ * ifctn_mask_fibres: whole mode-`mode` fibres (0-based) missing.  Fibre index of entry
+ *   u = i_0 + I_0(i_1 + …) is its linear index with mode `mode` removed (remaining modes
+ *   ascending, lowest fastest); the `missing_fibres` selected fibres (keys over the fibre
+ *   index space [0, n/I_mode)) are 0 along their whole length, every other entry is 1.
+ *   mask    DEVICE, Π dims bytes, mode-1-fastest, caller-owned (written in full)
+ * Errors: E_ARG for a NULL/host mask, negative counts or a count above the population;
+ * E_SHAPE for a dim < 1; E_CUDA for a launch or allocation failure.                       */
+ifctn_status ifctn_mask_uniform(uint8_t* mask, int64_t n, int64_t observed, uint64_t seed, void* stream);
+ifctn_status ifctn_mask_fibres(uint8_t* mask, int order, const int64_t* dims, int mode,
+                               int64_t missing_fibres, uint64_t seed, void* stream);
+
 /* ---- Multi-instance driver: the paper's rank-grid protocol -------------
  * The paper reports its runtimes "including the time required to tune all parameters"
  * over rank grids such as R_{1,2} ∈ {3,6,9,15,30,36}, R_{1,3} = R_{2,3} ∈ {3,6,9}

@@ -21,7 +21,7 @@ from ._abi import (IFCTN_F32, IFCTN_F64, IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_GRAPH
                    IFCTN_FLAG_NONE, IFCTN_FLAG_X_FULL, IFCTN_MODEL, IFCTN_X, IfctnError,
                    ifctn_dist, ifctn_trace_row)
 
-__all__ = ["Solver", "IfctnError", "IFCTN_F32", "IFCTN_F64", "IFCTN_MODEL", "IFCTN_X",
+__all__ = ["Solver", "IfctnError", "IFCTN_F32", "IFCTN_F64", "IFCTN_MODEL", "IFCTN_X", "mask_uniform", "mask_fibres",
            "factor_layout", "num_params"]
 
 
@@ -189,3 +189,22 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+def mask_uniform(n, observed, seed=0, device=None):
+    """RM sampling set on the device (ifctn_mask_uniform): uint8[n], exactly `observed` ones."""
+    import torch
+    m = torch.empty(int(n), dtype=torch.uint8, device=device or "cuda")
+    stream = torch.cuda.current_stream(m.device).cuda_stream
+    _abi.ifctn_mask_uniform(m.data_ptr() if n else None, n, observed, seed, stream)
+    return m
+
+
+def mask_fibres(dims, mode, missing, seed=0, device=None):
+    """FM sampling set on the device (ifctn_mask_fibres): uint8[Π dims], mode-1-fastest, with
+    exactly `missing` whole mode-`mode` fibres unobserved."""
+    import torch
+    m = torch.empty(int(np.prod(dims)), dtype=torch.uint8, device=device or "cuda")
+    stream = torch.cuda.current_stream(m.device).cuda_stream
+    _abi.ifctn_mask_fibres(m.data_ptr(), dims, mode, missing, seed, stream)
+    return m

@@ -86,6 +86,8 @@ SIGNATURES = {
     "ifctn_status_string": (ctypes.c_char_p, [_I]),
     "ifctn_last_error": (ctypes.c_char_p, [_VP]),
     "ifctn_launch_count": (ctypes.c_int64, [_VP]),
+    "ifctn_mask_uniform": (_I, [_VP, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, _VP]),
+    "ifctn_mask_fibres": (_I, [_VP, _I, _I64P, _I, ctypes.c_int64, ctypes.c_uint64, _VP]),
     "ifctn_grid_run": (_I, [_I, _I64P, _I, _VP, _VP, _VP, ctypes.POINTER(ifctn_instance), _I, _I, _I,
                             ctypes.POINTER(ifctn_instance_result)]),
 }
@@ -244,3 +246,12 @@ def ifctn_grid_run(order, dims, dtype, observed_ptr, mask_ptr, truth_ptr, instan
         msg = lib().ifctn_last_error(None)
         raise IfctnError(st, (msg.decode() if msg else "") + f" (per-instance: {[o['status'] for o in out]})")
     return out
+
+
+def ifctn_mask_uniform(mask_ptr, n, observed, seed, stream=None):
+    check(lib().ifctn_mask_uniform(mask_ptr, int(n), int(observed), int(seed), stream))
+
+
+def ifctn_mask_fibres(mask_ptr, dims, mode, missing_fibres, seed, stream=None):
+    check(lib().ifctn_mask_fibres(mask_ptr, len(dims), _i64arr(dims), int(mode), int(missing_fibres),
+                                  int(seed), stream))
