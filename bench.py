@@ -335,6 +335,7 @@ def run_ours(args):
     if not args.no_extras and world == 1:
         line["other_configs"] = other_configs(torch)
         line["rank_grid"] = rank_grid_extra(torch)
+        line["mask_gen"] = mask_gen_extra(torch)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if tdist is not None:
@@ -434,6 +435,29 @@ def rank_grid_extra(torch):
         out[f"concurrency_{conc}"] = {"seconds": el, "instances_per_s": len(inst) / el,
                                       "sweeps_per_s": len(inst) * p.sweeps / el,
                                       "best_rse": res[best]["rse"], "best_ranks": list(MSI_GRID[best])}
+    return out
+
+
+def mask_gen_extra(torch):
+    """the on-device RM/FM sampling-set draws (ifctn_mask_uniform / _fibres) at
+    C5's RM size and C4's FM size; CUDA events on the current stream, median of 5."""
+    from paper_2511_16358_b200 import mask_fibres, mask_uniform
+    cases = {"C5_RM": (lambda: mask_uniform(64 ** 4 * 32, 26843546, 0), 64 ** 4 * 32),
+             "C4_FM": (lambda: mask_fibres((214, 61, 144, 4), 2, 36551, 0), 214 * 61 * 144 * 4)}
+    out = {}
+    for name, (fn, n) in cases.items():
+        fn()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            m = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+            del m
+        ms = sorted(ts)[2]
+        out[name] = {"n": n, "ms": ms, "entries_per_s": n / (ms * 1e-3)}
     return out
 
 
