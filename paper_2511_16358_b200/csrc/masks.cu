@@ -6,11 +6,13 @@
 // without replacement, as the k smallest of n i.i.d. keys.  Here the keys are the
 // counter-based splitmix64 stream, key(u) = fmix64(seed + (u+1)·γ): a bijection of u, so all
 // keys are distinct and "the k smallest" is unique (no tie rule needed).  The k-th smallest
-// key is found by an 8-digit (8-bit) MSD radix select, entirely stream-ordered: per digit one
-// histogram pass over the candidates that share the resolved prefix, then one 256-thread
-// scan kernel that fixes the digit and the remaining rank in device memory (no host sync).
+// key is found by an MSD radix select, entirely stream-ordered (no host sync): two 12-bit
+// digits, each one histogram pass over the keys sharing the resolved prefix plus one scan
+// kernel that fixes the digit and the remaining rank in device memory; then the ≈ n/2^24
+// keys left are collected and ranked in one CTA (8-bit full passes only on overflow).
 // A final pass writes mask[u] = key(u) ≤ T (RM: observed; FM: the fibre of u is missing).
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -31,59 +33,124 @@ __device__ __forceinline__ unsigned long long key_of(unsigned long long seed, un
 }
 
 // device-resident select state
+constexpr int kBins = 4096;   // widest digit (12 bits)
+constexpr int kCand = 4096;   // candidate buffer after the two 12-bit digits
+
 struct SelectState {
-    unsigned long long prefix;   // resolved high digits of the threshold key
+    unsigned long long prefix;   // resolved high digits of the threshold key (the full key at the end)
     unsigned long long rank;     // 1-based rank of the threshold among keys with that prefix
-    unsigned long long hist[256];
+    unsigned long long count;    // candidates matching the 24-bit prefix
+    int overflow;                // 1: more than kCand candidates -> finish with 8-bit full passes
+    int pad;
+    unsigned long long hist[kBins];
+    unsigned long long cand[kCand];
 };
 
-// Histogram of digit `d` (0 = most significant byte) over the keys whose higher digits equal
-// the resolved prefix.  Shared-memory bins, one global atomic per bin per CTA.
+// Histogram of the `width`-bit digit at `shift` over the keys whose bits above the digit equal
+// the resolved prefix.  Shared-memory bins, one global atomic per non-empty bin per CTA.
+// `fallback`: run only when the candidate buffer overflowed (else return at once).
 __global__ void __launch_bounds__(256) select_hist(SelectState* st, unsigned long long seed,
-                                                   long long n, int d) {
-    __shared__ unsigned int h[256];
-    h[threadIdx.x] = 0;
+                                                   long long n, int shift, int width, int fallback) {
+    if (fallback && !st->overflow) return;
+    __shared__ unsigned int h[kBins];
+    const int bins = 1 << width;
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    const int shift = 56 - 8 * d;
     const unsigned long long pre = st->prefix;
-    const unsigned long long hi_mask = d == 0 ? 0ull : (~0ull << (64 - 8 * d));
+    const unsigned long long hi_mask = shift + width >= 64 ? 0ull : (~0ull << (shift + width));
+    const unsigned int dmask = bins - 1;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
         const unsigned long long k = key_of(seed, (unsigned long long)u);
-        if ((k & hi_mask) == pre) atomicAdd(&h[(k >> shift) & 0xFF], 1u);
+        if ((k & hi_mask) == pre) atomicAdd(&h[(unsigned)(k >> shift) & dmask], 1u);
     }
     __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&st->hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+    for (int b = threadIdx.x; b < bins; b += blockDim.x)
+        if (h[b]) atomicAdd(&st->hist[b], (unsigned long long)h[b]);
 }
 
-// Fix digit d: the bin holding the rank-th smallest candidate; clear the histogram.
-__global__ void __launch_bounds__(256) select_digit(SelectState* st, int d) {
-    __shared__ unsigned long long c[256];
+// Fix the digit at `shift`: the bin holding the rank-th smallest candidate; clear the
+// histogram.  1024 threads, each owning bins/1024 consecutive bins (≥ 1 when width ≥ 10,
+// else threads past `bins` own none).
+__global__ void __launch_bounds__(1024) select_digit(SelectState* st, int shift, int width, int fallback) {
+    if (fallback && !st->overflow) return;
+    __shared__ unsigned long long c[1024];
     const int t = threadIdx.x;
-    c[t] = st->hist[t];
+    const int bins = 1 << width;
+    const int per = bins >= 1024 ? bins / 1024 : 1;
+    const int b0 = t * per;
+    unsigned long long own = 0;
+    for (int q = 0; q < per && b0 + q < bins; ++q) own += st->hist[b0 + q];
+    c[t] = own;
     __syncthreads();
-    // inclusive scan (Hillis–Steele; 256 entries)
-    for (int off = 1; off < 256; off <<= 1) {
+    for (int off = 1; off < 1024; off <<= 1) {   // inclusive scan (Hillis–Steele)
         const unsigned long long v = t >= off ? c[t - off] : 0ull;
         __syncthreads();
         c[t] += v;
         __syncthreads();
     }
     const unsigned long long r = st->rank;
-    const unsigned long long below = t ? c[t - 1] : 0ull;
+    unsigned long long below = t ? c[t - 1] : 0ull;
     __syncthreads();
     if (below < r && r <= c[t]) {
-        st->prefix |= (unsigned long long)t << (56 - 8 * d);
-        st->rank = r - below;
+        for (int q = 0; q < per; ++q) {
+            const unsigned long long h = st->hist[b0 + q];
+            if (r <= below + h) {
+                st->prefix |= (unsigned long long)(b0 + q) << shift;
+                st->rank = r - below;
+                break;
+            }
+            below += h;
+        }
     }
-    st->hist[t] = 0ull;
+    __syncthreads();
+    for (int q = 0; q < per && b0 + q < bins; ++q) st->hist[b0 + q] = 0ull;
 }
 
-__global__ void __launch_bounds__(256) init_state(SelectState* st, unsigned long long k) {
-    st->hist[threadIdx.x] = 0ull;
+// Append every key matching the resolved prefix (bits ≥ `shift`) to the candidate buffer.
+__global__ void __launch_bounds__(256) select_collect(SelectState* st, unsigned long long seed, long long n,
+                                                     int shift, unsigned long long cap) {
+    const unsigned long long pre = st->prefix;
+    const unsigned long long hi_mask = ~0ull << shift;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += stride) {
+        const unsigned long long k = key_of(seed, (unsigned long long)u);
+        if ((k & hi_mask) == pre) {
+            const unsigned long long slot = atomicAdd(&st->count, 1ull);
+            if (slot < cap) st->cand[slot] = k;
+        }
+    }
+}
+
+// The rank-th smallest candidate (keys are distinct): for each candidate, count the smaller
+// ones.  Sets prefix = T, or flags overflow for the 8-bit fallback passes.
+__global__ void __launch_bounds__(1024) select_resolve(SelectState* st, unsigned long long cap) {
+    const unsigned long long cnt = st->count;
+    if (cnt > cap) {
+        if (threadIdx.x == 0) st->overflow = 1;
+        return;
+    }
+    __shared__ unsigned long long c[kCand];
+    for (unsigned long long x = threadIdx.x; x < cnt; x += blockDim.x) c[x] = st->cand[x];
+    __syncthreads();
+    const unsigned long long r = st->rank;
+    for (unsigned long long x = threadIdx.x; x < cnt; x += blockDim.x) {
+        unsigned long long less = 0;
+        for (unsigned long long y = 0; y < cnt; ++y) less += c[y] < c[x];
+        if (less + 1 == r) {
+            st->prefix = c[x];
+            st->rank = 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) init_state(SelectState* st, unsigned long long k) {
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) st->hist[b] = 0ull;
     if (threadIdx.x == 0) {
         st->prefix = 0ull;
         st->rank = k;
+        st->count = 0ull;
+        st->overflow = 0;
     }
 }
 
@@ -125,16 +192,24 @@ __global__ void __launch_bounds__(256) write_fibres(uint8_t* __restrict__ mask, 
                                                     long long inner, long long Im, int none, int every) {
     const unsigned long long T = st->prefix;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    const long long span = inner * Im;
     for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g * 16 < n; g += stride) {
         const long long u0 = g * 16;
+        // (lo, mid, hi) of u0 once, then stepped: u = lo + inner·(mid + Im·hi)
+        long long lo = u0 % inner, q = u0 / inner;
+        long long mid = q % Im, hi = q / Im;
         uint8_t b[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const long long u = u0 + j;
-            const long long f = u % inner + inner * (u / span);
+            const long long f = lo + inner * hi;
             const bool miss = every || (!none && key_of(seed, (unsigned long long)f) <= T);
             b[j] = miss ? 0 : 1;
+            if (++lo == inner) {
+                lo = 0;
+                if (++mid == Im) {
+                    mid = 0;
+                    ++hi;
+                }
+            }
         }
         store16(mask, u0, n, b);
     }
@@ -148,13 +223,27 @@ int grid_for(long long work) {
     return (int)(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
-// Radix-select the k-th smallest of key(0..n-1) into st->prefix (1 ≤ k ≤ n).
+// Select the k-th smallest of key(0..n-1) into st->prefix (1 ≤ k ≤ n): two 12-bit digits
+// over all keys, then the ~n/2^24 keys left are collected and ranked in one CTA; only if more
+// than kCand remain (never expected below n ≈ 2^34) do five 8-bit full passes finish the job.
 cudaError_t select_kth(SelectState* st, unsigned long long seed, long long n, long long k, cudaStream_t s) {
-    init_state<<<1, 256, 0, s>>>(st, (unsigned long long)k);
+    init_state<<<1, 1024, 0, s>>>(st, (unsigned long long)k);
     const int g = grid_for(n);
-    for (int d = 0; d < 8; ++d) {
-        select_hist<<<g, 256, 0, s>>>(st, seed, n, d);
-        select_digit<<<1, 256, 0, s>>>(st, d);
+    for (int shift : {52, 40}) {
+        select_hist<<<g, 256, 0, s>>>(st, seed, n, shift, 12, 0);
+        select_digit<<<1, 1024, 0, s>>>(st, shift, 12, 0);
+    }
+    // IFCTN_MASK_CAND_CAP (tests only) lowers the buffer to exercise the fallback passes
+    static const long long cap_env = [] {
+        const char* e = getenv("IFCTN_MASK_CAND_CAP");
+        return e ? atoll(e) : (long long)kCand;
+    }();
+    const unsigned long long cap = (unsigned long long)(cap_env < 0 ? 0 : (cap_env > kCand ? kCand : cap_env));
+    select_collect<<<g, 256, 0, s>>>(st, seed, n, 40, cap);
+    select_resolve<<<1, 1024, 0, s>>>(st, cap);
+    for (int shift = 32; shift >= 0; shift -= 8) {
+        select_hist<<<g, 256, 0, s>>>(st, seed, n, shift, 8, 1);
+        select_digit<<<1, 1024, 0, s>>>(st, shift, 8, 1);
     }
     return cudaGetLastError();
 }
@@ -183,7 +272,7 @@ extern "C" ifctn_status ifctn_mask_uniform(uint8_t* mask, int64_t n, int64_t obs
     if (observed > 0 && !all) {
         if (select_kth(st, seed, n, observed, stream) != cudaSuccess) return IFCTN_E_CUDA;
     } else {
-        init_state<<<1, 256, 0, stream>>>(st, 0ull);  // T unused: all observed, or memset below
+        init_state<<<1, 1024, 0, stream>>>(st, 0ull);  // T unused: all observed, or memset below
     }
     if (observed == 0) {
         if (cudaMemsetAsync(mask, 0, (size_t)n, stream) != cudaSuccess) return IFCTN_E_CUDA;
@@ -215,7 +304,7 @@ extern "C" ifctn_status ifctn_mask_fibres(uint8_t* mask, int order, const int64_
     if (!none && !every) {
         if (select_kth(st, seed, nf, missing_fibres, stream) != cudaSuccess) return IFCTN_E_CUDA;
     } else {
-        init_state<<<1, 256, 0, stream>>>(st, 0ull);  // T unused (none / every flag)
+        init_state<<<1, 1024, 0, stream>>>(st, 0ull);  // T unused (none / every flag)
     }
     write_fibres<<<grid_for((n + 15) / 16), 256, 0, stream>>>(mask, st, seed, n, inner, Im, none, every);
     if (cudaFreeAsync(st, stream) != cudaSuccess) return IFCTN_E_CUDA;

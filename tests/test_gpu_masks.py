@@ -81,3 +81,56 @@ def test_errors():
         _abi.ifctn_mask_fibres(buf.data_ptr(), (4, 4), 2, 1, 0)
     with pytest.raises(IfctnError):
         _abi.ifctn_mask_fibres(buf.data_ptr(), (4, 4), 0, 5, 0)
+
+
+@pytest.mark.parametrize("kind", ["RM", "FM"])
+def test_device_mask_drives_a_sweep(kind):
+    """A device-drawn sampling set fed straight into ifctn_create: one sweep within the
+    north-star 1e-4 of the oracle run on the oracle's own draw of the same set."""
+    from oracle import oracle as O
+    from paper_2511_16358_b200 import Solver, mask_fibres, mask_uniform
+    from synth import make_problem
+
+    from gpu_util import dev, rel
+    p = make_problem("C4s-like", (14, 9, 12, 4), 3, np.float32, "normal", scale_noise=0.01, sr=0.1, sweeps=1)
+    if kind == "RM":
+        m_dev = mask_uniform(p.n, p.n // 10, 21)
+        m = MK.mask_uniform(p.n, p.n // 10, 21)
+    else:
+        m_dev = mask_fibres(p.dims, 2, 300, 21)
+        m = MK.mask_fibres(p.dims, 2, 300, 21)
+    observed = np.where(m.astype(bool), p.truth, 0).astype(p.dtype)
+    s = Solver(p.dims, p.ranks, dev(observed), m_dev, dev(p.G0), rho=p.rho)
+    s.sweep(1)
+    Xg = s.reconstruct().cpu().numpy()
+    Gg = s.factors().cpu().numpy()
+    s.close()
+    sh = O.Shape(p.dims, p.ranks)
+    G = p.G0.astype(np.float64)
+    X = O.init_x(observed, m)
+    st, _, _ = O.sweep(sh, G, X, m, p.rho, O.objective(sh, G, X), False)
+    assert st == 0
+    assert rel(Gg, G) <= 1e-4 and rel(Xg, X) <= 1e-4
+    obs = m.astype(bool)
+    assert np.array_equal(Xg[obs].view(np.uint8), observed[obs].view(np.uint8))
+
+
+def test_select_fallback_passes():
+    """The 8-bit fallback passes (taken when more keys than the candidate buffer share the
+    24-bit prefix; forced here with IFCTN_MASK_CAND_CAP=0 in a child process) give the same
+    draw."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "from paper_2511_16358_b200 import mask_uniform, mask_fibres\n"
+            "from oracle import masks as MK\n"
+            "for n, k in [(1, 1), (17, 5), (100003, 31337)]:\n"
+            "    assert np.array_equal(mask_uniform(n, k, 9).cpu().numpy(), MK.mask_uniform(n, k, 9))\n"
+            "d = (7, 9, 11, 13)\n"
+            "assert np.array_equal(mask_fibres(d, 1, 500, 4).cpu().numpy(), MK.mask_fibres(d, 1, 500, 4))\n"
+            "print('ok')\n") % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IFCTN_MASK_CAND_CAP="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
