@@ -159,6 +159,39 @@ def oracle_cpu_baseline(p, target_s=12.0, max_sweeps=3):
                       f"scaled by n_slab/n = {frac:.5f}"}
 
 
+def oracle_single_thread():
+    """the float64 oracle on ONE host thread for C1 (its 10 configured sweeps) and
+    C2 (one sweep), plus the host CPU model; a baseline, not a target."""
+    from oracle import oracle as O
+    from synth import make_config
+    cpu = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    prev = O.get_threads()
+    O.set_threads(1)
+    out = {"threads": 1, "cpu_model": cpu, "logical_cpus": os.cpu_count()}
+    try:
+        for name, sweeps in (("C1", 10), ("C2", 1)):
+            p = make_config(name)
+            sh = O.Shape(p.dims, p.ranks)
+            G = p.G0.astype(np.float64)
+            X = O.init_x(p.observed, p.mask)
+            F = O.objective(sh, G, X)
+            t0 = time.perf_counter()
+            for _ in range(sweeps):
+                st, F, _ = O.sweep(sh, G, X, p.mask, p.rho, F, False)
+            el = time.perf_counter() - t0
+            out[name] = {"sweeps": sweeps, "seconds": el, "sweeps_per_s": sweeps / el}
+    finally:
+        O.set_threads(prev)
+    return out
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -332,6 +365,8 @@ def run_ours(args):
         line["e2e"] = e2e(torch, p, args.steps, obs, msk, g0, mk_dist, barrier, tdist)
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = oracle_cpu_baseline(p)
+        if not args.no_extras:
+            line["cpu_baseline"]["single_thread"] = oracle_single_thread()
     if not args.no_extras and world == 1:
         line["other_configs"] = other_configs(torch)
         line["rank_grid"] = rank_grid_extra(torch)
