@@ -194,10 +194,24 @@ __device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t 
     const int64_t base = slot_base(Q, v, nslots) + e;
     const int64_t stride = Q.VB * Q.Lv;
     IFCTN_CHECK(nslots < 1 || base + (nslots - 1) * stride < Q.part_cap, "solve gather slots");
+    // all loads of a group of 8 slots in flight before the (in-order) sums: one L2 round
+    // trip per 8 slots instead of one per slot (predicated tail); same summation order
     double sb = 0.0, sw = 0.0;
-    for (int64_t s = 0; s < nslots; ++s) {
-        sb += (double)Q.part_b[base + s * stride];
-        sw += (double)Q.part_w[base + s * stride];
+    for (int64_t s = 0; s < nslots; s += 8) {
+        const int64_t rem = nslots - s;
+        T vb[8], vw[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            vb[q] = q < rem ? Q.part_b[base + (s + q) * stride] : T(0);
+            vw[q] = q < rem ? Q.part_w[base + (s + q) * stride] : T(0);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q < rem) {
+                sb += (double)vb[q];
+                sw += (double)vw[q];
+            }
+        }
     }
     b = sb;
     w = sw;
