@@ -26,6 +26,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the float64 oracle (cpu_baseline / --impl reference) runs one OpenMP thread per physical
+# core, packed; read by the OpenMP runtime when the oracle library first runs
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
 
 METRIC = "iFCTN-TC PAM sweeps/s"
 UNIT = "sweeps/s"
@@ -118,45 +122,77 @@ def dist_env():
     return world, rank, local
 
 
-def oracle_cpu_baseline(p, target_s=12.0, max_sweeps=3):
-    """The float64 oracle (as it stands) on a slab of the same workload: the first S slices of
-    the last mode, one or more full sweeps; value scaled by n_slab / n to sweeps/s of the
-    whole tensor (per-entry sweep cost is independent of the slab size)."""
-    from oracle import oracle as O
-    threads = os.cpu_count() or 1
-    O.set_threads(threads)
-    dims = list(p.dims)
-    N = len(dims)
-    S = 1
-    slab = dims[:-1] + [S]
-    n_slab = int(np.prod(slab))
-    # factors: chains of the last mode keep only their first S columns
-    from paper_2511_16358_b200 import factor_layout
-    G = []
-    for (k, i, off, R, Ik) in factor_layout(dims, p.ranks):
-        blk = p.G0[off:off + R * Ik].reshape(Ik, R)
-        if k == N - 1:
-            blk = blk[:S]
-        G.append(blk.reshape(-1))
-    G = np.concatenate(G).astype(np.float64)
-    sh = O.Shape(slab, p.ranks)
-    obs = p.observed[:n_slab]
-    mask = p.mask[:n_slab]
-    X = O.init_x(obs, mask)
-    F = O.objective(sh, G, X)
-    t0 = time.perf_counter()
-    done = 0
-    while True:
-        st, F, row = O.sweep(sh, G, X, mask, p.rho, F, False)
-        done += 1
+def host_cpu():
+    """(physical cores, CPU model) of this host: unique (package, core) pairs of /proc/cpuinfo
+    (psutil's count as a cross-check), the model name line."""
+    model, pairs, phys, core = "", set(), None, None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            k, _, v = ln.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "model name" and not model:
+                model = v
+            elif k == "physical id":
+                phys = v
+            elif k == "core id":
+                core = v
+            elif not k and phys is not None and core is not None:
+                pairs.add((phys, core))
+                phys = core = None
+        if phys is not None and core is not None:
+            pairs.add((phys, core))
+    except OSError:
+        pass
+    n = len(pairs)
+    if n == 0:
+        try:
+            import psutil
+            n = psutil.cpu_count(logical=False) or 0
+        except Exception:
+            n = 0
+    return max(1, n or (os.cpu_count() or 1)), model
+
+
+class OracleRun:
+    """The float64 oracle (as it stands) on the FULL workload: X⁽⁰⁾ = P_Ω(O), G⁰, then one
+    full Algorithm 1 sweep per call (the run continues from sweep to sweep), timed with the
+    host clock; one OpenMP thread per physical core, OMP_PROC_BIND=close."""
+
+    def __init__(self, p):
+        from oracle import oracle as O
+        self.O = O
+        self.cores, self.model = host_cpu()
+        O.set_threads(self.cores)
+        self.p = p
+        self.sh = O.Shape(p.dims, p.ranks)
+        self.G = p.G0.astype(np.float64)
+        self.X = O.init_x(p.observed, p.mask)
+        self.F = O.objective(self.sh, self.G, self.X)
+        self.done = 0
+
+    def sweep(self):
+        t0 = time.perf_counter()
+        st, self.F, _ = self.O.sweep(self.sh, self.G, self.X, self.p.mask, self.p.rho, self.F, False)
         el = time.perf_counter() - t0
-        if el >= target_s or done >= max_sweeps:
-            break
-    frac = n_slab / p.n
-    return {"value": done * frac / el, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"{done} full float64 oracle sweep(s) over a {'x'.join(map(str, slab))} slab "
-                      f"(first {S} of {dims[-1]} last-mode slices, {n_slab} entries) in {el:.1f} s, "
-                      f"scaled by n_slab/n = {frac:.5f}"}
+        if st:
+            raise RuntimeError(f"oracle sweep status {st}")
+        self.done += 1
+        return el
+
+    def sample(self, k, seconds):
+        p = self.p
+        return (f"{k} full float64 oracle sweep(s) of {p.name} ({'x'.join(map(str, p.dims))}, {p.n} entries, "
+                f"all {p.N * (p.N - 1)} blocks + refill, measured, not extrapolated) in {seconds:.1f} s; "
+                f"{self.cores} OpenMP threads = physical cores, OMP_PROC_BIND={os.environ.get('OMP_PROC_BIND')}; "
+                f"CPU: {self.model}")
+
+
+def oracle_cpu_baseline(p, sweeps=1):
+    """cpu_baseline of the bench line: `sweeps` full oracle sweeps of the bench workload."""
+    run = OracleRun(p)
+    el = sum(run.sweep() for _ in range(sweeps))
+    return {"value": sweeps / el, "unit": UNIT, "cores": run.cores, "kind": "oracle",
+            "sample": run.sample(sweeps, el), "cpu_model": run.model}
 
 
 def oracle_single_thread():
@@ -174,7 +210,7 @@ def oracle_single_thread():
         pass
     prev = O.get_threads()
     O.set_threads(1)
-    out = {"threads": 1, "cpu_model": cpu, "logical_cpus": os.cpu_count()}
+    out = {"threads": 1, "cpu_model": cpu, "logical_cpus": os.cpu_count(), "physical_cores": host_cpu()[0]}
     try:
         for name, sweeps in (("C1", 10), ("C2", 1)):
             p = make_config(name)
@@ -193,26 +229,30 @@ def oracle_single_thread():
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the float64 oracle, as it stands, on
+    the host cores — W untimed then K timed FULL sweeps of the bench workload (one step =
+    one sweep, the run continuing from step to step).  Rank 0 only under torchrun."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     from synth import make_config
     p = make_config(args.config)
-    times = []
-    res = None
-    for s in range(args.warmup + args.steps):
-        r = oracle_cpu_baseline(p, target_s=0.0, max_sweeps=1)
-        if s >= args.warmup:
-            times.append(1.0 / r["value"])
-        res = r
-    v = 1.0 / statistics.mean(times)
+    run = OracleRun(p)
+    for _ in range(args.warmup):
+        run.sweep()
+    times = [run.sweep() for _ in range(args.steps)]
+    el = sum(times)
+    v = args.steps / el
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * el / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(p, world),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": res["cores"], "kind": "oracle",
-                             "sample": "per step: " + res["sample"]},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": run.cores, "kind": "oracle",
+                             "sample": "per step: " + run.sample(1, el / args.steps) +
+                                       f"; {args.steps} timed steps after {args.warmup} warm-up sweeps",
+                             "cpu_model": run.model},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "step_seconds": {"min": min(times), "median": statistics.median(times), "max": max(times)}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -442,23 +482,32 @@ def other_configs(torch):
 
 
 def rank_grid_extra(torch):
-    """the paper's MSI rank grid (P:L485, 18 instances) on the C2 recipe, 100
-    sweeps each, through ifctn_grid_run at concurrency 1 and 8 (wall time of the whole grid,
-    inputs resident, contexts created inside the timed region)."""
+    """the paper's two rank-tuning grids through ifctn_grid_run at concurrency
+    1 and 8 (wall time of the whole grid, inputs resident, contexts created inside the timed
+    region): the MSI grid (P:L485, 18 instances) on the C2 recipe and the traffic grid
+    (P:L562, 28 instances) on the Guangzhou-shaped C4 recipe (C4g, 214×61×144)."""
+    from synth import MSI_GRID, TRAFFIC_GRID
+    return {"msi": _grid_bench(torch, "C2", MSI_GRID,
+                               "C2 recipe x MSI rank grid (P:L485): R12 in {3,6,9,15,30,36} x R13=R23 in {3,6,9}"),
+            "traffic": _grid_bench(torch, "C4g", TRAFFIC_GRID,
+                                   "C4g (214x61x144, C4 recipe) x traffic rank grid (P:L562): "
+                                   "R12 in {2,3,4,6,9,12,36} x R13=R23 in {3,6,9,12}")}
+
+
+def _grid_bench(torch, cfg, pairs, label):
     import time as _t
 
     from paper_2511_16358_b200.grid import rank_grid
-    from synth import MSI_GRID, grid_rank_matrix, init_factors, make_config
-    p = make_config("C2")
+    from synth import grid_rank_matrix, init_factors, make_config
+    p = make_config(cfg)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     inst = []
-    for (r12, r3) in MSI_GRID:
+    for (r12, r3) in pairs:
         R = grid_rank_matrix(r12, r3)
         g, _ = init_factors(p.dims, R, p.observed, p.mask, p.dtype, "uniform", 0)
         inst.append(dict(ranks=R, rho=p.rho, init=dev(g)))
     obs, mask, truth = dev(p.observed), dev(p.mask), dev(p.truth)
-    out = {"workload": "C2 recipe x MSI rank grid (P:L485): R12 in {3,6,9,15,30,36} x R13=R23 in {3,6,9}",
-           "instances": len(inst), "sweeps_per_instance": p.sweeps}
+    out = {"workload": label, "instances": len(inst), "sweeps_per_instance": p.sweeps}
     rank_grid(p.dims, obs, mask, inst[:2], 2, truth=truth, concurrency=2)   # warm-up
     for conc in (1, 8):
         torch.cuda.synchronize()
@@ -469,7 +518,7 @@ def rank_grid_extra(torch):
         best = min(range(len(res)), key=lambda q: res[q]["rse"])
         out[f"concurrency_{conc}"] = {"seconds": el, "instances_per_s": len(inst) / el,
                                       "sweeps_per_s": len(inst) * p.sweeps / el,
-                                      "best_rse": res[best]["rse"], "best_ranks": list(MSI_GRID[best])}
+                                      "best_rse": res[best]["rse"], "best_ranks": list(pairs[best])}
     return out
 
 

@@ -70,16 +70,6 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NO_VBLOCK 8u /* diagnostic: plain fibre walk for every block (no v-blocking) */
 #define IFCTN_FLAG_NO_SOLVE_REDUCE 64u /* diagnostic: separate a2 reduce kernel even when the
                                         * small-rank solve can absorb it                     */
-#define IFCTN_FLAG_PERSISTENT 128u    /* run fixed-count sweeps (eps ≤ 0, no trace) in one
-                                       * persistent cooperative launch (sweep.cuh); default
-                                       * for single-GPU tensors of ≤ 64 Mi entries          */
-#define IFCTN_FLAG_NO_PERSISTENT 256u /* never use the persistent sweep kernel            */
-#define IFCTN_FLAG_PASS_FINALIZE 512u   /* experimental: the norm passes run the sweep
-                                          * finaliser in their last CTA (one launch fewer;
-                                          * measured no faster — off by default)         */
-#define IFCTN_FLAG_PDL 32u      /* experimental: launch sweep kernels with programmatic
-                                  * dependent launch (measured: no gain on C2-C5, a loss on
-                                  * C2r — off by default)                                   */
 #define IFCTN_FLAG_NO_FUSE 16u  /* diagnostic: never fuse a sweep's X update into the next
                                    sweep's first block (see ifctn_sweep)                      */
 
@@ -151,9 +141,7 @@ ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims,
  * With eps ≤ 0 and t_max ≥ 2 the X update of sweep s and the first block of sweep s+1
  * run as one pass over X (they use the same factors); results are the same sweeps up to
  * floating-point summation order.  With a trace on that path the rows are gathered on the
- * device and read back once, after the last sweep (a single synchronisation).
- * IFCTN_FLAG_PERSISTENT: eps ≤ 0 without trace runs all t_max sweeps in one cooperative
- * launch (unfused order, bit-identical to the unfused launch sequence).                  */
+ * device and read back once, after the last sweep (a single synchronisation).          */
 ifctn_status ifctn_sweep(ifctn_ctx* ctx, int t_max, double eps, int* sweeps_done,
                          ifctn_trace_row* trace);
 

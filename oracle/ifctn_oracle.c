@@ -201,15 +201,6 @@ double orc_model_at(int N, const int64_t* dims, const int32_t* ranks, const doub
     return m;
 }
 
-/* Eq. 9 at one entry (sampled checks at full size): observed entries keep x, the others
- * take the prox minimiser (t + ρx)/(1+ρ) with t = iFCTN(G)(idx).                        */
-double orc_refill_at(int N, const int64_t* dims, const int32_t* ranks, const double* G, double x,
-                     int observed, double rho, const int64_t* idx) {
-    if (observed) return x;
-    const double t = orc_model_at(N, dims, ranks, G, idx);
-    return (t + rho * x) / (1.0 + rho);
-}
-
 /* ---- a2: coefficient contraction of block (k,i)  (Prop. 1; Eq. 8)
  *   β(a,j) = Σ_{i: i_i=a, i_k=j} M^{(k,i)}(i) X(i),   ω(a,j) = Σ_{i: i_i=a, i_k=j} M^{(k,i)}(i)²
  * with M^{(k,i)} = Π_{{p,q}≠{k,i}} H_{p,q}(i_p,i_q). Outputs are I_i × I_k column-major.  */

@@ -49,7 +49,6 @@ def lib():
             "orc_pair_gram": (None, [c_int, i64p, i32p, dp, c_int, c_int, dp]),
             "orc_model": (None, [c_int, i64p, i32p, dp, dp]),
             "orc_model_at": (c_d, [c_int, i64p, i32p, dp, i64p]),
-            "orc_refill_at": (c_d, [c_int, i64p, i32p, dp, c_d, c_int, c_d, i64p]),
             "orc_block_contract": (None, [c_int, i64p, i32p, dp, vp, c_int, c_int, c_int, dp, dp]),
             "orc_block_contract_at": (None, [c_int, i64p, i32p, dp, vp, c_int, c_int, c_int,
                                              c_i64, c_i64, dp, dp]),
@@ -142,13 +141,6 @@ def model_at(sh: Shape, G, idx) -> float:
     G = _f64(G)
     idx = _i64(idx)
     return float(lib().orc_model_at(*sh.args, _p(G, ctypes.c_double), _p(idx, ctypes.c_int64)))
-
-
-def refill_at(sh: Shape, G, x: float, observed: bool, rho: float, idx) -> float:
-    G = _f64(G)
-    idx = _i64(idx)
-    return float(lib().orc_refill_at(*sh.args, _p(G, ctypes.c_double), float(x), int(bool(observed)),
-                                     float(rho), _p(idx, ctypes.c_int64)))
 
 
 def _xarg(X):

@@ -15,9 +15,8 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (IFCTN_F32, IFCTN_F64, IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_PDL,  # noqa: F401
-                   IFCTN_FLAG_PASS_FINALIZE, IFCTN_FLAG_NO_PERSISTENT, IFCTN_FLAG_NO_SOLVE_REDUCE,
-                   IFCTN_FLAG_NO_VBLOCK, IFCTN_FLAG_PERSISTENT,
+from ._abi import (IFCTN_F32, IFCTN_F64, IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_GRAPH,  # noqa: F401
+                   IFCTN_FLAG_NO_SOLVE_REDUCE, IFCTN_FLAG_NO_VBLOCK,
                    IFCTN_FLAG_NONE, IFCTN_FLAG_X_FULL, IFCTN_MODEL, IFCTN_X, IfctnError,
                    ifctn_dist, ifctn_trace_row)
 
@@ -58,6 +57,30 @@ def _ptr(x):
     return ctypes.c_void_p(x.ctypes.data)
 
 
+def check_buffer(x, name, kind, count):
+    """Validate a buffer before its raw address crosses the C-ABI (the library cannot see
+    dtype, extent or strides): `kind` is "f32", "f64" or "u8" (mask: uint8 or bool bytes),
+    `count` the element count the call reads or writes.  Raises IfctnError(E_ARG)."""
+    if x is None:
+        raise IfctnError(1, f"{name} must not be None")
+    if hasattr(x, "data_ptr"):  # torch tensor
+        import torch
+        ok = {"f32": (torch.float32,), "f64": (torch.float64,), "u8": (torch.uint8, torch.bool)}[kind]
+        dt, n, contig = x.dtype, x.numel(), x.is_contiguous()
+    elif isinstance(x, np.ndarray):
+        ok = {"f32": (np.dtype(np.float32),), "f64": (np.dtype(np.float64),),
+              "u8": (np.dtype(np.uint8), np.dtype(np.bool_))}[kind]
+        dt, n, contig = x.dtype, x.size, x.flags["C_CONTIGUOUS"]
+    else:
+        raise IfctnError(1, f"{name} must be a torch tensor or a numpy array")
+    if dt not in ok:
+        raise IfctnError(1, f"{name} has dtype {dt}, expected {kind}")
+    if n != count:
+        raise IfctnError(1, f"{name} has {n} elements, expected {count}")
+    if not contig:
+        raise IfctnError(1, f"{name} must be contiguous")
+
+
 class Solver:
     """One iFCTN-TC problem on one GPU (or one rank's shard).
 
@@ -83,20 +106,9 @@ class Solver:
         self._torch_dtype = torch.float64 if dtype == IFCTN_F64 else torch.float32
         flat = [int(v) for v in self.ranks.reshape(-1)]
         self.ws_bytes = _abi.ifctn_workspace_bytes(self.N, self.dims, flat, dtype, dist)
-        self.workspace = None
-        ws_ptr = None
-        if workspace:
-            self.workspace = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device="cuda")
-            base = self.workspace.data_ptr()
-            ws_ptr = ctypes.c_void_p((base + 255) // 256 * 256)
-        if stream is None:
-            stream = torch.cuda.current_stream().cuda_stream
-        self.stream = stream
-        if isinstance(mask, np.ndarray):
-            mask = np.ascontiguousarray(mask, dtype=np.uint8)
-        self.ctx = _abi.ifctn_create(self.N, self.dims, flat, dtype, self.rho, _ptr(observed),
-                                     _ptr(mask), _ptr(init_factors), ws_ptr, self.ws_bytes, dist,
-                                     ctypes.c_void_p(stream), flags)
+        if isinstance(mask, np.ndarray) and mask.dtype == np.bool_:
+            mask = mask.view(np.uint8)
+        # local extents (this rank's shard under dist) — every buffer is checked against them
         if dist is not None and dist.world > 1:
             sm, b, e = _abi.ifctn_shard_range(self.N, self.dims, dist)
             self.shard_mode, self.shard_begin, self.shard_end = sm, b, e
@@ -109,6 +121,27 @@ class Solver:
         self.n_local = int(np.prod(self.local_dims))
         lay = factor_layout(self.local_dims, self.ranks)
         self.n_params_local = lay[-1][2] + lay[-1][3] * lay[-1][4]
+        self._kind = "f64" if dtype == IFCTN_F64 else "f32"
+        check_buffer(observed, "observed", self._kind, self.n_local)
+        check_buffer(mask, "mask", "u8", self.n_local)
+        check_buffer(init_factors, "init_factors", self._kind, self.n_params_local)
+        # Ω must be non-empty (Algorithm 1 needs an observation); the library checks host masks
+        # itself, device masks are checked here (single GPU: a shard may be empty)
+        if hasattr(mask, "data_ptr") and mask.is_cuda and (dist is None or dist.world <= 1):
+            if not bool(mask.any()):
+                raise IfctnError(11, "the mask has no observed entry")
+        self.workspace = None
+        ws_ptr = None
+        if workspace:
+            self.workspace = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device="cuda")
+            base = self.workspace.data_ptr()
+            ws_ptr = ctypes.c_void_p((base + 255) // 256 * 256)
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        self.stream = stream
+        self.ctx = _abi.ifctn_create(self.N, self.dims, flat, dtype, self.rho, _ptr(observed),
+                                     _ptr(mask), _ptr(init_factors), ws_ptr, self.ws_bytes, dist,
+                                     ctypes.c_void_p(stream), flags)
 
     # -- Algorithm 1 -------------------------------------------------------------------
     def sweep(self, t_max, eps=0.0, trace=False):
@@ -133,6 +166,7 @@ class Solver:
         import torch
         if out is None:
             out = torch.empty(self.n_local, dtype=self._torch_dtype, device="cuda")
+        check_buffer(out, "out", self._kind, self.n_local)
         _abi.ifctn_reconstruct(self.ctx, what, _ptr(out))
         return out
 
@@ -140,14 +174,17 @@ class Solver:
         import torch
         if out is None:
             out = torch.empty(self.n_params_local, dtype=self._torch_dtype, device="cuda")
+        check_buffer(out, "out", self._kind, self.n_params_local)
         _abi.ifctn_get_factors(self.ctx, _ptr(out))
         return out
 
     def rse(self, truth) -> float:
+        check_buffer(truth, "truth", self._kind, self.n_local)
         return _abi.ifctn_rse(self.ctx, _ptr(truth))
 
     def metrics(self, truth) -> dict:
         """RSE, RMSE on Ω^c, band-mean PSNR, SSIM (ifctn_metrics)."""
+        check_buffer(truth, "truth", self._kind, self.n_local)
         return _abi.ifctn_metrics(self.ctx, _ptr(truth))
 
     def objective(self) -> float:

@@ -18,10 +18,7 @@ IFCTN_F32, IFCTN_F64 = 0, 1
 IFCTN_MODEL, IFCTN_X = 0, 1
 IFCTN_FLAG_NONE, IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_X_FULL, IFCTN_FLAG_NO_VBLOCK = 0, 1, 2, 8
 IFCTN_FLAG_NO_FUSE = 16
-IFCTN_FLAG_PDL = 32
 IFCTN_FLAG_NO_SOLVE_REDUCE = 64
-IFCTN_FLAG_PERSISTENT, IFCTN_FLAG_NO_PERSISTENT = 128, 256
-IFCTN_FLAG_PASS_FINALIZE = 512
 IFCTN_MAX_ORDER, IFCTN_MAX_RANK = 6, 64
 
 STATUS = ["IFCTN_OK", "IFCTN_E_ARG", "IFCTN_E_SHAPE", "IFCTN_E_RANKS", "IFCTN_E_WORKSPACE",

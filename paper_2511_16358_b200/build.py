@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "ifctn.cu")
-SRCS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("sweep_kernels.cu", "sweep_kernels_f64.cu", "grid.cu", "masks.cu")]
+SRCS = [SRC] + [os.path.join(HERE, "csrc", f) for f in ("grid.cu", "masks.cu")]
 OUT = os.path.join(HERE, "libifctn.so")
 DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + \
        [os.path.join(ROOT, "include", "ifctn.h")]

@@ -115,13 +115,6 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
     } while (0)
 #endif
 
-// ---- programmatic dependent launch (sweep kernels are launched with programmatic stream
-// serialization: the next kernel's CTAs may start while this one runs; each kernel lets its
-// dependents launch at once and waits for its predecessor's completion before touching data
-// the predecessor produced).  No-ops when launched without the attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // ---- TMA bulk copies + mbarriers (sm_90+ PTX; UBLKCP / SYNCS in sm_100a SASS) -------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -267,16 +260,6 @@ struct PassParams {
     unsigned* sched;               // tiled pass: [next chunk, retired warps], zero between launches
     int full_norms;                // fused pass: all three norms (traced sweeps), else ‖X_new‖² only
     int64_t part_cap, x_cap, mask_cap;  // element / word capacities (IFCTN_DEBUG_CHECKS)
-    // norm passes: the last CTA to finish runs the sweep finaliser (finalize_norms_body) —
-    // one launch fewer per sweep; fin_cnt is the arrival counter (self-resetting)
-    int fin;
-    unsigned* fin_cnt;
-    const double* fin_delta;
-    int64_t fin_ndelta, fin_sh_off, fin_sh_len;
-    double* fin_p5;
-    double* fin_scal;
-    int* fin_flags;
-    int fin_obj_only, fin_combine;
 };
 
 template <typename T>

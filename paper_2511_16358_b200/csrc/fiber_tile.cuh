@@ -45,8 +45,6 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
     for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
     if (lane == 0)
         for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
-    pdl_trigger();  // see fiber_walk.cuh: setup above overlaps the predecessor's tail
-    pdl_wait();
     {
         const float4* s1 = reinterpret_cast<const float4*>(P.H + P.hres_src);
         const float4* s2 = reinterpret_cast<const float4*>(P.H + P.vf2_off);
@@ -414,8 +412,6 @@ __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     fiber_pass_vb_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, gridDim.x);
-    if constexpr (MODE == PASS_FUSED)
-        if (P.fin) pass_finalize(P, smem_raw);
 }
 
 }  // namespace ifctn

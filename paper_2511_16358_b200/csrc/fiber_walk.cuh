@@ -331,8 +331,7 @@ __device__ __forceinline__ bool walker_next(Walker& w, const PassParams<T>& P) {
     return true;
 }
 
-// The body of one pass for CTA `cta` of `ncta` (the __global__ wrapper below, or the
-// persistent sweep kernel of sweep.cuh, which runs every pass of a sweep in one launch).
+// The body of one pass for CTA `cta` (the __global__ wrapper below).
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned char* smem_raw, int cta) {
     // PASS_FUSED = the a5 refill of sweep s fused with the a2 contraction of block (0,1) of
@@ -358,13 +357,10 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
 
     // CTA setup: per warp zero the ring (row tails past I1p must read as 0) and init the
-    // stage barriers — independent of the previous kernel, so it overlaps its tail (PDL) —
-    // then, after the predecessor completed, the resident H_{0,r0} block (HRES).
+    // stage barriers, then the resident H_{0,r0} block (HRES).
     for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
     if (lane == 0)
         for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
-    pdl_trigger();
-    pdl_wait();
     if constexpr (HRES) {
         const float4* src = reinterpret_cast<const float4*>(P.H + P.hres_src);
         float4* dst = reinterpret_cast<float4*>(hres);
@@ -671,32 +667,10 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
     }
 }
 
-// Last-CTA sweep finaliser of a norm pass (PassParams::fin): after the body, every CTA
-// arrives on fin_cnt; the last one sums the norm partials and ΔG² (finalize_norms_body, the
-// same fixed order as the standalone finalize_norms launch) in its now idle shared memory.
-template <typename T>
-__device__ __forceinline__ void pass_finalize(const PassParams<T>& P, unsigned char* smem_raw) {
-    __shared__ unsigned last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = (atomicAdd(P.fin_cnt, 1u) == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    finalize_norms_body(P.norms, P.ngroups, P.fin_delta, P.fin_ndelta, P.fin_sh_off, P.fin_sh_len, P.fin_p5,
-                        P.fin_scal, P.fin_flags, P.fin_obj_only, P.fin_combine,
-                        reinterpret_cast<double*>(smem_raw));
-    if (threadIdx.x == 0) *P.fin_cnt = 0u;
-}
-
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     fiber_pass_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, blockIdx.x);
-    if constexpr (MODE == PASS_REFILL || MODE == PASS_OBJ || MODE == PASS_FUSED)
-        if (P.fin) pass_finalize(P, smem_raw);
 }
 
 }  // namespace ifctn

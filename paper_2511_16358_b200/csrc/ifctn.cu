@@ -21,7 +21,6 @@
 #include "fiber_tile.cuh"
 #include "solve.cuh"
 #include "metrics.cuh"
-#include "sweep.cuh"  // SweepOp / SweepProg (the kernels are in sweep_kernels.cu)
 #include "nccl_lite.h"
 
 namespace ifctn {
@@ -53,8 +52,6 @@ static int pow2ceil(int x) {
 }
 
 constexpr int64_t kGroupBoundThreads = 160LL * 2048;  // ≥ resident threads of any B200 part
-constexpr int64_t kPersistentMaxEntries = 64LL << 20;  // sweep_persistent up to this many entries
-constexpr int64_t kChunksPerWarp = 1;                  // tiled pass: dynamic chunks per warp (IFCTN_TUNE_CHUNKS)
 constexpr unsigned kFlagNoVBlock = IFCTN_FLAG_NO_VBLOCK;
 constexpr unsigned kFlagNoFuse = IFCTN_FLAG_NO_FUSE;
 
@@ -353,7 +350,6 @@ struct BlockPlan {
     SolveParams<T> sol;
     dim3 sol_grid;
     unsigned sol_threads = 128;
-    bool sol_warp = false;     // block_solve_w: a warp per column
     size_t sol_smem = 0;
     const void* sol_fn = nullptr;
     // multi-GPU, k ≠ shard mode: project → all-reduce → solve
@@ -402,15 +398,6 @@ static PassKernel pick_pass(int epl, int lpf, bool hres) {
     return hres ? pick_pass_cfg<T, MODE, true>(epl, lpf) : pick_pass_cfg<T, MODE, false>(epl, lpf);
 }
 
-// sweep_persistent instances live in their own translation unit (sweep_kernels.cu, compiled
-// in parallel with this one)
-const void* persistent_kernel(int esize, int epl, int lpf);
-
-template <typename T>
-static const void* pick_persistent(int epl, int lpf) {
-    return persistent_kernel((int)sizeof(T), epl, lpf);
-}
-
 template <typename T>
 static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
     switch (mode) {
@@ -423,21 +410,6 @@ static PassKernel pick_pass_mode(int mode, int epl, int lpf, bool hres) {
         case PASS_REFILL: return pick_pass<T, PASS_REFILL>(epl, lpf, hres);
         case PASS_OBJ: return pick_pass<T, PASS_OBJ>(epl, lpf, hres);
         default: return pick_pass<T, PASS_MODEL>(epl, lpf, hres);
-    }
-}
-
-template <typename T, int SM>
-static const void* pick_solve_w(int R) {
-    switch (R) {
-        case 1: return (const void*)block_solve_w<T, 1, SM>;
-        case 2: return (const void*)block_solve_w<T, 2, SM>;
-        case 3: return (const void*)block_solve_w<T, 3, SM>;
-        case 4: return (const void*)block_solve_w<T, 4, SM>;
-        case 5: return (const void*)block_solve_w<T, 5, SM>;
-        case 6: return (const void*)block_solve_w<T, 6, SM>;
-        case 7: return (const void*)block_solve_w<T, 7, SM>;
-        case 8: return (const void*)block_solve_w<T, 8, SM>;
-        default: return (const void*)block_solve_w<T, 9, SM>;
     }
 }
 
@@ -457,12 +429,7 @@ static const void* pick_solve_sm(int R) {
 }
 
 template <typename T>
-static const void* pick_solve(int R, int sm = SOLVE_FULL, bool warp = false) {
-    if (warp && R <= MAXR_SMALL) {
-        if (sm == SOLVE_PROJECT) return pick_solve_w<T, SOLVE_PROJECT>(R);
-        if (sm == SOLVE_FROM_PROJ) return pick_solve_w<T, SOLVE_FROM_PROJ>(R);
-        return pick_solve_w<T, SOLVE_FULL>(R);
-    }
+static const void* pick_solve(int R, int sm = SOLVE_FULL) {
     if (R > MAXR_SMALL) {
         const void* fn = sm == SOLVE_PROJECT     ? (const void*)block_solve_big<T, SOLVE_PROJECT>
                          : sm == SOLVE_FROM_PROJ ? (const void*)block_solve_big<T, SOLVE_FROM_PROJ>
@@ -511,20 +478,7 @@ struct Solver : SolverBase {
     int64_t n_mid_t = 0, n_last_t = 0;
     int64_t nlaunch_sweep = 0, last_launches = 0;
     int64_t ctr = 0;                       // kernels enqueued so far (graph nodes at capture)
-    // persistent whole-sweep kernel (sweep.cuh; single GPU, small tensors)
-    bool persist = false;
-    const void* persist_fn = nullptr;
-    int persist_ncta = 0;
-    size_t persist_smem = 0;
-    SweepProg<T> prog{};
-    void* prog_mem = nullptr;
-    int tune_ctas = 0;                     // experiment knob: cap fibre-pass CTAs per SM
-    bool pdl = false;                      // programmatic dependent launch (IFCTN_FLAG_PDL)
-    int64_t chunks_per_warp = kChunksPerWarp;  // tiled-pass chunks per warp (env knob)
-    bool solve_warp = false;               // warp-per-system small-rank solve (env IFCTN_TUNE_SOLVE_WARP=1;
-                                           // measured slower on C2–C5, faster on C1)
-    int64_t solve_slots = 64;              // max serial slot chain for the solve to absorb
-                                           // the reduce (env IFCTN_TUNE_SOLVE_SLOTS)
+    static constexpr int64_t solve_slots = 64;  // max serial slot chain for the solve to absorb the reduce
     int64_t n_full = 0, n_first = 0, n_mid = 0, n_last = 0;  // kernels per captured graph
     int64_t sh_off = 0, sh_len = 0;        // ΔG² range of the shard-mode chains
     double* p5 = nullptr;                  // norm partials (see finalize_norms)
@@ -539,10 +493,6 @@ struct Solver : SolverBase {
         for (cudaGraphExec_t e : {gexec, gexec_first, gexec_mid, gexec_last, gexec_mid_t, gexec_last_t})
             if (e) cudaGraphExecDestroy(e);
         if (trace_rows) cudaFree(trace_rows);
-        if (prog_mem) {
-            if (st) cudaStreamSynchronize(st);
-            cudaFree(prog_mem);
-        }
         if (comm && nccl) nccl->commDestroy(comm);
         if (st) cudaStreamSynchronize(st);
         if (own_ws && ws) cudaFree(ws);
@@ -582,22 +532,8 @@ struct Solver : SolverBase {
         launch_raw(fn, g, b, smem, args);
     }
 
-    // With IFCTN_FLAG_PDL, sweep kernels go out with programmatic stream serialization: the
-    // next kernel's CTAs launch while this one drains and wait in griddepcontrol.wait
-    // (common.cuh) for its completion.  Off by default: measured no gain on C2–C5 and a loss
-    // on C2r (early-resident dependents take SM slots from the running kernel).
     void launch_raw(const void* fn, dim3 g, dim3 b, size_t smem, void** args) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = g;
-        cfg.blockDim = b;
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = pdl ? at : nullptr;
-        cfg.numAttrs = pdl ? 1 : 0;
-        CU(cudaLaunchKernelExC(&cfg, fn, args));
+        CU(cudaLaunchKernel(fn, g, b, args, smem, st));
         ++ctr;
     }
 
@@ -774,15 +710,14 @@ struct Solver : SolverBase {
         int nb = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pp.fn, kPassThreads, smem));
         if (nb < 1) nb = 1;
-        if (tune_ctas > 0) nb = std::min(nb, tune_ctas);
         // grid: one wave of warps.  Plain walk: one fibre range ("group") per warp, equal
-        // fibre counts.  Tiled pass: kChunksPerWarp× more fixed chunks ("groups") than warps,
-        // claimed dynamically (fiber_tile.cuh), so no SM idles while others finish.
+        // fibre counts.  Tiled pass: one fixed chunk ("group") per warp, claimed dynamically
+        // (fiber_tile.cuh), so no SM idles while others finish.
         int64_t gmax = (int64_t)nsm * nb * nwarps;
         gmax = std::min(gmax, s.groups_bound);
         const int64_t unit = vblk ? kern.F : 1;  // v-blocked ranges hold whole runs
         const int64_t nunits = p.nfib / unit;
-        const int64_t nchunk = vblk ? std::min(gmax * chunks_per_warp, s.groups_bound) : gmax;
+        const int64_t nchunk = gmax;
         const int64_t L = std::max<int64_t>(1, (nunits + nchunk - 1) / nchunk) * unit;
         p.L = L;
         p.ngroups = (p.nfib + L - 1) / L;
@@ -896,8 +831,6 @@ struct Solver : SolverBase {
                 const bool gather_ok = r.kept1 ? (i == 0 && chain <= solve_slots) : (slots_per_v <= 16 && s.ld[i] >= 16);
                 q.fused_reduce = (q.R <= MAXR_SMALL && gather_ok && !(flags & IFCTN_FLAG_NO_SOLVE_REDUCE)) ? 1 : 0;
                 b.sol_grid = dim3((unsigned)s.ld[k]);
-                b.sol_warp = solve_warp && q.R <= MAXR_SMALL;
-                if (b.sol_warp) b.sol_grid = dim3((unsigned)((s.ld[k] + 3) / 4));
                 if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): a CTA per column
                     b.sol_threads = kBigThreads;
                     // stage all of G_{i,k} at once when it fits in ≈ 96 KB, else 32-column tiles
@@ -917,11 +850,11 @@ struct Solver : SolverBase {
                 b.dist = s.dpath && k != s.shard;
                 if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
                     const int R = s.R(k, i);
-                    b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT, b.sol_warp);
-                    b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ, b.sol_warp);
+                    b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT);
+                    b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ);
                     b.proj_count = s.ld[k] * (R * (R + 1) / 2 + R);
                 } else {
-                    b.sol_fn = pick_solve<T>(s.R(k, i), SOLVE_FULL, b.sol_warp);
+                    b.sol_fn = pick_solve<T>(s.R(k, i), SOLVE_FULL);
                 }
                 blocks.push_back(b);
             }
@@ -949,144 +882,6 @@ struct Solver : SolverBase {
             fused_sol.red = fused_red;
             has_fused = true;
         }
-        set_fin(refill, 0);
-        set_fin(obj, 1);
-        if (has_fused) set_fin(fused, 0);
-    }
-
-    // IFCTN_FLAG_PASS_FINALIZE: the norm passes run the sweep finaliser in their last CTA
-    // (needs 40 KB of their shared memory as scratch; bit-identical to the finalize_norms
-    // launch, measured no faster — the 1024-thread finaliser kernel is quicker than one
-    // 256-thread CTA at the end of a pass)
-    void set_fin(PassPlan<T>& pp, int obj_only) {
-        PassParams<T>& p = pp.p;
-        p.fin = ((flags & IFCTN_FLAG_PASS_FINALIZE) && pp.smem >= sizeof(double) * 5 * 1024) ? 1 : 0;
-        p.fin_cnt = sched + 4;
-        p.fin_delta = delta;
-        p.fin_ndelta = obj_only ? 0 : s.ndelta;
-        p.fin_sh_off = sh_off;
-        p.fin_sh_len = sh_len;
-        p.fin_p5 = p5;
-        p.fin_scal = scal;
-        p.fin_flags = dflags;
-        p.fin_obj_only = obj_only;
-        p.fin_combine = s.dpath ? 0 : 1;
-    }
-
-    // after a norm pass: its finaliser (in-pass or a launch), then the cross-rank combine
-    void finish_norm_pass(const PassParams<T>& p, int obj_only) {
-        if (!p.fin) {
-            enqueue_finalize(p.ngroups, obj_only);
-            return;
-        }
-        prof_mark();  // the finaliser ran inside the pass: empty interval in ifctn_profile_sweep
-        if (s.dpath) {
-            allreduce_dev(p5, 4);
-            prof_mark();
-            int a3 = obj_only;
-            void* args[] = {&p5, &scal, &dflags, &a3};
-            launch_raw((const void*)combine_norms, dim3(1), dim3(32), 0, args);
-        }
-    }
-
-    // The op list of one unfused sweep for sweep_persistent, its parameters copied to the
-    // device, and its launch shape (the pass one-wave grid; every pass grid must fit).
-    void build_persistent() {
-        persist = false;
-        // opt-in: measured slower than the graph path on C1–C4
-        const bool want = (flags & IFCTN_FLAG_PERSISTENT) && !(flags & IFCTN_FLAG_NO_PERSISTENT);
-        if (!want || s.dpath || (flags & IFCTN_FLAG_NO_GRAPH)) return;
-        for (const auto& b : blocks)  // validated for the register solve only (R ≤ 9)
-            if (b.sol.R > MAXR_SMALL) return;
-        std::vector<SweepOp> ops;
-        std::vector<PassParams<T>> pv;
-        std::vector<ReduceParams<T>> rv;
-        std::vector<SolveParams<T>> sv;
-        size_t smem = sweep_scratch_bytes(0);
-        int64_t max_pass_grid = 0;
-        auto add_pass = [&](const PassPlan<T>& pp, int mode, bool vblk) {
-            SweepOp op{};
-            op.kind = OP_PASS;
-            op.variant = mode * 4 + (vblk ? 2 : 0) + (pp.p.hres_elems > 0 ? 1 : 0);
-            op.idx = (int)pv.size();
-            pv.push_back(pp.p);
-            pv.back().fin = 0;  // the program has its own OP_FINALIZE
-            ops.push_back(op);
-            smem = std::max(smem, pp.smem);
-            max_pass_grid = std::max<int64_t>(max_pass_grid, pp.grid.x);
-        };
-        for (const auto& b : blocks) {
-            add_pass(b.pass, (b.k == 0 || b.i == 0) ? PASS_KEPT1 : PASS_RED1, b.vblk);
-            if (!b.sol.fused_reduce) {
-                SweepOp op{};
-                op.kind = OP_REDUCE;
-                op.variant = b.red_l.fn == (const void*)reduce_partials_warp<T> ? 0 : 1;
-                op.idx = (int)rv.size();
-                op.nvb = (int64_t)b.red_l.grid.x * b.red_l.grid.y * b.red_l.grid.z;
-                op.gy = (int)b.red_l.grid.y;
-                op.gz = (int)b.red_l.grid.z;
-                rv.push_back(b.red);
-                ops.push_back(op);
-            }
-            SweepOp op{};
-            op.kind = b.sol.R > MAXR_SMALL ? OP_SOLVE_BIG : OP_SOLVE;
-            op.variant = b.sol.R + (b.sol_warp ? 16 : 0);
-            op.idx = (int)sv.size();
-            op.nvb = b.sol_warp ? (s.ld[b.k] + 3) / 4 : s.ld[b.k];
-            sv.push_back(b.sol);
-            ops.push_back(op);
-            if (op.kind == OP_SOLVE_BIG) smem = std::max(smem, sweep_scratch_bytes(b.sol_smem));
-        }
-        add_pass(refill, PASS_REFILL, false);
-        {
-            SweepOp op{};
-            op.kind = OP_FINALIZE;
-            ops.push_back(op);
-        }
-        const void* fn = pick_persistent<T>(s.epl, s.lpf);
-        cudaFuncAttributes fa;
-        CU(cudaFuncGetAttributes(&fa, fn));
-        if (smem + fa.sharedSizeBytes > smem_limit) return;
-        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int occ = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kPassThreads, smem));
-        const int ncta = nsm * std::min(occ, kPassMinBlocks);
-        if (occ < 1 || ncta < max_pass_grid) return;
-        // device copy of the program
-        const size_t bo = 0, bp = align_up((int64_t)(ops.size() * sizeof(SweepOp)), 256);
-        const size_t br = bp + align_up((int64_t)(pv.size() * sizeof(PassParams<T>)), 256);
-        const size_t bs = br + align_up((int64_t)(std::max<size_t>(rv.size(), 1) * sizeof(ReduceParams<T>)), 256);
-        const size_t total = bs + std::max<size_t>(sv.size(), 1) * sizeof(SolveParams<T>);
-        CU(cudaMalloc(&prog_mem, total));
-        unsigned char* base = (unsigned char*)prog_mem;
-        CU(cudaMemcpyAsync(base + bo, ops.data(), ops.size() * sizeof(SweepOp), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(base + bp, pv.data(), pv.size() * sizeof(PassParams<T>), cudaMemcpyHostToDevice, st));
-        if (!rv.empty())
-            CU(cudaMemcpyAsync(base + br, rv.data(), rv.size() * sizeof(ReduceParams<T>), cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(base + bs, sv.data(), sv.size() * sizeof(SolveParams<T>), cudaMemcpyHostToDevice, st));
-        CU(cudaStreamSynchronize(st));
-        prog.ops = (const SweepOp*)(base + bo);
-        prog.nops = (int)ops.size();
-        prog.pass = (const PassParams<T>*)(base + bp);
-        prog.red = (const ReduceParams<T>*)(base + br);
-        prog.sol = (const SolveParams<T>*)(base + bs);
-        prog.norms = norms;
-        prog.ngroups = refill.p.ngroups;
-        prog.delta = delta;
-        prog.ndelta = s.ndelta;
-        prog.p5 = p5;
-        prog.scal = scal;
-        prog.flags = dflags;
-        persist_fn = fn;
-        persist_ncta = ncta;
-        persist_smem = smem;
-        persist = true;
-    }
-
-    void launch_persistent(int nsweeps) {
-        void* args[] = {(void*)&prog, (void*)&nsweeps};
-        CU(cudaLaunchCooperativeKernel(persist_fn, dim3(persist_ncta), dim3(kPassThreads), args, persist_smem, st));
-        ++ctr;
     }
 
     void build_all_H() {
@@ -1146,7 +941,7 @@ struct Solver : SolverBase {
 
     void enqueue_xupdate() {
         launch(refill.fn, refill.grid, dim3(kPassThreads), refill.smem, refill.p);
-        finish_norm_pass(refill.p, 0);
+        enqueue_finalize(refill.p.ngroups, 0);
     }
 
     void enqueue_sweep() {
@@ -1170,7 +965,7 @@ struct Solver : SolverBase {
         PassParams<T> fp = fused.p;
         fp.full_norms = traced ? 1 : 0;
         launch(fused.fn, fused.grid, dim3(kPassThreads), fused.smem, fp);
-        finish_norm_pass(fp, 0);
+        enqueue_finalize(fp.ngroups, 0);
         if (traced) enqueue_trace_push();
         if (!b0.sol.fused_reduce) launch(fused_red_l.fn, fused_red_l.grid, dim3(256), 0, fused_red);
         enqueue_solve(b0, &fused_sol);
@@ -1190,11 +985,6 @@ struct Solver : SolverBase {
         int smo = 0;
         CU(cudaDeviceGetAttribute(&smo, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         smem_limit = (size_t)smo;
-        if (const char* e = getenv("IFCTN_TUNE_CTAS")) tune_ctas = atoi(e);  // experiments only
-        pdl = (flags & IFCTN_FLAG_PDL) != 0;
-        if (const char* e = getenv("IFCTN_TUNE_CHUNKS")) chunks_per_warp = std::max(1, atoi(e));
-        if (const char* e = getenv("IFCTN_TUNE_SOLVE_SLOTS")) solve_slots = atoi(e);
-        if (const char* e = getenv("IFCTN_TUNE_SOLVE_WARP")) solve_warp = atoi(e) != 0;
         CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
@@ -1261,7 +1051,6 @@ struct Solver : SolverBase {
         }
         plan();
         build_all_H();
-        build_persistent();
         CU(cudaStreamSynchronize(st));
         end();
     }
@@ -1324,13 +1113,6 @@ struct Solver : SolverBase {
         int s_done = 0;
         last_launches = 0;
         const int64_t c0 = ctr;
-        if (persist && !need_sync && t_max >= 1) {  // small tensor: every sweep in one launch
-            launch_persistent(t_max);
-            last_launches = 1;
-            if (done) *done = t_max;
-            end();
-            return;
-        }
         if (has_fused && trace && !(eps > 0.0) && use_graph && t_max >= 2) {
             // traced, fixed sweep count: the fused sequence with full norms; every sweep's row
             // is appended on the device and read back once
@@ -1578,7 +1360,7 @@ struct Solver : SolverBase {
     double objective() override {
         begin();
         launch(obj.fn, obj.grid, dim3(kPassThreads), obj.smem, obj.p);
-        finish_norm_pass(obj.p, 1);
+        enqueue_finalize(obj.p.ngroups, 1);
         CU(cudaMemcpyAsync(hscal, scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         end();

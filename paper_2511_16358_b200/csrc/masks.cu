@@ -137,10 +137,7 @@ __global__ void __launch_bounds__(1024) select_resolve(SelectState* st, unsigned
     for (unsigned long long x = threadIdx.x; x < cnt; x += blockDim.x) {
         unsigned long long less = 0;
         for (unsigned long long y = 0; y < cnt; ++y) less += c[y] < c[x];
-        if (less + 1 == r) {
-            st->prefix = c[x];
-            st->rank = 1;
-        }
+        if (less + 1 == r) st->prefix = c[x];  // rank is not read after a resolve
     }
 }
 
@@ -257,6 +254,14 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Single exit after the scratch allocation: the scratch is always released on the stream,
+// whatever failed before (a failed launch leaves the stream usable for the free).
+ifctn_status finish(SelectState* st, cudaStream_t stream, cudaError_t e) {
+    if (e == cudaSuccess) e = cudaGetLastError();
+    const cudaError_t f = cudaFreeAsync(st, stream);
+    return (e == cudaSuccess && f == cudaSuccess) ? IFCTN_OK : IFCTN_E_CUDA;
+}
+
 }  // namespace
 
 extern "C" ifctn_status ifctn_mask_uniform(uint8_t* mask, int64_t n, int64_t observed, uint64_t seed,
@@ -269,18 +274,17 @@ extern "C" ifctn_status ifctn_mask_uniform(uint8_t* mask, int64_t n, int64_t obs
     if (cudaMallocAsync(reinterpret_cast<void**>(&st), sizeof(SelectState), stream) != cudaSuccess)
         return IFCTN_E_CUDA;
     const int all = observed == n;
+    cudaError_t e = cudaSuccess;
     if (observed > 0 && !all) {
-        if (select_kth(st, seed, n, observed, stream) != cudaSuccess) return IFCTN_E_CUDA;
+        e = select_kth(st, seed, n, observed, stream);
     } else {
         init_state<<<1, 1024, 0, stream>>>(st, 0ull);  // T unused: all observed, or memset below
     }
-    if (observed == 0) {
-        if (cudaMemsetAsync(mask, 0, (size_t)n, stream) != cudaSuccess) return IFCTN_E_CUDA;
-    } else {
-        write_uniform<<<grid_for((n + 15) / 16), 256, 0, stream>>>(mask, st, seed, n, all);
+    if (e == cudaSuccess) {
+        if (observed == 0) e = cudaMemsetAsync(mask, 0, (size_t)n, stream);
+        else write_uniform<<<grid_for((n + 15) / 16), 256, 0, stream>>>(mask, st, seed, n, all);
     }
-    if (cudaFreeAsync(st, stream) != cudaSuccess) return IFCTN_E_CUDA;
-    return cudaGetLastError() == cudaSuccess ? IFCTN_OK : IFCTN_E_CUDA;
+    return finish(st, stream, e);
 }
 
 extern "C" ifctn_status ifctn_mask_fibres(uint8_t* mask, int order, const int64_t* dims, int mode,
@@ -301,12 +305,13 @@ extern "C" ifctn_status ifctn_mask_fibres(uint8_t* mask, int order, const int64_
     if (cudaMallocAsync(reinterpret_cast<void**>(&st), sizeof(SelectState), stream) != cudaSuccess)
         return IFCTN_E_CUDA;
     const int none = missing_fibres == 0, every = missing_fibres == nf;
+    cudaError_t e = cudaSuccess;
     if (!none && !every) {
-        if (select_kth(st, seed, nf, missing_fibres, stream) != cudaSuccess) return IFCTN_E_CUDA;
+        e = select_kth(st, seed, nf, missing_fibres, stream);
     } else {
         init_state<<<1, 1024, 0, stream>>>(st, 0ull);  // T unused (none / every flag)
     }
-    write_fibres<<<grid_for((n + 15) / 16), 256, 0, stream>>>(mask, st, seed, n, inner, Im, none, every);
-    if (cudaFreeAsync(st, stream) != cudaSuccess) return IFCTN_E_CUDA;
-    return cudaGetLastError() == cudaSuccess ? IFCTN_OK : IFCTN_E_CUDA;
+    if (e == cudaSuccess)
+        write_fibres<<<grid_for((n + 15) / 16), 256, 0, stream>>>(mask, st, seed, n, inner, Im, none, every);
+    return finish(st, stream, e);
 }

@@ -66,8 +66,6 @@ __device__ __forceinline__ void reduce_partials_warp_body(const ReduceParams<T>&
 
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_partials_warp(const ReduceParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
     reduce_partials_warp_body(P, blockIdx.x);
 }
 
@@ -151,8 +149,6 @@ __device__ __forceinline__ void reduce_partials_body(const ReduceParams<T>& P, i
 
 template <typename T>
 __global__ void __launch_bounds__(256) reduce_partials(const ReduceParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
     __shared__ double sb[256], sw[256];
     __shared__ unsigned last;
     reduce_partials_body(P, blockIdx.x, blockIdx.y, blockIdx.z, sb, sw, &last);
@@ -217,20 +213,16 @@ __device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t 
     w = sw;
 }
 
-template <typename T, int R, int SM, bool W = false>
+template <typename T, int R, int SM>
 // nthr (a multiple of 32, ≤ blockDim.x) threads take part; the others only pass the barriers
 __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_t j, int nthr,
                                                  double* red /*(nthr/32)·NA*/, double* cs /*R*/) {
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
     const int nw = nthr >> 5;
-    // W: the "CTA" is one warp (warp-per-system: lane ids, __syncwarp, nthr = 32)
-    const int tid = W ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
-    const int ntot = W ? 32 : (int)blockDim.x;
-    auto sync = [&]() {
-        if constexpr (W) __syncwarp();
-        else __syncthreads();
-    };
+    const int tid = (int)threadIdx.x;
+    const int ntot = (int)blockDim.x;
+    auto sync = [&]() { __syncthreads(); };
     double acc[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
@@ -358,25 +350,10 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
 
 template <typename T, int R, int SM>
 __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
     constexpr int NA = R * (R + 1) / 2 + R;
     __shared__ double red[4 * NA];
     __shared__ double cs[R];
     block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs);
-}
-
-// warp per system: 4 columns per 128-thread CTA, no CTA-wide barrier (north-star design)
-template <typename T, int R, int SM>
-__global__ void __launch_bounds__(128) block_solve_w(const SolveParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
-    constexpr int NA = R * (R + 1) / 2 + R;
-    __shared__ double red[4][NA];
-    __shared__ double cs[4][R];
-    const int w = threadIdx.x >> 5;
-    const int64_t j = (int64_t)blockIdx.x * 4 + w;
-    if (j < P.Ik) block_solve_body<T, R, SM, true>(P, j, 32, red[w], cs[w]);
 }
 
 // ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------
@@ -670,8 +647,6 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
 
 template <typename T, int SM>
 __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
-    pdl_trigger();
-    pdl_wait();
     extern __shared__ __align__(16) double bsm[];
     __shared__ int ok;
     __shared__ double colb[2 * 64];
@@ -753,8 +728,6 @@ static __global__ void __launch_bounds__(1024) finalize_norms(const double* norm
                                                        int64_t sh_off, int64_t sh_len, double* p5,
                                                        double* scal, int* flags, int obj_only,
                                                        int combine) {
-    pdl_trigger();
-    pdl_wait();
     __shared__ double s[5 * 1024];
     finalize_norms_body(norms, ngroups, delta, ndelta, sh_off, sh_len, p5, scal, flags, obj_only, combine, s);
 }
@@ -774,8 +747,6 @@ static __global__ void trace_push(const double* scal, double* rows, int* count) 
 }
 
 static __global__ void combine_norms(const double* p5, double* scal, int* flags, int obj_only) {
-    pdl_trigger();
-    pdl_wait();
     if (threadIdx.x == 0 && blockIdx.x == 0) combine_into(p5, scal, flags, obj_only);
 }
 

@@ -34,15 +34,22 @@ def rank_grid(dims, observed, mask, instances, t_max, truth=None, concurrency=8,
         dt = observed.dtype
         is64 = (dt == np.float64) if isinstance(dt, np.dtype) else (dt == torch.float64)
         dtype = IFCTN_F64 if is64 else IFCTN_F32
-    if isinstance(mask, np.ndarray):
-        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    from . import check_buffer, factor_layout
+    if isinstance(mask, np.ndarray) and mask.dtype == np.bool_:
+        mask = mask.view(np.uint8)
+    kind = "f64" if dtype == IFCTN_F64 else "f32"
+    n = int(np.prod(dims))
+    check_buffer(observed, "observed", kind, n)
+    check_buffer(mask, "mask", "u8", n)
+    if truth is not None:
+        check_buffer(truth, "truth", kind, n)
     keep = []
     inst = []
-    for d in instances:
+    for q, d in enumerate(instances):
         R = np.asarray(d["ranks"], dtype=np.int32).reshape(N, N)
         g = d["init"]
-        if isinstance(g, np.ndarray):
-            g = np.ascontiguousarray(g)
+        lay = factor_layout(dims, R)
+        check_buffer(g, f"instances[{q}].init", kind, lay[-1][2] + lay[-1][3] * lay[-1][4])
         keep.append(g)
         inst.append(([int(v) for v in R.reshape(-1)], float(d.get("rho", 0.1)), _ptr(g)))
     return _abi.ifctn_grid_run(N, dims, dtype, _ptr(observed), _ptr(mask), _ptr(truth), inst,

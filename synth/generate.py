@@ -178,6 +178,10 @@ def init_factors(dims, ranks, observed, mask, dtype, init_kind="uniform", seed=0
 MSI_GRID = [(r12, r3) for r12 in (3, 6, 9, 15, 30, 36) for r3 in (3, 6, 9)]
 
 
+# The paper's traffic rank grid: R_{1,2} ∈ {2,3,4,6,9,12,36}, R_{1,3} = R_{2,3} ∈ {3,6,9,12}
+TRAFFIC_GRID = [(r12, r3) for r12 in (2, 3, 4, 6, 9, 12, 36) for r3 in (3, 6, 9, 12)]
+
+
 def grid_rank_matrix(r12: int, r3: int) -> np.ndarray:
     return np.array([[0, r12, r3], [r12, 0, r3], [r3, r3, 0]], np.int32)
 
@@ -231,6 +235,11 @@ CONFIGS = {
     "C4": dict(dims=(214, 61, 144, 4), R=5, dtype="float32", truth_kind="traffic",
                scale_noise=0.05, mask_kind="fibre", fibre_missing_ratio=0.70, fibre_mode=2,
                init_kind="uniform", sweeps=200),
+    # The 3rd-order Guangzhou shape itself (214×61×144) on the C4 recipe: the tensor
+    # the paper's traffic rank grid (TRAFFIC_GRID) is tuned on (f2 bench).
+    "C4g": dict(dims=(214, 61, 144), R=5, dtype="float32", truth_kind="traffic", scale_noise=0.05,
+                mask_kind="fibre", fibre_missing_ratio=0.70, fibre_mode=2, init_kind="uniform",
+                sweeps=100),
     "C5": dict(dims=(64, 64, 64, 64, 32), R=4, dtype="float32", truth_kind="normal", sr=0.05,
                init_kind="normal", sweeps=50),
     # Reduced-size twins with the same recipes, for oracle-speed parity tests (ragged mode-1

@@ -147,3 +147,30 @@ def test_header_is_plain_c(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("IFCTN_OK")
+
+
+def test_binding_validates_buffers_before_the_call(abi):
+    """The binding checks dtype, element count (local shard / factor layout) and contiguity
+    of every buffer before its raw address crosses the ABI — a float64 G⁰ for a float32
+    problem, a view, or a buffer of the wrong extent raises E_ARG instead of being read as
+    garbage (all rejected before any device work, so this runs without a GPU)."""
+    from paper_2511_16358_b200 import IfctnError, Solver, num_params
+    dims, R = (6, 5, 4), 2
+    n = int(np.prod(dims))
+    obs = np.zeros(n, np.float32)
+    mask = np.ones(n, np.uint8)
+    g0 = np.zeros(num_params(dims, R), np.float32)
+    cases = [
+        (obs.astype(np.float64), mask, g0, "dtype"),                # O of another dtype than G⁰
+        (obs, mask, g0.astype(np.float64), "dtype"),                # G⁰ float64, O float32
+        (obs[:-1], mask, g0, "elements"),                           # short O
+        (obs, mask[:-3], g0, "elements"),                           # short mask
+        (obs, mask, g0[:-1], "elements"),                           # short G⁰
+        (np.zeros(2 * n, np.float32)[::2], mask, g0, "contiguous"),  # strided view
+        (obs, mask.astype(np.int32), g0, "dtype"),                  # mask not bytes
+    ]
+    for o, m, g, what in cases:
+        with pytest.raises(IfctnError, match=f"E_ARG.*{what}"):
+            Solver(dims, R, o, m, g)
+    with pytest.raises(IfctnError, match="E_ARG.*dtype"):
+        Solver(dims, R, obs, mask, g0, dtype=abi.IFCTN_F64)        # declared dtype wins

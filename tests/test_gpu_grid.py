@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from synth import MSI_GRID, grid_rank_matrix, init_factors, make_config
+from synth import MSI_GRID, TRAFFIC_GRID, grid_rank_matrix, init_factors, make_config
 
 from gpu_util import dev, rel, requires_cuda, torch
 
@@ -70,3 +70,26 @@ def test_grid_reports_bad_instance():
     bad["ranks"] = np.array([[0, 65, 3], [65, 0, 3], [3, 3, 0]], np.int32)   # above IFCTN_MAX_RANK
     with pytest.raises(IfctnError):
         rank_grid(p.dims, dev(p.observed), dev(p.mask), [inst[0], bad], 2, concurrency=2)
+
+
+@pytest.mark.parametrize("pair", [(2, 3), (9, 6), (36, 12)])
+def test_traffic_grid_instances_vs_oracle_rse(pair):
+    """The paper's traffic rank grid on the Guangzhou-shaped C4 recipe (C4g,
+    214×61×144, fibre mask 70%): spot-check instances — smallest, middle, largest R_{1,2} —
+    of a grid run against the float64 oracle's RSE after 10 sweeps (reading R22)."""
+    import os
+    from paper_2511_16358_b200.grid import rank_grid
+    O.set_threads(max(1, min(16, os.cpu_count() or 1)))
+    p = make_config("C4g")
+    assert len(TRAFFIC_GRID) == 28 and pair in TRAFFIC_GRID
+    inst = _grid(p, [pair, (4, 9)])
+    res = rank_grid(p.dims, dev(p.observed), dev(p.mask), inst, 10, truth=dev(p.truth), concurrency=2)
+    assert all(r["status"] == 0 for r in res)
+    d = inst[0]
+    sh = O.Shape(p.dims, d["ranks"])
+    G = np.asarray(d["init"], np.float64).copy()
+    X = O.init_x(p.observed, p.mask)
+    r, _ = O.solve(sh, G, X, p.mask, p.rho, 10, 0.0, False)
+    assert r == 10
+    ro = O.rse(p.truth.astype(np.float64), X)
+    assert abs(res[0]["rse"] - ro) <= 1e-3 * ro + 1e-5, (res[0]["rse"], ro)

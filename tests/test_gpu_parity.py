@@ -38,6 +38,37 @@ def test_initial_x_is_masked_observed_bit_exact(name):
     assert np.array_equal(G.view(np.uint8), p.G0.view(np.uint8))
 
 
+@pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "C5s"])
+def test_values_off_omega_are_ignored(name):
+    """X⁽⁰⁾ = P_Ω(O) (reading R7; include/ifctn.h "values off Ω are ignored"): an O
+    carrying nonzero garbage on Ω^c gives the same X⁽⁰⁾ as the zero-filled O — bit for bit,
+    from device and from host buffers — and the same first sweep as the oracle started
+    from the same dirty O."""
+    from paper_2511_16358_b200 import Solver
+    p = make_config(name)
+    obs = p.mask.astype(bool)
+    rng = np.random.default_rng(7)
+    dirty = p.observed.copy()
+    dirty[~obs] = (rng.standard_normal(int((~obs).sum())) + 3.0).astype(p.dtype)
+    assert np.all(dirty[~obs] != 0)
+    Xo = O.init_x(dirty, p.mask)                       # the oracle's own P_Ω
+    assert np.array_equal(Xo, O.init_x(p.observed, p.mask))
+    for s in (Solver(p.dims, p.ranks, dev(dirty), dev(p.mask), dev(p.G0), rho=p.rho),
+              Solver(p.dims, p.ranks, dirty, p.mask, p.G0, rho=p.rho)):
+        X0 = s.reconstruct().cpu().numpy()
+        assert np.array_equal(X0.astype(np.float64), Xo)
+        assert np.array_equal(X0.view(np.uint8), np.where(obs, p.observed, 0).astype(p.dtype).view(np.uint8))
+        s.sweep(1)
+        sh, G = O.Shape(p.dims, p.ranks), p.G0.astype(np.float64)
+        X = Xo.copy()
+        st, _, _ = O.sweep(sh, G, X, p.mask, p.rho, O.objective(sh, G, X), True)
+        assert st == 0
+        assert rel(s.factors().cpu().numpy(), G) <= tol_for(p)
+        Xg = s.reconstruct().cpu().numpy()
+        assert rel(Xg, X) <= tol_for(p)
+        assert np.array_equal(Xg[obs].view(np.uint8), p.observed[obs].view(np.uint8))
+
+
 def test_host_and_device_inputs_agree():
     from paper_2511_16358_b200 import Solver
     p = make_config("C4s")
@@ -110,6 +141,32 @@ def test_block_coefficients(name, vblock):
             bo, wo = O.block_contract(sh, G, Xin, k, i)
             assert rel(w, wo) <= tol, (k, i, rel(w, wo))
             assert rel(b, bo) <= tol, (k, i, rel(b, bo))
+            _check_columns(p, Xin, k, i, b, w, bo, wo, tol)
+
+
+def _slab_sq_sums(p, X, k, i):
+    """Σ X² over the entries with i_i = a, i_k = j, as an I_i × I_k array (plain numpy)."""
+    Xt = np.asarray(X, np.float64).reshape(tuple(reversed(p.dims)))   # axis N-1-m ↔ mode m
+    red = tuple(p.N - 1 - m for m in range(p.N) if m not in (k, i))
+    S = (Xt * Xt).sum(axis=red) if red else Xt * Xt
+    # remaining axes in descending mode order; want [a = i_i, j = i_k]
+    return S.T if i < k else S
+
+
+def _check_columns(p, X, k, i, b, w, bo, wo, tol):
+    """Element-wise and per-column checks of β, ω (so a wrong small column cannot hide under
+    the large ones in one Frobenius norm).  ω is a sum of squares: every entry within
+    tol·ω.  β is a signed sum: |β − β_o| ≤ tol·(|β_o| + Σ|M X|), with Σ|M X| bounded by
+    Cauchy–Schwarz as sqrt(ω · Σ X²) over the same entries; per column (j) the same
+    bound in the 2-norm."""
+    b, w, bo, wo = (np.asarray(x, np.float64) for x in (b, w, bo, wo))   # (I_i, I_k): [a, j]
+    scale = np.sqrt(wo * _slab_sq_sums(p, X, k, i))
+    assert np.all(np.abs(w - wo) <= tol * wo + 1e-300), (k, i)
+    eb = np.abs(b - bo)
+    assert np.all(eb <= tol * (np.abs(bo) + scale) + 1e-300), (k, i, float((eb / (np.abs(bo) + scale + 1e-300)).max()))
+    for j in range(p.dims[k]):
+        assert np.linalg.norm(w[:, j] - wo[:, j]) <= tol * np.linalg.norm(wo[:, j]) + 1e-300, (k, i, j)
+        assert np.linalg.norm(b[:, j] - bo[:, j]) <= tol * (np.linalg.norm(bo[:, j]) + np.linalg.norm(scale[:, j])) + 1e-300, (k, i, j)
 
 
 # ------------------------------------------------------------ a3/a4: one block update ---
@@ -152,9 +209,11 @@ def test_x_update_and_norms(name):
 
 # ----------------------------------------------------------------- one whole sweep ---
 
-@pytest.mark.parametrize("name", SMALL + ["C2", "C3", "C4", "C2r"])
+@pytest.mark.parametrize("name", SMALL + ["C2", "C3", "C4", "C2r", "C5"])
 def test_one_sweep_parity(name):
-    """North-star bar: factors and X within 1e-4 relative Frobenius after one sweep."""
+    """North-star bar: factors and X within 1e-4 relative Frobenius after one sweep — on
+    every configuration at full size, C5 included (64⁴×32: the float64 oracle sweep takes
+    ≈ 12–35 s on the host cores, input generation ≈ 25 s)."""
     p = make_config(name)
     s = make_solver(p)
     sh, G, X = oracle_state(p)
@@ -200,11 +259,11 @@ def test_trace_lemma2_and_feasibility(name):
 
 @pytest.mark.parametrize("name", ["C2s", "C5s"])
 def test_graph_and_plain_launches_bit_identical(name):
-    from paper_2511_16358_b200 import IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_NO_PERSISTENT
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_GRAPH
     p = make_config(name)
-    a = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
+    a = make_solver(p)
     b = make_solver(p, flags=IFCTN_FLAG_NO_GRAPH)
-    c = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
+    c = make_solver(p)
     for x in (a, b, c):
         x.sweep(3)
     Xa, Xb, Xc = (x.reconstruct().cpu().numpy() for x in (a, b, c))
@@ -224,10 +283,10 @@ def test_graph_and_plain_launches_bit_identical(name):
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C2"])
 def test_fused_sweeps_match_plain_sweeps(name):
     """The fused a5(s) ⊕ a2(0,1)(s+1) pass reproduces the plain sweep sequence."""
-    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_PERSISTENT
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE
     p = make_config(name)
-    a = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
-    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE | IFCTN_FLAG_NO_PERSISTENT)
+    a = make_solver(p)
+    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE)
     a.sweep(2)   # sweep 1's blocks, [a5(1) ⊕ a2(0,1)(2)], sweep 2's other blocks, a5(2)
     b.sweep(2)
     tol = tol_for(p, 1e-5, 1e-12)
@@ -259,9 +318,8 @@ def test_traced_fused_rows_match_unfused_trace(name):
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C3"])
 def test_fused_three_sweeps_vs_oracle(name):
     """Three sweeps through the fused sequence against three oracle sweeps (north-star bar)."""
-    from paper_2511_16358_b200 import IFCTN_FLAG_NO_PERSISTENT
     p = make_config(name)
-    s = make_solver(p, flags=IFCTN_FLAG_NO_PERSISTENT)
+    s = make_solver(p)
     s.sweep(3)
     sh, G, X = oracle_state(p)
     F = O.objective(sh, G, X)
@@ -271,58 +329,6 @@ def test_fused_three_sweeps_vs_oracle(name):
     tol = tol_for(p)
     assert rel(s.factors().cpu().numpy(), G) <= tol
     assert rel(s.reconstruct().cpu().numpy(), X) <= tol
-
-
-@pytest.mark.parametrize("name", ["C1", "C2s", "C4s", "C2"])
-def test_in_pass_finaliser_bit_identical(name):
-    """IFCTN_FLAG_PASS_FINALIZE: the norm passes run the sweep finaliser in their last CTA
-    (same fixed summation order as the finalize_norms launch): traces, objective and state
-    are bit-identical."""
-    from paper_2511_16358_b200 import IFCTN_FLAG_PASS_FINALIZE
-    p = make_config(name)
-    a = make_solver(p, flags=IFCTN_FLAG_PASS_FINALIZE)
-    b = make_solver(p)
-    ra = a.sweep(3, trace=True)[1] + a.sweep(1, trace=True)[1]
-    rb = b.sweep(3, trace=True)[1] + b.sweep(1, trace=True)[1]
-    assert ra == rb
-    a.sweep(2)
-    b.sweep(2)
-    assert a.objective() == b.objective()
-    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
-    na, nb = a.x_update(), b.x_update()
-    assert list(na) == list(nb)
-
-
-@pytest.mark.parametrize("name", ["C2s", "C4s", "C2rs"])
-def test_pdl_launches_bit_identical(name):
-    """IFCTN_FLAG_PDL (programmatic dependent launch: kernels start early and wait in
-    griddepcontrol.wait) changes only launch timing, never results."""
-    from paper_2511_16358_b200 import IFCTN_FLAG_PDL
-    p = make_config(name)
-    a = make_solver(p, flags=IFCTN_FLAG_PDL)
-    b = make_solver(p)
-    for x in (a, b):
-        x.sweep(3)
-    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
-    assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
-
-
-@pytest.mark.timeout(120)
-@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C2", "C4"])
-def test_persistent_sweeps_bit_identical_to_launch_sequence(name):
-    """the persistent whole-sweep kernel (one cooperative launch for all
-    sweeps) runs the same op bodies with the same work split as the unfused launch sequence,
-    so factors and X agree bit for bit."""
-    from paper_2511_16358_b200 import IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_PERSISTENT, IFCTN_FLAG_PERSISTENT
-    p = make_config(name)
-    a = make_solver(p, flags=IFCTN_FLAG_PERSISTENT)
-    b = make_solver(p, flags=IFCTN_FLAG_NO_FUSE | IFCTN_FLAG_NO_PERSISTENT)
-    a.sweep(3)
-    b.sweep(3)
-    assert a.launch_count() == 1
-    assert np.array_equal(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy())
-    assert np.array_equal(a.factors().cpu().numpy(), b.factors().cpu().numpy())
-    assert a.objective() == b.objective()
 
 
 @pytest.mark.parametrize("name,sweeps", [("C1", 10), ("C2s", 20), ("C3s", 20), ("C4s", 20), ("C5s", 10),

@@ -406,6 +406,32 @@ def test_exact_recovery_C1_recipe():
     assert O.rse(p.truth, X) < 1e-10
 
 
+# ------------------------------------------------- init and RSE (hand values) ---
+
+def test_init_x_zeroes_unobserved_entries():
+    """X⁽⁰⁾ = P_Ω(O) (Alg. 1 initialisation; reading R7): entries off Ω are 0 even
+    when O carries (nonzero) values there; entries on Ω are O bit for bit (f64 and f32)."""
+    O64 = np.array([1.5, -2.0, 3.25, 7.0, -0.125], dtype=np.float64)
+    m = np.array([1, 0, 1, 0, 1], dtype=np.uint8)
+    X = O.init_x(O64, m)
+    assert X.tolist() == [1.5, 0.0, 3.25, 0.0, -0.125]
+    O32 = np.array([0.1, 9.0, -0.3], dtype=np.float32)
+    X = O.init_x(O32, np.array([0, 1, 1], np.uint8))
+    assert X[0] == 0.0 and X[1] == 9.0 and X[2] == float(np.float32(-0.3))
+
+
+def test_rse_denominator_is_the_truth_norm():
+    """RSE = ‖T − X‖_F / ‖T‖_F (reading R10).  T = [3, 4], X = [3, 0]: ‖T − X‖ = 4,
+    ‖T‖ = 5 → 0.8; the paper's printed ‖X‖ denominator would give 4/3 and a squared or
+    unsquared-numerator slip 16/25 or 16/5 — all separated by this hand value."""
+    T = np.array([3.0, 4.0])
+    X = np.array([3.0, 0.0])
+    assert O.rse(T, X) == 0.8
+    # exact recovery and the all-zero estimate
+    assert O.rse(T, T.copy()) == 0.0
+    assert O.rse(T, np.zeros(2)) == 1.0
+
+
 # ---------------------------------------------------------- paper-printed counts ---
 
 def test_storage_counts_golden():
