@@ -411,6 +411,8 @@ def run_ours(args):
         line["other_configs"] = other_configs(torch)
         line["rank_grid"] = rank_grid_extra(torch)
         line["mask_gen"] = mask_gen_extra(torch)
+        if p.name == "C5":
+            line["c5_shard8_rank0"] = shard_rank0_extra(torch, p, 8, k2_gbs)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if tdist is not None:
@@ -479,6 +481,32 @@ def other_configs(torch):
                                                     for k, v in met.items()},
                      "regime": "launch/latency-bound" if name == "C1" else "L2-resident"}
     return out
+
+
+def shard_rank0_extra(torch, p, world, full_k2_gbs):
+    """SURVEY §8(e) on one GPU: rank 0's context of the `world`-way C5 run (sharded along
+    mode 1 = API mode 0, 8 slices; stored with modes 0 and 1 swapped so fibres stay 64 long),
+    one profiled sweep with a no-op host all-reduce (one process).  The a2 pass over the
+    268 MB shard against the full tensor's per-pass GB/s."""
+    from paper_2511_16358_b200 import Solver
+    from paper_2511_16358_b200 import dist as D
+    sm, sb, se = D.shard_range(p.dims, world, 0)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    obs = D.shard_tensor(p.observed, p.dims, sm, sb, se)
+    d = D.make_dist(0, world, -1, host_allreduce=lambda a: None)
+    s = Solver(p.dims, p.ranks, dev(obs), dev(D.shard_tensor(p.mask, p.dims, sm, sb, se)),
+               dev(D.shard_factors(p.G0, p.dims, p.ranks, sm, sb, se)), rho=p.rho, dist=d)
+    s._dist_keep = d
+    s.profile_sweep()
+    prof = s.profile_sweep()
+    s.close()
+    k2, _, _, refill_ms, _ = split_profile(prof, p.N, world, sm)
+    n = obs.size
+    gbs = n * p.dtype.itemsize / (statistics.mean(k2) / 1e3) / 1e9
+    return {"shard_mode": sm, "slice": [sb, se], "entries": n, "a2_ms_mean": statistics.mean(k2),
+            "a2_ms_by_block": [round(v, 4) for v in k2], "a2_gbs": gbs,
+            "frac_of_full_c5_a2_gbs": gbs / full_k2_gbs,
+            "refill_gbs": n * (2 * p.dtype.itemsize + 1 / 8) / (refill_ms / 1e3) / 1e9}
 
 
 def rank_grid_extra(torch):

@@ -82,8 +82,12 @@ typedef struct {
     const void* nccl_unique_id; /* ncclUniqueId (128 bytes), identical on all ranks       */
     int rank;
     int world;
-    int shard_mode;             /* 0-based; -1 = the largest mode, the LAST on ties (keeps
-                                   mode 0, the fibre/lane mode, whole when it can)         */
+    int shard_mode;             /* 0-based; -1 = the largest mode, the first on ties
+                                   (SURVEY §8(e)).  When the shard mode is mode 0 (the
+                                   fibre/lane mode of the passes) and order ≥ 3, the library
+                                   stores the shard internally with mode 0 swapped for the
+                                   largest of modes 1..N-2, so fibres stay long; every
+                                   argument keeps the layout documented here.              */
     /* Optional: sum across ranks on the host instead of NCCL (several ranks driven from host
      * threads on one device in tests, or a custom transport).  Called synchronously with a
      * host buffer of `count` doubles that must be replaced by the element-wise sum over all

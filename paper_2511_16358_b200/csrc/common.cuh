@@ -248,7 +248,8 @@ struct PassParams {
     // ((vb·FR + r)·F + f), vb = b + nb0·kidx1.
     int64_t nb0;
     int64_t vf2_off, hres2_elems;  // tiled pass: resident H_{0,r0} block after H_{0,1}
-    int64_t h01_off, hres3_elems;  // fused pass: H_{0,1} (global offset; resident when tiled)
+    int64_t h01_off, hres3_elems;  // fused pass: H_{0,m} of the first block's pair {0,m}
+    int h01_mode;                  // (global offset; resident when tiled, m = 1), and m
     // tiled pass: scalar factors touching mode 1 (A: H_{1,q}, q fixed in the tile), r0 (B: the
     // sf_* lists) or both (C: H_{1,r0}, -1 when {1,r0} is the kept pair); value of an entry is
     // H[off + idx[fix]·mul + x·inc] with x = v (A) or i_{r0} (B)

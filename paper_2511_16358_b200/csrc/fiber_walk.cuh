@@ -522,9 +522,9 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
         __syncwarp();
         const int64_t ebase = (int64_t)C.fib * I1p;
         const T* hrun = hres + (HRES && has_fast ? ri0 * I1p : 0) + ebc;
-        T h01v[EPL];  // fused: the excluded pair's column H_{0,1}(·, i_1) completes t = M·H_{0,1}
+        T h01v[EPL];  // fused: the excluded pair's column H_{0,m}(·, i_m) completes t = M·H_{0,m}
         if constexpr (kFused) {
-            const T* hb = Hb + P.h01_off + (int64_t)idx(1) * I1p + eb;
+            const T* hb = Hb + P.h01_off + (int64_t)idx(P.h01_mode) * I1p + eb;
 #pragma unroll
             for (int e = 0; e < EPL; ++e) h01v[e] = ev[e] ? hb[e] : T(0);
         }

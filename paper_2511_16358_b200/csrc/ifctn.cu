@@ -82,6 +82,18 @@ struct Shape {
     int64_t part_elems = 0, max_bw = 0, ndelta = 0, groups_bound = 0;
     int64_t delta_off[MAXN][MAXN] = {};
     int64_t proj_elems = 0;  // multi-GPU projected Gram/RHS buffer (doubles)
+    // Internal mode order.  Everything above is in INTERNAL numbering: internal mode m is API
+    // mode perm[m].  The identity unless the shard mode is API mode 0 (the lane/fibre mode of
+    // every pass, which a shard would cut to I_0/W): then the two largest middle modes become
+    // internal modes 0 (lane) and 1 (run/tile mode), the rest follow in API order and the last
+    // mode stays last (bands stay the slowest mode), so each rank's passes see the long
+    // fibres and runs of the unsharded tensor.  The block order, the factor layout and every
+    // dense tensor at the boundary stay in API numbering (see Solver).
+    int perm[MAXN] = {};
+    bool permuted = false;
+    int shard_api = 0;          // shard mode in API numbering
+    int64_t eld[MAXN] = {};     // API-order local dims
+    int64_t egoff[MAXN][MAXN] = {};  // API-order factor offsets (ABI layout)
 
     int R(int p, int q) const { return ranks[p * N + q]; }
 };
@@ -128,10 +140,10 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
         s.world = dist->world;
         s.rank = dist->rank;
         int sm = dist->shard_mode;
-        if (sm < 0) {  // the largest mode; ties go to the highest index, which keeps the
-            sm = 0;    // fibre mode (mode 1, the lane dimension of every pass) whole
+        if (sm < 0) {  // the largest mode, the first on ties
+            sm = 0;
             for (int m = 1; m < order; ++m)
-                if (dims[m] >= dims[sm]) sm = m;
+                if (dims[m] > dims[sm]) sm = m;
         }
         if (sm >= order) fail(IFCTN_E_ARG, "shard_mode out of range");
         if (dims[sm] < dist->world) fail(IFCTN_E_SHAPE, "shard mode smaller than the world size");
@@ -153,6 +165,51 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
     shard_range_of(s.dims[s.shard], s.world, s.rank, &s.sbegin, &s.send);
     for (int m = 0; m < order; ++m) s.ld[m] = s.dims[m];
     s.ld[s.shard] = s.send - s.sbegin;
+    // API-order views, then the internal mode order (see Shape::perm)
+    s.shard_api = s.shard;
+    for (int m = 0; m < order; ++m) {
+        s.eld[m] = s.ld[m];
+        s.perm[m] = m;
+    }
+    {
+        int64_t off = 0;
+        for (int k = 0; k < order; ++k)
+            for (int i = 0; i < order; ++i) {
+                if (i == k) continue;
+                s.egoff[k][i] = off;
+                off += (int64_t)s.R(k, i) * s.eld[k];
+            }
+    }
+    if (s.dpath && s.shard == 0 && order >= 3) {
+        // internal order: [m1, m2, the other modes ascending, N-1] with m1, m2 the largest of
+        // the middle modes 1..N-2 (first on ties) when longer than the shard slice; m2 makes
+        // internal mode 1 (the run / tile mode of the passes, fibre stride 1) long as well
+        int m1 = 1;
+        for (int q = 2; q <= order - 2; ++q)
+            if (s.eld[q] > s.eld[m1]) m1 = q;
+        if (s.eld[m1] > s.eld[0]) {
+            int m2 = -1;
+            for (int q = 1; q <= order - 2; ++q)
+                if (q != m1 && (m2 < 0 || s.eld[q] > s.eld[m2])) m2 = q;
+            if (m2 >= 0 && !(s.eld[m2] > s.eld[0])) m2 = -1;
+            int t = 0;
+            s.perm[t++] = m1;
+            if (m2 >= 0) s.perm[t++] = m2;
+            for (int q = 0; q < order - 1; ++q)
+                if (q != m1 && q != m2) s.perm[t++] = q;
+            s.perm[t++] = order - 1;
+            s.permuted = true;
+            int32_t rk[MAXN * MAXN];
+            for (int p = 0; p < order; ++p)
+                for (int q = 0; q < order; ++q) rk[p * order + q] = s.ranks[s.perm[p] * order + s.perm[q]];
+            for (int p = 0; p < order * order; ++p) s.ranks[p] = rk[p];
+            for (int p = 0; p < order; ++p) {
+                s.dims[p] = dims[s.perm[p]];
+                s.ld[p] = s.eld[s.perm[p]];
+                if (s.perm[p] == 0) s.shard = p;  // internal index of API mode 0
+            }
+        }
+    }
 
     s.I1 = s.ld[0];
     s.I1p = align_up(s.I1, s.vw);
@@ -227,9 +284,16 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
             }
             pmax = std::max(pmax, slots * Lv);
             bw = std::max(bw, s.ld[i] * s.ld[k]);
-            s.delta_off[k][i] = nd;
-            nd += s.ld[k];
         }
+    // ΔG² slots per block, the shard-mode chains LAST: the replicated entries then sit at the
+    // same positions on every rank (finalize_norms sums them in the same order everywhere)
+    for (int pass = 0; pass < 2; ++pass)
+        for (int k = 0; k < order; ++k)
+            for (int i = 0; i < order; ++i) {
+                if (i == k || (pass == 0) == (s.dpath && k == s.shard)) continue;
+                s.delta_off[k][i] = nd;
+                nd += s.ld[k];
+            }
     s.part_elems = align_up(pmax, s.vw);
     s.max_bw = bw;
     s.ndelta = nd;
@@ -561,7 +625,10 @@ struct Solver : SolverBase {
         p.nouter = N - 1;
         for (int m = 0; m < N; ++m) p.fstride[m] = s.fstride[m];
         const bool contract = (mode == PASS_KEPT1 || mode == PASS_RED1 || mode == PASS_FUSED);
-        if (mode == PASS_FUSED) p.h01_off = s.hoff[0][1];
+        if (mode == PASS_FUSED) {  // block (0,m) or (m,0): the refill's t needs H_{0,m}
+            p.h01_mode = std::max(k, i);
+            p.h01_off = s.hoff[0][p.h01_mode];
+        }
         // kept outer modes (ascending), reduced outer modes
         std::vector<int> kept, red;
         for (int m = 1; m < N; ++m) {
@@ -569,7 +636,9 @@ struct Solver : SolverBase {
             else red.push_back(m);
         }
         // odometer order: r0 = the largest reduced mode (ties: lowest), then ascending
-        // (v-blocked: ascending; the fast index is the kept mode 1)
+        // (v-blocked: ascending; the fast index is the kept mode 1).  Measured on a C5 shard:
+        // preferring the contiguous mode 1 when it is short (8 fibres, 2 KB runs) doubled the
+        // pass time (runs too short for the per-run setup) — keep the long runs.
         if (!red.empty() && !vblk) {
             int best = 0;
             for (size_t t = 1; t < red.size(); ++t)
@@ -774,9 +843,11 @@ struct Solver : SolverBase {
     void plan() {
         const int N = s.N;
         blocks.clear();
-        for (int k = 0; k < N; ++k)
-            for (int i = 0; i < N; ++i) {
-                if (i == k) continue;
+        // Gauss–Seidel order k↑, i↑ in API numbering (reading R6), blocks in internal numbering
+        for (int ke = 0; ke < N; ++ke)
+            for (int ie = 0; ie < N; ++ie) {
+                if (ie == ke) continue;
+                const int k = int_mode(ke), i = int_mode(ie);
                 BlockPlan<T> b;
                 b.k = k;
                 b.i = i;
@@ -864,14 +935,15 @@ struct Solver : SolverBase {
         nlaunch_sweep = 3 * (int64_t)blocks.size() + 2;
         // ΔG² of the shard-mode chains (local columns) is summed across ranks; the rest is
         // replicated: delta layout is block order, so blocks (s, ·) are one contiguous range
-        sh_off = s.dpath ? s.delta_off[s.shard][s.shard == 0 ? 1 : 0] : 0;
+        sh_off = s.dpath ? s.delta_off[s.shard][s.shard == 0 ? 1 : 0] : 0;  // the last range
         sh_len = s.dpath ? (int64_t)(s.N - 1) * s.ld[s.shard] : 0;
         // fused a5(s) + a2 of block (0,1) of sweep s+1 (same G, X read and written once)
         has_fused = false;
-        if (!(flags & kFlagNoFuse) && blocks[0].k == 0 && blocks[0].i == 1) {
+        // (the first block keeps the lane mode 0: API (0,1), or its image under Shape::perm)
+        if (!(flags & kFlagNoFuse) && std::min(blocks[0].k, blocks[0].i) == 0) {
             const BlockPlan<T>& b0 = blocks[0];
-            const bool vb = b0.vblk && s.I1p * s.ld[1] * s.esize <= 32 * 1024;
-            fused = make_pass(PASS_FUSED, 0, 1, vb);
+            const bool vb = b0.vblk && std::max(b0.k, b0.i) == 1 && s.I1p * s.ld[1] * s.esize <= 32 * 1024;
+            fused = make_pass(PASS_FUSED, b0.k, b0.i, vb);
             fused_red = b0.red;
             fused_red.FR = fused.p.FR;
             fused_red.L = fused.p.L;
@@ -976,6 +1048,67 @@ struct Solver : SolverBase {
         if (traced) enqueue_trace_push();
     }
 
+    // Dense tensor of this rank's shard between the API linearisation and the internal mode
+    // order (only when s.permuted).  to_internal: src API-dense → dst internal-dense; else
+    // src internal-dense → dst API-dense.
+    template <typename E>
+    void permute_api(const E* src, E* dst, bool to_internal) {
+        const int N = s.N;
+        PermDesc d{};
+        d.N = N;
+        // source mode q ↔ its extent, source stride and destination stride
+        int64_t dstride_api[MAXN], dstride_int[MAXN];
+        int64_t acc = 1;
+        for (int q = 0; q < N; ++q) {  // API-dense strides
+            dstride_api[q] = acc;
+            acc *= s.eld[q];
+        }
+        acc = 1;
+        for (int t = 0; t < N; ++t) {  // internal-dense strides
+            dstride_int[t] = acc;
+            acc *= s.ld[t];
+        }
+        for (int q = 0; q < N; ++q) {
+            if (to_internal) {  // source = API mode q = internal mode int_mode(q)
+                d.dim[q] = s.eld[q];
+                d.sstr[q] = dstride_api[q];
+                d.dstr[q] = dstride_int[int_mode(q)];
+            } else {            // source = internal mode q = API mode perm[q]
+                d.dim[q] = s.ld[q];
+                d.sstr[q] = dstride_int[q];
+                d.dstr[q] = dstride_api[s.perm[q]];
+            }
+        }
+        d.ym = to_internal ? s.perm[0] : int_mode(0);  // the source mode fastest in dst
+        int64_t nb = 1;
+        for (int q = 1; q < N; ++q)
+            if (q != d.ym) nb *= d.dim[q];
+        const int64_t tiles = ((d.dim[0] + kPermTile - 1) / kPermTile) * ((d.dim[d.ym] + kPermTile - 1) / kPermTile);
+        const dim3 grid((unsigned)tiles, (unsigned)std::min<int64_t>(nb, 65535));
+        permute_modes<E><<<grid, kPermTile * 8, 0, st>>>(src, dst, d);
+        CU(cudaGetLastError());
+    }
+    // internal mode of API mode m (perm is an involution, but do not rely on it)
+    int int_mode(int m) const {
+        for (int q = 0; q < s.N; ++q)
+            if (s.perm[q] == m) return q;
+        return m;
+    }
+    // factor chains between the ABI layout (API block order) and the internal layout
+    void copy_factors(const T* src, T* dst, bool to_internal, cudaMemcpyKind kind) {
+        if (!s.permuted) {
+            CU(cudaMemcpyAsync(dst, src, (size_t)s.gtotal * s.esize, kind, st));
+            return;
+        }
+        for (int k = 0; k < s.N; ++k)
+            for (int i = 0; i < s.N; ++i) {
+                if (i == k) continue;
+                const int64_t eo = s.egoff[k][i], io = s.goff[int_mode(k)][int_mode(i)];
+                const size_t bytes = (size_t)s.R(int_mode(k), int_mode(i)) * s.eld[k] * s.esize;
+                CU(cudaMemcpyAsync(to_internal ? dst + io : dst + eo, to_internal ? src + eo : src + io, bytes, kind, st));
+            }
+    }
+
     void init(const void* observed, const uint8_t* mask, const void* G0, void* workspace,
               size_t wbytes, cudaStream_t stream) {
         user_stream = stream;
@@ -1022,10 +1155,13 @@ struct Solver : SolverBase {
         // inputs → device (temporary copies when the caller passed host memory)
         const size_t obytes = (size_t)s.nloc * s.esize;
         // pinned host inputs are read in place by pack_input (one pass over the host link)
-        const T* dobs = (const T*)device_view(observed);
-        const uint8_t* dmask = (const uint8_t*)device_view(mask);
+        // (a mode swap reads transposed: pinned host inputs are staged by DMA first)
+        const T* dobs = (const T*)(s.permuted ? (is_device_ptr(observed) ? observed : nullptr) : device_view(observed));
+        const uint8_t* dmask = (const uint8_t*)(s.permuted ? (is_device_ptr(mask) ? mask : nullptr) : device_view(mask));
         void* tmp_o = nullptr;
         void* tmp_m = nullptr;
+        void* tmp_po = nullptr;
+        void* tmp_pm = nullptr;
         if (!dobs) {
             CU(cudaMallocAsync(&tmp_o, obytes, st));
             CU(cudaMemcpyAsync(tmp_o, observed, obytes, cudaMemcpyHostToDevice, st));
@@ -1036,14 +1172,21 @@ struct Solver : SolverBase {
             CU(cudaMemcpyAsync(tmp_m, mask, (size_t)s.nloc, cudaMemcpyHostToDevice, st));
             dmask = (const uint8_t*)tmp_m;
         }
+        if (s.permuted) {  // API order → internal mode order, then the usual packing
+            CU(cudaMallocAsync(&tmp_po, obytes, st));
+            CU(cudaMallocAsync(&tmp_pm, (size_t)s.nloc, st));
+            permute_api<T>(dobs, (T*)tmp_po, true);
+            permute_api<uint8_t>(dmask, (uint8_t*)tmp_pm, true);
+            dobs = (const T*)tmp_po;
+            dmask = (const uint8_t*)tmp_pm;
+        }
         const int64_t nw = (s.npad + 31) / 32;
         pack_input<T><<<(unsigned)std::min<int64_t>((nw + 7) / 8, 64 * nsm), 256, 0, st>>>(
             dobs, dmask, s.I1, s.I1p, s.npad, (flags & IFCTN_FLAG_X_FULL) ? 1 : 0, X, bits);
         CU(cudaGetLastError());
-        CU(cudaMemcpyAsync(G, G0, (size_t)s.gtotal * s.esize,
-                           is_device_ptr(G0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-        if (tmp_o) CU(cudaFreeAsync(tmp_o, st));
-        if (tmp_m) CU(cudaFreeAsync(tmp_m, st));
+        copy_factors((const T*)G0, G, true, is_device_ptr(G0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+        for (void* t : {tmp_o, tmp_m, tmp_po, tmp_pm})
+            if (t) CU(cudaFreeAsync(t, st));
         {
             std::vector<T> ones((size_t)s.I1p, T(1));
             CU(cudaMemcpyAsync(H + s.ones_off, ones.data(), ones.size() * sizeof(T), cudaMemcpyHostToDevice, st));
@@ -1226,7 +1369,34 @@ struct Solver : SolverBase {
         begin();
         const size_t bytes = (size_t)s.nloc * s.esize;
         const bool host = !is_device_ptr(out);
-        if (what == IFCTN_X && s.I1 == s.I1p) {
+        if (s.permuted) {  // internal mode order → API order
+            T* dout = host ? nullptr : (T*)out;
+            void* tmp = nullptr;
+            void* tmpm = nullptr;
+            if (!dout) {
+                CU(cudaMallocAsync(&tmp, bytes, st));
+                dout = (T*)tmp;
+            }
+            const T* dense = X;  // internal-dense source
+            if (what == IFCTN_X) {
+                if (s.I1 != s.I1p) {
+                    CU(cudaMallocAsync(&tmpm, bytes, st));
+                    unpack_x<T><<<(unsigned)((s.nloc + 255) / 256), 256, 0, st>>>(X, s.I1, s.I1p, s.nloc, (T*)tmpm);
+                    CU(cudaGetLastError());
+                    dense = (const T*)tmpm;
+                }
+            } else {
+                CU(cudaMallocAsync(&tmpm, bytes, st));
+                PassParams<T> p = model.p;
+                p.out = (T*)tmpm;
+                launch(model.fn, model.grid, dim3(kPassThreads), model.smem, p);
+                dense = (const T*)tmpm;
+            }
+            permute_api<T>(dense, dout, false);
+            if (tmp) CU(cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, st));
+            for (void* t : {tmp, tmpm})
+                if (t) CU(cudaFreeAsync(t, st));
+        } else if (what == IFCTN_X && s.I1 == s.I1p) {
             // unpadded fibres: X already is the natural layout, one copy
             CU(cudaMemcpyAsync(out, X, bytes, cudaMemcpyDefault, st));
         } else {
@@ -1258,29 +1428,43 @@ struct Solver : SolverBase {
         if (!out) fail(IFCTN_E_ARG, "out must not be NULL");
         begin();
         const bool dev = is_device_ptr(out);
-        CU(cudaMemcpyAsync(out, G, (size_t)s.gtotal * s.esize, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        copy_factors(G, (T*)out, false, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
         if (!dev) CU(cudaStreamSynchronize(st));
         end();
+    }
+
+    // A device view of a truth tensor (API layout, host or device) in the internal mode order
+    // (dense, leading dim I1); temporaries in *tmp/*tmpp, freed by the caller on st.
+    const T* truth_view(const void* truth, void** tmp, void** tmpp) {
+        const size_t bytes = (size_t)s.nloc * s.esize;
+        const T* dt = (const T*)(s.permuted ? (is_device_ptr(truth) ? truth : nullptr) : device_view(truth));
+        if (!dt) {
+            CU(cudaMallocAsync(tmp, bytes, st));
+            CU(cudaMemcpyAsync(*tmp, truth, bytes, cudaMemcpyHostToDevice, st));
+            dt = (const T*)*tmp;
+        }
+        if (s.permuted) {
+            CU(cudaMallocAsync(tmpp, bytes, st));
+            permute_api<T>(dt, (T*)*tmpp, true);
+            dt = (const T*)*tmpp;
+        }
+        return dt;
     }
 
     double rse(const void* truth) override {
         if (!truth) fail(IFCTN_E_ARG, "truth must not be NULL");
         begin();
-        const size_t bytes = (size_t)s.nloc * s.esize;
-        const T* dt = (const T*)device_view(truth);
         void* tmp = nullptr;
-        if (!dt) {
-            CU(cudaMallocAsync(&tmp, bytes, st));
-            CU(cudaMemcpyAsync(tmp, truth, bytes, cudaMemcpyHostToDevice, st));
-            dt = (const T*)tmp;
-        }
+        void* tmpp = nullptr;
+        const T* dt = truth_view(truth, &tmp, &tmpp);
         const int nb = 1024;
         rse_partial<T><<<nb, 256, 0, st>>>(dt, X, s.I1, s.I1p, s.nloc, rsep);
         sum_pairs<<<1, 32, 0, st>>>(rsep, nb, rsep + 2 * nb);
         CU(cudaGetLastError());
         allreduce_dev(rsep + 2 * nb, 2);
         CU(cudaMemcpyAsync(hscal + 8, rsep + 2 * nb, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        if (tmp) CU(cudaFreeAsync(tmp, st));
+        for (void* t : {tmp, tmpp})
+            if (t) CU(cudaFreeAsync(t, st));
         CU(cudaStreamSynchronize(st));
         end();
         const double num = hscal[8], den = hscal[9];
@@ -1316,13 +1500,9 @@ struct Solver : SolverBase {
         double* spart = part + bl * chunks * 5;
         double* red = spart + bl * ntiles;
         double* fin = red + nred;
-        const T* dt = (const T*)device_view(truth);
         void* tmpt = nullptr;
-        if (!dt) {
-            CU(cudaMallocAsync(&tmpt, (size_t)s.nloc * s.esize, st));
-            CU(cudaMemcpyAsync(tmpt, truth, (size_t)s.nloc * s.esize, cudaMemcpyHostToDevice, st));
-            dt = (const T*)tmpt;
-        }
+        void* tmptp = nullptr;
+        const T* dt = truth_view(truth, &tmpt, &tmptp);
         metric_sums<T><<<dim3((unsigned)chunks, (unsigned)bl), kMetThreads, 0, st>>>(dt, X, bits, s.I1, s.I1p, fpb,
                                                                                       chunk, part);
         CU(cudaGetLastError());
@@ -1342,7 +1522,8 @@ struct Solver : SolverBase {
         metric_finish<<<1, 1, 0, st>>>(red, IN, band_n, ssim_ok ? nwin * (double)IN : 0.0, fin);
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(hscal + 8, fin, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        if (tmpt) CU(cudaFreeAsync(tmpt, st));
+        for (void* t : {tmpt, tmptp})
+            if (t) CU(cudaFreeAsync(t, st));
         CU(cudaFreeAsync(tmp, st));
         CU(cudaStreamSynchronize(st));
         end();
@@ -1367,8 +1548,10 @@ struct Solver : SolverBase {
         return hscal[6];
     }
 
-    const BlockPlan<T>& find_block(int k, int i) {
+    const BlockPlan<T>& find_block(int k, int i) {  // k, i: API numbering
         if (k < 0 || i < 0 || k >= s.N || i >= s.N || k == i) fail(IFCTN_E_ARG, "block (k,i) out of range");
+        k = int_mode(k);  // API → internal numbering
+        i = int_mode(i);
         for (const auto& b : blocks)
             if (b.k == k && b.i == i) return b;
         fail(IFCTN_E_ARG, "block not found");
@@ -1380,7 +1563,7 @@ struct Solver : SolverBase {
         const auto& b = find_block(k, i);
         begin();
         enqueue_contract(b, true);
-        const size_t bytes = (size_t)(s.ld[i] * s.ld[k]) * sizeof(double);
+        const size_t bytes = (size_t)(s.eld[i] * s.eld[k]) * sizeof(double);
         CU(cudaMemcpyAsync(bo, beta, bytes, cudaMemcpyDefault, st));
         CU(cudaMemcpyAsync(wo, omega, bytes, cudaMemcpyDefault, st));
         CU(cudaStreamSynchronize(st));
@@ -1475,7 +1658,7 @@ ifctn_status ifctn_shard_range(int order, const int64_t* dims, const ifctn_dist*
         std::vector<int32_t> ranks(order * order, 1);
         for (int m = 0; m < order; ++m) ranks[m * order + m] = 0;
         ifctn::Shape s = ifctn::make_shape(order, dims, ranks.data(), IFCTN_F32, dist);
-        if (shard_mode) *shard_mode = s.shard;
+        if (shard_mode) *shard_mode = s.shard_api;
         if (begin) *begin = s.sbegin;
         if (end) *end = s.send;
     });

@@ -778,6 +778,49 @@ __global__ void pack_input(const T* obs, const uint8_t* mask, int64_t I1, int64_
     }
 }
 
+// Mode permutation between the API linearisation and the internal mode order (Shape::perm):
+// a batched 32×32 shared-memory transpose of the source's fastest mode (x) and the source
+// mode that is fastest in the destination (y); every other mode is a batch index (decoded per
+// tile).  Dense tensors on both sides; src mode q has extent dim[q], stride sstr[q] in the
+// source and dstr[q] in the destination.  Coalesced reads along x and writes along y.
+constexpr int kPermTile = 32;
+struct PermDesc {
+    int N, ym;
+    int64_t dim[MAXN], sstr[MAXN], dstr[MAXN];
+};
+template <typename E>
+__global__ void __launch_bounds__(kPermTile * 8) permute_modes(const E* __restrict__ src, E* __restrict__ dst,
+                                                               const PermDesc d) {
+    __shared__ E tile[kPermTile][kPermTile + 1];
+    const int64_t X = d.dim[0], Y = d.dim[d.ym];
+    const int64_t tx_n = (X + kPermTile - 1) / kPermTile;
+    const int64_t x0 = (int64_t)(blockIdx.x % tx_n) * kPermTile, y0 = (int64_t)(blockIdx.x / tx_n) * kPermTile;
+    int64_t nb = 1;
+    for (int q = 1; q < d.N; ++q)
+        if (q != d.ym) nb *= d.dim[q];
+    const int tx = threadIdx.x % kPermTile, ty = threadIdx.x / kPermTile;
+    for (int64_t bt = blockIdx.y; bt < nb; bt += gridDim.y) {
+        int64_t r = bt, so = 0, dof = 0;
+        for (int q = 1; q < d.N; ++q) {
+            if (q == d.ym) continue;
+            const int64_t c = r % d.dim[q];
+            r /= d.dim[q];
+            so += c * d.sstr[q];
+            dof += c * d.dstr[q];
+        }
+        __syncthreads();
+        for (int y = ty; y < kPermTile; y += 8) {
+            const int64_t xx = x0 + tx, yy = y0 + y;
+            if (xx < X && yy < Y) tile[y][tx] = src[so + xx + yy * d.sstr[d.ym]];
+        }
+        __syncthreads();
+        for (int y = ty; y < kPermTile; y += 8) {
+            const int64_t yy = y0 + tx, xx = x0 + y;
+            if (xx < X && yy < Y) dst[dof + yy + xx * d.dstr[0]] = tile[tx][y];
+        }
+    }
+}
+
 template <typename T>
 __global__ void unpack_x(const T* X, int64_t I1, int64_t I1p, int64_t n, T* out) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

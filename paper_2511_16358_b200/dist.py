@@ -18,7 +18,7 @@ from . import _abi
 
 def shard_range(dims, world: int, rank: int, shard_mode: int = -1):
     """(shard mode, begin, end) of this rank's slice — the library's own rule (reading R21:
-    ⌈I_s/W⌉ slices first, then ⌊I_s/W⌋; shard mode = largest, the last on ties)."""
+    ⌈I_s/W⌉ slices first, then ⌊I_s/W⌋; shard mode = largest, the first on ties)."""
     d = _abi.ifctn_dist(None, rank, world, shard_mode)
     return _abi.ifctn_shard_range(len(dims), dims, d if world > 1 else None)
 

@@ -96,7 +96,8 @@ def test_create_validates_before_device_work(abi):
 
 
 def test_shard_ranges(abi):
-    """Reading R21: ⌈I/W⌉ slices first; shard mode = largest (the last on ties)."""
+    """Reading R21: ⌈I/W⌉ slices first; shard mode = largest, the first on ties (SURVEY §8(e):
+    C5 shards along mode 1 = API mode 0)."""
     dims = (214, 61, 144, 4)
     sizes = []
     for r in range(8):
@@ -110,8 +111,9 @@ def test_shard_ranges(abi):
     assert sizes == [27] * 6 + [26] * 2 and prev_e == 214
     d = abi.ifctn_dist(None, 1, 8, -1)
     assert abi.ifctn_shard_range(4, (144, 176, 3, 50), d) == (1, 22, 44)
-    assert abi.ifctn_shard_range(3, (64, 64, 32), abi.ifctn_dist(None, 0, 2, -1))[0] == 1
-    assert abi.ifctn_shard_range(5, (64, 64, 64, 64, 32), abi.ifctn_dist(None, 0, 8, -1)) == (3, 0, 8)
+    assert abi.ifctn_shard_range(3, (64, 64, 32), abi.ifctn_dist(None, 0, 2, -1))[0] == 0
+    assert abi.ifctn_shard_range(3, (32, 64, 64), abi.ifctn_dist(None, 0, 2, -1))[0] == 1
+    assert abi.ifctn_shard_range(5, (64, 64, 64, 64, 32), abi.ifctn_dist(None, 0, 8, -1)) == (0, 0, 8)
     assert abi.ifctn_shard_range(3, (8, 8, 8), None) == (0, 0, 8)
 
 
