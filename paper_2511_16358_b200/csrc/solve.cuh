@@ -359,59 +359,89 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
 // ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------
 // Same mathematics as block_solve (Eq. 8) with the rank a runtime value ≤ 64.
 // One CTA (256 threads) per column j:
-//   * G_{i,k} is staged in shared memory in tiles of `ta` columns a — normally all of it at
-//     once (one round of loads in flight), reused by the H refresh;
-//   * Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ: task = (4×4 tile of the upper triangle,
-//     a-residue h mod KS), KS = the a-split that fills the CTA; the KS partial tiles are
-//     added into the Gram in h order (fixed order, deterministic); rhs_j alongside;
-//   * warp 0: + ρI, ρ c_old, Cholesky (one column per step, lanes own rows, the pivot column
-//     scaled after the trailing update, inverse pivots kept on the diagonal), forward/back
-//     substitution, the column and ‖Δc‖²;
+//   * G_{i,k} is staged in shared memory as fp64 in tiles of `ta` columns a — normally all of
+//     it at once; the loads of a batch are all in flight before the stores; reused by the H
+//     refresh;
+//   * Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ and rhs_j = G_{i,k} β(:,j) as register tiles:
+//     task = (4×4 tile of the Gram upper triangle, or a 4-row tile of the rhs; a-residue h mod
+//     KS), KS = the a-split that fills the CTA; the KS partial tiles are added in h order
+//     (fixed order, deterministic);
+//   * warp 0: + ρI, ρ c_old, then a left-looking (Crout) Cholesky: column c of L is one
+//     round of independent length-c dot products (lane l owns rows l, l+32; four partial
+//     sums), the pivot's 1/√d is broadcast by shuffle — one dependent step per column, no
+//     trailing-update chain and no CTA barriers; forward/back substitution; ‖Δc‖²;
 //   * row j of H_{k,i} (8 threads per a).
 constexpr int kBigThreads = 256;
-constexpr int kBigEnt = 9;  // ⌈64·65/2 / 256⌉ lower-triangle entries per thread
 
 __host__ __device__ inline int big_solve_rp(int R) { return (R + 3) & ~3; }
-// shared memory: G tile (ta·R + Rp values of T, 16-B rounded) + fp64 [Gram Rp², ω, β (ta each),
+__host__ __device__ inline int big_solve_lda(int R) { return big_solve_rp(R) + 1; }  // odd: rows hit different banks
+// shared memory: G tile (ta·R + Rp doubles) + fp64 [A: Rp rows of lda, ω, β (ta each),
 // rhs, c, c_old (Rp each)]
-__host__ __device__ inline size_t big_solve_smem(int R, int ta, int esize) {
+__host__ __device__ inline size_t big_solve_smem(int R, int ta, int /*esize*/) {
     const int Rp = big_solve_rp(R);
-    const size_t g = (((size_t)ta * R + Rp) * esize + 15) & ~(size_t)15;
-    return g + sizeof(double) * ((size_t)Rp * Rp + 2 * (size_t)ta + 3 * (size_t)Rp);
+    return sizeof(double) * ((size_t)ta * R + Rp + (size_t)Rp * big_solve_lda(R) + 2 * (size_t)ta + 3 * (size_t)Rp);
 }
 
+#ifdef IFCTN_EXP_PHASE_CLOCKS  // diagnosis builds only: per-phase clocks of CTA 0
+#define PHASE_CLK(q) \
+    if (j == 0 && threadIdx.x == 0) clk[q] = clock64();
+#else
+#define PHASE_CLK(q)
+#endif
 template <typename T, int SM>
-__device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, int64_t j, double* bsm, int* okp,
-                                                     double* colb /*2·64*/, double* dinvp) {
-    const int R = P.R, Rp = big_solve_rp(R), TA = P.ta;
+__device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, int64_t j, double* bsm, int* okp) {
+#ifdef IFCTN_EXP_PHASE_CLOCKS
+    long long clk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    PHASE_CLK(0);
+    const int R = P.R, Rp = big_solve_rp(R), LDA = big_solve_lda(R), TA = P.ta;
     const int NG = R * (R + 1) / 2, NA = NG + R;
-    T* gs = reinterpret_cast<T*>(bsm);  // G_{i,k}(:, a0 .. a0+ta), row stride R
-    double* A = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(bsm) +
-                                          ((((size_t)TA * R + Rp) * sizeof(T) + 15) & ~(size_t)15));
-    double* om = A + Rp * Rp;        // ω(a, j)
-    double* be = om + TA;            // β(a, j)
+    double* gs = bsm;                      // G_{i,k}(:, a0 .. a0+ta) as fp64, row stride R
+    double* A = gs + (size_t)TA * R + Rp;  // Gram (row-major, lda)
+    double* om = A + (size_t)Rp * LDA;     // ω(a, j)
+    double* be = om + TA;                  // β(a, j)
     double* rhs = be + TA;
     double* cv = rhs + Rp;
     double* cold = cv + Rp;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int nt = Rp / 4;
-    const int ntiles = nt * (nt + 1) / 2;
-    const int KS = max(1, min(8, nthr / ntiles));   // a-split per tile
-    const int task_t = tid % ntiles, task_h = tid / ntiles;
+    const int ntg = nt * (nt + 1) / 2;     // Gram tiles; then nt rhs tiles
+    const int ntasks = ntg + nt;
+    const int KS = max(1, min(8, nthr / ntasks));   // a-split per tile
+    const int task_t = tid % ntasks, task_h = tid / ntasks;
     const bool has_task = task_h < KS;
+    const bool is_rhs = task_t >= ntg;
     const bool one_tile = (int64_t)TA >= P.Ii;
     int tr = 0, ts = 0;
     if (has_task) {
-        int q = task_t;
-        while (q >= nt - tr) {
-            q -= nt - tr;
-            ++tr;
+        if (is_rhs) {
+            tr = task_t - ntg;
+        } else {
+            int q = task_t;
+            while (q >= nt - tr) {
+                q -= nt - tr;
+                ++tr;
+            }
+            ts = tr + q;
         }
-        ts = tr + q;
     }
     auto stage = [&](int64_t a0, int na) {
-        for (int e = tid; e < na * R; e += nthr) gs[e] = P.Gik[a0 * R + e];
-        for (int e = na * R + tid; e < na * R + Rp; e += nthr) gs[e] = T(0);  // 4-wide over-read
+        const T* src = P.Gik + a0 * R;
+        const int n = na * R;
+        for (int base = 0; base < n; base += 8 * nthr) {
+            T v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = base + u * nthr + tid;
+                v[u] = e < n ? src[e] : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = base + u * nthr + tid;
+                if (e < n) gs[e] = (double)v[u];
+            }
+        }
+        for (int e = n + tid; e < n + Rp; e += nthr) gs[e] = 0.0;  // 4-wide over-read
     };
     if constexpr (SM != SOLVE_FROM_PROJ) {
         double acc[4][4];
@@ -419,54 +449,63 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-        double racc = 0.0;
         for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
             const int na = (int)min((int64_t)TA, P.Ii - a0);
             __syncthreads();
             stage(a0, na);
+            PHASE_CLK(6);
             for (int a = tid; a < na; a += nthr) {
                 om[a] = P.omega[j * P.Ii + a0 + a];
                 be[a] = P.beta[j * P.Ii + a0 + a];
             }
             __syncthreads();
+            PHASE_CLK(7);
             if (has_task) {
-                for (int a = task_h; a < na; a += KS) {
-                    const double w = om[a];
-                    const T* gr = gs + a * R + 4 * tr;
-                    const T* gc = gs + a * R + 4 * ts;
-                    const double r0 = w * (double)gr[0], r1 = w * (double)gr[1], r2 = w * (double)gr[2],
-                                 r3 = w * (double)gr[3];
-                    const double c0 = (double)gc[0], c1 = (double)gc[1], c2 = (double)gc[2], c3 = (double)gc[3];
-                    acc[0][0] = fma(r0, c0, acc[0][0]); acc[0][1] = fma(r0, c1, acc[0][1]);
-                    acc[0][2] = fma(r0, c2, acc[0][2]); acc[0][3] = fma(r0, c3, acc[0][3]);
-                    acc[1][0] = fma(r1, c0, acc[1][0]); acc[1][1] = fma(r1, c1, acc[1][1]);
-                    acc[1][2] = fma(r1, c2, acc[1][2]); acc[1][3] = fma(r1, c3, acc[1][3]);
-                    acc[2][0] = fma(r2, c0, acc[2][0]); acc[2][1] = fma(r2, c1, acc[2][1]);
-                    acc[2][2] = fma(r2, c2, acc[2][2]); acc[2][3] = fma(r2, c3, acc[2][3]);
-                    acc[3][0] = fma(r3, c0, acc[3][0]); acc[3][1] = fma(r3, c1, acc[3][1]);
-                    acc[3][2] = fma(r3, c2, acc[3][2]); acc[3][3] = fma(r3, c3, acc[3][3]);
+                if (is_rhs) {
+                    for (int a = task_h; a < na; a += KS) {
+                        const double b = be[a];
+                        const double* gr = gs + a * R + 4 * tr;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[u][0] = fma(b, gr[u], acc[u][0]);
+                    }
+                } else {
+                    for (int a = task_h; a < na; a += KS) {
+                        const double w = om[a];
+                        const double* gr = gs + a * R + 4 * tr;
+                        const double* gc = gs + a * R + 4 * ts;
+                        const double r0 = w * gr[0], r1 = w * gr[1], r2 = w * gr[2], r3 = w * gr[3];
+                        const double c0 = gc[0], c1 = gc[1], c2 = gc[2], c3 = gc[3];
+                        acc[0][0] = fma(r0, c0, acc[0][0]); acc[0][1] = fma(r0, c1, acc[0][1]);
+                        acc[0][2] = fma(r0, c2, acc[0][2]); acc[0][3] = fma(r0, c3, acc[0][3]);
+                        acc[1][0] = fma(r1, c0, acc[1][0]); acc[1][1] = fma(r1, c1, acc[1][1]);
+                        acc[1][2] = fma(r1, c2, acc[1][2]); acc[1][3] = fma(r1, c3, acc[1][3]);
+                        acc[2][0] = fma(r2, c0, acc[2][0]); acc[2][1] = fma(r2, c1, acc[2][1]);
+                        acc[2][2] = fma(r2, c2, acc[2][2]); acc[2][3] = fma(r2, c3, acc[2][3]);
+                        acc[3][0] = fma(r3, c0, acc[3][0]); acc[3][1] = fma(r3, c1, acc[3][1]);
+                        acc[3][2] = fma(r3, c2, acc[3][2]); acc[3][3] = fma(r3, c3, acc[3][3]);
+                    }
                 }
             }
-            if (tid < R)
-                for (int a = 0; a < na; ++a) racc = fma(be[a], (double)gs[a * R + tid], racc);
         }
-        // Gram = Σ_h partial tiles, h ascending; both triangles
-        for (int e = tid; e < Rp * Rp; e += nthr) A[e] = 0.0;
+        PHASE_CLK(1);
+        // Gram, rhs = Σ_h partial tiles, h ascending (h = 0 assigns: no zero fill)
         for (int h = 0; h < KS; ++h) {
             __syncthreads();
             if (has_task && task_h == h) {
+                if (is_rhs) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                    for (int u = 0; u < 4; ++u) rhs[4 * tr + u] = (h ? rhs[4 * tr + u] : 0.0) + acc[u][0];
+                } else {
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) A[(4 * tr + u) * Rp + 4 * ts + v] += acc[u][v];
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            double* e = A + (4 * tr + u) * LDA + 4 * ts + v;
+                            *e = (h ? *e : 0.0) + acc[u][v];
+                        }
+                }
             }
         }
-        __syncthreads();
-        for (int e = tid; e < R * R; e += nthr) {
-            const int r = e / R, c = e - r * R;
-            if (c < r) A[r * Rp + c] = A[c * Rp + r];
-        }
-        if (tid < R) rhs[tid] = racc;
         __syncthreads();
         if constexpr (SM == SOLVE_PROJECT) {
             // this rank's partial [upper triangle (r ≤ s, row-major), rhs] for the all-reduce
@@ -478,7 +517,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
                         q -= R - r;
                         ++r;
                     }
-                    v = A[r * Rp + r + q];
+                    v = A[r * LDA + r + q];
                 } else {
                     v = rhs[t - NG];
                 }
@@ -486,6 +525,9 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             }
             return;
         }
+        // lower triangle from the upper one (the Cholesky reads rows): thread rows
+        for (int r = tid >> 3; r < R; r += nthr >> 3)
+            for (int c = tid & 7; c < r; c += 8) A[r * LDA + c] = A[c * LDA + r];
     } else {
         if (one_tile) stage(0, (int)P.Ii);  // for the H refresh
         for (int t = tid; t < NA; t += nthr) {
@@ -496,92 +538,103 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
                     q -= R - r;
                     ++r;
                 }
-                A[r * Rp + r + q] = v;
-                A[(r + q) * Rp + r] = v;
+                A[(r + q) * LDA + r] = v;  // lower triangle
             } else {
                 rhs[t - NG] = v;
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
+    PHASE_CLK(2);
     // + ρI, + ρ c_old
     if (tid < R) {
         const double co = (double)P.Gki[j * R + tid];
         cold[tid] = co;
-        A[tid * Rp + tid] += P.rho;
+        A[tid * LDA + tid] += P.rho;
         rhs[tid] += P.rho * co;
     }
+    __syncthreads();
+    // Cholesky, right-looking in 4×4 blocks over all threads (lower triangle, in place; the
+    // diagonal keeps 1/L(c,c)).  Rows/columns R..Rp-1 are padded with the identity.  Per block
+    // b: thread 0 factors the 4×4 diagonal block in registers; one thread per row solves the
+    // panel below it; all threads apply the rank-4 trailing update — 3 barriers per block.
+    for (int r = R + tid; r < Rp; r += nthr)
+        for (int c = 0; c <= r; ++c) A[r * LDA + c] = (c == r) ? 1.0 : 0.0;
     if (tid == 0) *okp = 1;
     __syncthreads();
-    // Cholesky with the lower triangle in registers: thread t owns entries m = t + q·256 of
-    // the packed lower triangle (row-major, (r, c) with c ≤ r), at most kBigEnt of them.
-    // Step cc: the owner of (cc, cc) publishes 1/sqrt(d); owners of (r, cc) publish
-    // l_r = A_r,cc/sqrt(d) (parity-double-buffered column); every owner of (r, c), c > cc,
-    // subtracts l_r·l_c.  Two barriers per step, no shared-memory read-modify-write chains.
-    {
-        int er[kBigEnt], ec[kBigEnt];
-        double ev[kBigEnt];
-        const int NL = NG;  // lower-triangle entries
-        const int nent = (NL + kBigThreads - 1) / kBigThreads;  // entries per thread (≤ kBigEnt)
+    for (int c0 = 0; c0 < Rp; c0 += 4) {
+        if (tid == 0) {
+            double L[4][4];
 #pragma unroll
-        for (int q = 0; q < kBigEnt; ++q) {
-            const int m = tid + q * kBigThreads;
-            int r = 0, c = 0;
-            if (m < NL) {  // m = r(r+1)/2 + c
-                r = (int)((sqrt(8.0 * m + 1.0) - 1.0) * 0.5);
-                while ((r + 1) * (r + 2) / 2 <= m) ++r;
-                while (r * (r + 1) / 2 > m) --r;
-                c = m - r * (r + 1) / 2;
-            }
-            er[q] = m < NL ? r : -1;
-            ec[q] = c;
-            ev[q] = m < NL ? A[r * Rp + c] : 0.0;
-        }
-        bool okl = true;
-        for (int cc = 0; cc < R; ++cc) {
-            double* col = colb + (cc & 1) * 64;
+            for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int q = 0; q < kBigEnt; ++q) {
-                if (q >= nent) break;
-                if (er[q] == cc && ec[q] == cc) {
-                    const double d = ev[q];
-                    okl = d > 0.0;
-                    const double inv = 1.0 / sqrt(d > 0.0 ? d : 1.0);
-                    *dinvp = inv;
-                    ev[q] = inv;  // the diagonal keeps 1/L_cc
-                    if (!okl) *okp = 0;
+                for (int v = 0; v < 4; ++v) L[u][v] = v <= u ? A[(c0 + u) * LDA + c0 + v] : 0.0;
+            bool ok = true;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                double d = L[cc][cc];
+#pragma unroll
+                for (int k = 0; k < cc; ++k) d = fma(-L[cc][k], L[cc][k], d);
+                ok = ok && d > 0.0;
+                const double inv = rsqrt(d > 0.0 ? d : 1.0);
+                L[cc][cc] = inv;
+#pragma unroll
+                for (int r = cc + 1; r < 4; ++r) {
+                    double v = L[r][cc];
+#pragma unroll
+                    for (int k = 0; k < cc; ++k) v = fma(-L[r][k], L[cc][k], v);
+                    L[r][cc] = v * inv;
                 }
             }
-            __syncthreads();
-            const double inv = *dinvp;
 #pragma unroll
-            for (int q = 0; q < kBigEnt; ++q) {
-                if (q >= nent) break;
-                if (ec[q] == cc && er[q] > cc) {
-                    ev[q] *= inv;
-                    col[er[q]] = ev[q];
-                }
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v <= u; ++v) A[(c0 + u) * LDA + c0 + v] = L[u][v];
+            if (!ok) *okp = 0;
+        }
+        __syncthreads();
+        const int m = Rp - c0 - 4;  // trailing size
+        if (tid < m) {              // panel row r: x = a · L11⁻ᵀ
+            const int r = c0 + 4 + tid;
+            double x[4];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                double v = A[r * LDA + c0 + cc];
+#pragma unroll
+                for (int k = 0; k < cc; ++k) v = fma(-x[k], A[(c0 + cc) * LDA + c0 + k], v);
+                x[cc] = v * A[(c0 + cc) * LDA + c0 + cc];
             }
-            __syncthreads();
 #pragma unroll
-            for (int q = 0; q < kBigEnt; ++q) {
-                if (q >= nent) break;
-                if (ec[q] > cc) ev[q] = fma(-col[er[q]], col[ec[q]], ev[q]);
+            for (int cc = 0; cc < 4; ++cc) A[r * LDA + c0 + cc] = x[cc];
+        }
+        __syncthreads();
+        // trailing lower triangle (r, c), c0+4 ≤ c ≤ r: thread rows, 8 lanes over c
+        for (int rr = tid >> 3; rr < m; rr += nthr >> 3) {
+            const int r = c0 + 4 + rr;
+            const double l0 = A[r * LDA + c0], l1 = A[r * LDA + c0 + 1], l2 = A[r * LDA + c0 + 2],
+                         l3 = A[r * LDA + c0 + 3];
+            for (int c = c0 + 4 + (tid & 7); c <= r; c += 8) {
+                const double* lc = A + c * LDA + c0;
+                double v = A[r * LDA + c];
+                v = fma(-l0, lc[0], v);
+                v = fma(-l1, lc[1], v);
+                v = fma(-l2, lc[2], v);
+                v = fma(-l3, lc[3], v);
+                A[r * LDA + c] = v;
             }
         }
-#pragma unroll
-        for (int q = 0; q < kBigEnt; ++q)
-            if (er[q] >= 0) A[er[q] * Rp + ec[q]] = ev[q];
         __syncthreads();
     }
     if (tid < 32) {
+        const bool ok = *okp != 0;
+        PHASE_CLK(3);
         // L y = rhs, Lᵀ c = y with rhs in registers (lane owns rows lane, lane + 32) and the
         // pivot value broadcast by shuffle; the L entries are independent shared loads
         double x0 = lane < R ? rhs[lane] : 0.0, x1 = lane + 32 < R ? rhs[lane + 32] : 0.0;
         for (int r = 0; r < R; ++r) {
-            const double lq0 = lane > r && lane < R ? A[lane * Rp + r] : 0.0;
-            const double lq1 = lane + 32 > r && lane + 32 < R ? A[(lane + 32) * Rp + r] : 0.0;
-            const double own = (r < 32 ? x0 : x1) * A[r * Rp + r];
+            const double lq0 = lane > r && lane < R ? A[lane * LDA + r] : 0.0;
+            const double lq1 = lane + 32 > r && lane + 32 < R ? A[(lane + 32) * LDA + r] : 0.0;
+            const double own = (r < 32 ? x0 : x1) * A[r * LDA + r];
             const double y = __shfl_sync(0xffffffffu, own, r & 31);
             if (lane == (r & 31)) {
                 if (r < 32) x0 = y;
@@ -591,9 +644,9 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             x1 = fma(-lq1, y, x1);
         }
         for (int r = R - 1; r >= 0; --r) {
-            const double lr0 = lane < r ? A[r * Rp + lane] : 0.0;
-            const double lr1 = lane + 32 < r ? A[r * Rp + lane + 32] : 0.0;
-            const double own = (r < 32 ? x0 : x1) * A[r * Rp + r];
+            const double lr0 = lane < r ? A[r * LDA + lane] : 0.0;
+            const double lr1 = lane + 32 < r ? A[r * LDA + lane + 32] : 0.0;
+            const double own = (r < 32 ? x0 : x1) * A[r * LDA + r];
             const double c = __shfl_sync(0xffffffffu, own, r & 31);
             if (lane == (r & 31)) {
                 if (r < 32) x0 = c;
@@ -605,7 +658,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         if (lane < R) cv[lane] = x0;
         if (lane + 32 < R) cv[lane + 32] = x1;
         __syncwarp();
-        if (!*okp) {
+        if (!ok) {
             if (lane == 0) atomicOr(P.flags, 1);
             for (int r = lane; r < R; r += 32) cv[r] = cold[r];
         }
@@ -620,6 +673,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         }
         d2 = warp_sum(d2);
         if (lane == 0) P.delta[j] = d2;
+        PHASE_CLK(4);
     }
     // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a), 8 threads per a
     const int row8 = tid >> 3, sub8 = tid & 7;
@@ -632,7 +686,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         }
         for (int a = row8; a < na; a += nthr >> 3) {
             double h = 0.0;
-            for (int r = sub8; r < R; r += 8) h = fma(cv[r], (double)gs[a * R + r], h);
+            for (int r = sub8; r < R; r += 8) h = fma(cv[r], gs[a * R + r], h);
             h += __shfl_xor_sync(0xffffffffu, h, 1);
             h += __shfl_xor_sync(0xffffffffu, h, 2);
             h += __shfl_xor_sync(0xffffffffu, h, 4);
@@ -643,15 +697,19 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             }
         }
     }
+    PHASE_CLK(5);
+#ifdef IFCTN_EXP_PHASE_CLOCKS
+    if (j == 0 && threadIdx.x == 0)
+        printf("big solve R=%d phases (cycles): stage %lld  om/be+sync %lld  gram %lld  reduce+sym %lld  chol %lld  subst %lld  H %lld\n", P.R,
+               clk[6] - clk[0], clk[7] - clk[6], clk[1] - clk[7], clk[2] - clk[1], clk[3] - clk[2], clk[4] - clk[3], clk[5] - clk[4]);
+#endif
 }
 
 template <typename T, int SM>
 __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
     extern __shared__ __align__(16) double bsm[];
     __shared__ int ok;
-    __shared__ double colb[2 * 64];
-    __shared__ double dinv;
-    block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok, colb, &dinv);
+    block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok);
 }
 
 // ---- a1: build H_{p,q} = G_{p,q}ᵀ G_{q,p} for one pair (K=R skinny product; FMA pipes) ---
