@@ -29,7 +29,7 @@
 #pragma once
 
 #include "common.cuh"
-#include "solve.cuh"  // finalize_norms_body (last-CTA finaliser of the norm passes)
+#include "solve.cuh"
 
 namespace ifctn {
 

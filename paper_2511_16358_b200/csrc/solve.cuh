@@ -214,19 +214,25 @@ __device__ __forceinline__ void column_coeffs(const ReduceParams<T>& Q, int64_t 
 }
 
 template <typename T, int R, int SM>
-// nthr (a multiple of 32, ≤ blockDim.x) threads take part; the others only pass the barriers
+// nthr (a multiple of 32, ≤ blockDim.x) threads take part; the others only pass the barriers.
+// red: (nthr/32)·NA + NA doubles of shared scratch, cs: R.
 __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_t j, int nthr,
-                                                 double* red /*(nthr/32)·NA*/, double* cs /*R*/) {
+                                                 double* red, double* cs) {
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
+    constexpr int KEEP = 2;  // columns a of G_{i,k} kept in registers for the H refresh
     const int nw = nthr >> 5;
     const int tid = (int)threadIdx.x;
     const int ntot = (int)blockDim.x;
+    double* sum = red + nw * NA;
     auto sync = [&]() { __syncthreads(); };
     double acc[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
-    for (int64_t a = tid; a < (SM == SOLVE_FROM_PROJ || tid >= nthr ? 0 : P.Ii); a += nthr) {
+    T gk[KEEP][R];  // this thread's a = tid + q·nthr (q < KEEP) columns, reused by the H refresh
+    const int64_t na = (SM == SOLVE_FROM_PROJ || tid >= nthr) ? 0 : P.Ii;
+    int q = 0;
+    for (int64_t a = tid; a < na; a += nthr, ++q) {
         double b, w;
         if (P.fused_reduce) {
             column_coeffs(P.red, j, a, b, w);
@@ -234,9 +240,19 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
             b = P.beta[j * P.Ii + a];
             w = P.omega[j * P.Ii + a];
         }
+        T gt[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) gt[r] = P.Gik[a * R + r];
         double g[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) g[r] = (double)P.Gik[a * R + r];
+        for (int r = 0; r < R; ++r) g[r] = (double)gt[r];
+        if (q < KEEP) {
+#pragma unroll
+            for (int qq = 0; qq < KEEP; ++qq)
+                if (qq == q)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) gk[qq][r] = gt[r];
+        }
         int t = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -253,26 +269,22 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
             if (ln == 0 && wid < nw) red[wid * NA + t] = s;
         }
         sync();
-        if constexpr (SM == SOLVE_PROJECT) {
-            for (int t = tid; t < NA; t += ntot) {
-                double v = 0.0;
-                for (int q = 0; q < nw; ++q) v += red[q * NA + t];
-                P.proj[j * NA + t] = v;
-            }
-            return;
-        }
-    }
-    if (tid == 0) {
-        double sum[NA];
-#pragma unroll
-        for (int t = 0; t < NA; ++t) {
+        // entry t = Σ_q red[q][t], q ascending (one thread per entry)
+        for (int t = tid; t < NA; t += ntot) {
             double v = 0.0;
-            if constexpr (SM == SOLVE_FROM_PROJ) v = P.proj[j * NA + t];
-            else
-                for (int q = 0; q < nw; ++q) v += red[q * NA + t];
-            sum[t] = v;
+            for (int qw = 0; qw < nw; ++qw) v += red[qw * NA + t];
+            if constexpr (SM == SOLVE_PROJECT) P.proj[j * NA + t] = v;
+            else sum[t] = v;
         }
-        double A[R][R], L[R][R], y[R], c[R], cold[R];
+        if constexpr (SM == SOLVE_PROJECT) return;
+    } else {
+        for (int t = tid; t < NA; t += ntot) sum[t] = P.proj[j * NA + t];
+    }
+    sync();
+    if (tid == 0) {
+        // Cholesky with reciprocal pivots (1/√d by rsqrt; no divisions), substitutions by
+        // multiplication with the stored reciprocals
+        double A[R][R], L[R][R], inv[R], y[R], c[R], cold[R];
         int t = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -295,31 +307,30 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
         for (int cc = 0; cc < R; ++cc) {
             double d = A[cc][cc];
 #pragma unroll
-            for (int s = 0; s < cc; ++s) d -= L[cc][s] * L[cc][s];
+            for (int s = 0; s < cc; ++s) d = fma(-L[cc][s], L[cc][s], d);
             if (!(d > 0.0)) ok = false;
-            const double ld = sqrt(d > 0.0 ? d : 1.0);
-            L[cc][cc] = ld;
+            inv[cc] = rsqrt(d > 0.0 ? d : 1.0);
 #pragma unroll
             for (int r = cc + 1; r < R; ++r) {
                 double v = A[r][cc];
 #pragma unroll
-                for (int s = 0; s < cc; ++s) v -= L[r][s] * L[cc][s];
-                L[r][cc] = v / ld;
+                for (int s = 0; s < cc; ++s) v = fma(-L[r][s], L[cc][s], v);
+                L[r][cc] = v * inv[cc];
             }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             double v = rhs[r];
 #pragma unroll
-            for (int s = 0; s < r; ++s) v -= L[r][s] * y[s];
-            y[r] = v / L[r][r];
+            for (int s = 0; s < r; ++s) v = fma(-L[r][s], y[s], v);
+            y[r] = v * inv[r];
         }
 #pragma unroll
         for (int r = R - 1; r >= 0; --r) {
             double v = y[r];
 #pragma unroll
-            for (int s = r + 1; s < R; ++s) v -= L[s][r] * c[s];
-            c[r] = v / L[r][r];
+            for (int s = r + 1; s < R; ++s) v = fma(-L[s][r], c[s], v);
+            c[r] = v * inv[r];
         }
         if (!ok) {
             atomicOr(P.flags, 1);
@@ -338,11 +349,26 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
         P.delta[j] = d2;
     }
     sync();
-    // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a)
-    for (int64_t a = tid; a < P.Ii; a += ntot) {
+    // H refresh: H_{k,i}(j, a) = Σ_r c_r G_{i,k}(r, a) — from the registers where kept
+    double cr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) cr[r] = cs[r];
+    q = 0;
+    for (int64_t a = tid; a < P.Ii; a += ntot, ++q) {
+        T gt[R];
+        if (ntot == nthr && na > 0 && q < KEEP) {
+#pragma unroll
+            for (int qq = 0; qq < KEEP; ++qq)
+                if (qq == q)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) gt[r] = gk[qq][r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) gt[r] = P.Gik[a * R + r];
+        }
         double h = 0.0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) h += cs[r] * (double)P.Gik[a * R + r];
+        for (int r = 0; r < R; ++r) h += cr[r] * (double)gt[r];
         const int64_t o = P.k_lt_i ? (P.h_off + a * P.h_ld + j) : (P.h_off + j * P.h_ld + a);
         P.H[o] = (T)h;
     }
@@ -351,7 +377,7 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
 template <typename T, int R, int SM>
 __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     constexpr int NA = R * (R + 1) / 2 + R;
-    __shared__ double red[4 * NA];
+    __shared__ double red[5 * NA];
     __shared__ double cs[R];
     block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs);
 }
@@ -744,40 +770,39 @@ __device__ __forceinline__ void combine_into(const double* p5, double* scal, int
     if (!isfinite(dx2) || !isfinite(x2) || !isfinite(f) || !isfinite(dg2)) atomicOr(flags + 1, 1);
 }
 
-// Written for 1024 virtual threads (any blockDim.x dividing 1024 runs them in turn), so the
-// summation order is the same whatever the CTA size.  s: 5·1024 doubles of shared scratch.
+// One CTA of 1024 threads: strided per-thread sums, then a shuffle tree per warp and one over
+// the 32 warp sums (fixed order: deterministic).  s: 5·32 doubles of shared scratch.
 __device__ __forceinline__ void finalize_norms_body(const double* norms, int64_t ngroups, const double* delta,
                                                     int64_t ndelta, int64_t sh_off, int64_t sh_len, double* p5,
                                                     double* scal, int* flags, int obj_only, int combine,
                                                     double* s) {
-    constexpr int VT = 1024;
-    for (int vt = threadIdx.x; vt < VT; vt += blockDim.x) {
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-        for (int64_t g = vt; g < ngroups; g += VT) {  // L2 loads: written by other CTAs just now
-            a0 += __ldcg(norms + 3 * g + 0);
-            a1 += __ldcg(norms + 3 * g + 1);
-            a2 += __ldcg(norms + 3 * g + 2);
+    const int vt = threadIdx.x, nt = blockDim.x;
+    double a[5] = {0, 0, 0, 0, 0};
+    for (int64_t g = vt; g < ngroups; g += nt) {  // L2 loads: written by other CTAs just now
+        a[0] += __ldcg(norms + 3 * g + 0);
+        a[1] += __ldcg(norms + 3 * g + 1);
+        a[2] += __ldcg(norms + 3 * g + 2);
+    }
+    if (!obj_only)
+        for (int64_t d = vt; d < ndelta; d += nt) {
+            if (d >= sh_off && d < sh_off + sh_len) a[3] += delta[d];
+            else a[4] += delta[d];
         }
-        if (!obj_only)
-            for (int64_t d = vt; d < ndelta; d += VT) {
-                if (d >= sh_off && d < sh_off + sh_len) a3 += delta[d];
-                else a4 += delta[d];
-            }
-        s[0 * VT + vt] = a0;
-        s[1 * VT + vt] = a1;
-        s[2 * VT + vt] = a2;
-        s[3 * VT + vt] = a3;
-        s[4 * VT + vt] = a4;
+    const int w = vt >> 5, ln = vt & 31;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const double v = warp_sum(a[q]);
+        if (ln == 0) s[q * 32 + w] = v;
     }
     __syncthreads();
-    for (int st = VT >> 1; st > 0; st >>= 1) {
-        for (int vt = threadIdx.x; vt < st; vt += blockDim.x)
-            for (int q = 0; q < 5; ++q) s[q * VT + vt] += s[q * VT + vt + st];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < 5; ++q) p5[q] = s[q * VT];
-        if (combine) combine_into(p5, scal, flags, obj_only);
+    if (w == 0) {
+        const int nw = nt >> 5;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const double v = warp_sum(ln < nw ? s[q * 32 + ln] : 0.0);
+            if (ln == 0) p5[q] = v;
+        }
+        if (ln == 0 && combine) combine_into(p5, scal, flags, obj_only);
     }
 }
 
@@ -786,7 +811,7 @@ static __global__ void __launch_bounds__(1024) finalize_norms(const double* norm
                                                        int64_t sh_off, int64_t sh_len, double* p5,
                                                        double* scal, int* flags, int obj_only,
                                                        int combine) {
-    __shared__ double s[5 * 1024];
+    __shared__ double s[5 * 32];
     finalize_norms_body(norms, ngroups, delta, ndelta, sh_off, sh_len, p5, scal, flags, obj_only, combine, s);
 }
 
