@@ -9,6 +9,20 @@
 
 namespace ifctn {
 
+#ifdef IFCTN_EXP_TIMELINE  // diagnosis builds only: per-CTA %globaltimer stamps of the passes
+static __device__ unsigned long long g_tl[3 * 4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL_STAMP(q) \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_tl[3 * blockIdx.x + (q)] = gtimer();
+#else
+#define TL_STAMP(q)
+#endif
+
+
 constexpr int MAXN = 6;                        // IFCTN_MAX_ORDER
 constexpr int MAXP = MAXN * (MAXN - 1) / 2;    // pairs p<q
 constexpr int MAXSF = MAXN - 2;                // pairs involving the fast mode r0 (outer)

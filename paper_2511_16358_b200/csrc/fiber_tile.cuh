@@ -42,22 +42,14 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
     T* sfv = reinterpret_cast<T*>(smem_raw + P.sfv_off) + (size_t)warp * P.sfv_stride;
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);  // [H_{0,1} | H_{0,r0}]
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
+    // warp setup; the resident H blocks are loaded after the producer's first D stages are
+    // issued (their copies' latency overlaps the load), see the barrier below
     for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
     if (lane == 0)
         for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
-    {
-        const float4* s1 = reinterpret_cast<const float4*>(P.H + P.hres_src);
-        const float4* s2 = reinterpret_cast<const float4*>(P.H + P.vf2_off);
-        const float4* s3 = reinterpret_cast<const float4*>(P.H + P.h01_off);
-        float4* dst = reinterpret_cast<float4*>(hres);
-        const int n1 = (int)(P.hres_elems * sizeof(T) / 16), n2 = (int)(P.hres2_elems * sizeof(T) / 16);
-        const int n3 = (int)(P.hres3_elems * sizeof(T) / 16);
-        for (int e = threadIdx.x; e < n1 + n2 + n3; e += blockDim.x)
-            dst[e] = e < n1 ? s1[e] : (e < n1 + n2 ? s2[e - n1] : s3[e - n1 - n2]);
-    }
     fence_mbar_init();
     fence_proxy_async_smem();
-    __syncthreads();
+    __syncwarp();
 
     // Dynamic schedule: the stage range is cut into P.ngroups fixed chunks of L/F stages;
     // warps claim chunks from a global counter (P.sched[0]).  A chunk's partial slots and norm
@@ -196,6 +188,18 @@ __device__ __forceinline__ void fiber_pass_vb_body(const PassParams<T>& P, unsig
     };
     if (lane == 0)
         for (int d = 0; d < D; ++d) produce();
+    {
+        const float4* s1 = reinterpret_cast<const float4*>(P.H + P.hres_src);
+        const float4* s2 = reinterpret_cast<const float4*>(P.H + P.vf2_off);
+        const float4* s3 = reinterpret_cast<const float4*>(P.H + P.h01_off);
+        float4* dst = reinterpret_cast<float4*>(hres);
+        const int n1 = (int)(P.hres_elems * sizeof(T) / 16), n2 = (int)(P.hres2_elems * sizeof(T) / 16);
+        const int n3 = (int)(P.hres3_elems * sizeof(T) / 16);
+        for (int e = threadIdx.x; e < n1 + n2 + n3; e += blockDim.x)
+            dst[e] = e < n1 ? s1[e] : (e < n1 + n2 ? s2[e - n1] : s3[e - n1 - n2]);
+    }
+    __syncthreads();
+    TL_STAMP(1);
 
     T sb[NS][EPL], sw[NS][EPL];
 #pragma unroll
@@ -411,7 +415,12 @@ template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks)
     fiber_pass_vb(const __grid_constant__ PassParams<T> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    TL_STAMP(0);
     fiber_pass_vb_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, gridDim.x);
+#ifdef IFCTN_EXP_TIMELINE
+    __syncthreads();
+#endif
+    TL_STAMP(2);
 }
 
 }  // namespace ifctn

@@ -356,22 +356,18 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
     T* hres = reinterpret_cast<T*>(smem_raw + P.hres_off);
     T* stg = reinterpret_cast<T*>(smem_raw + P.stage_off) + (size_t)warp * Cfg::RING;
 
-    // CTA setup: per warp zero the ring (row tails past I1p must read as 0) and init the
-    // stage barriers, then the resident H_{0,r0} block (HRES).
+    // Warp setup: zero the ring (row tails past I1p must read as 0) and init the stage
+    // barriers; the producer then issues its first D stages BEFORE the CTA loads the resident
+    // H_{0,r0} block (HRES), so the first copies' latency overlaps that load.
     for (int e = lane; e < Cfg::RING; e += 32) stg[e] = T(0);
     if (lane == 0)
         for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
-    if constexpr (HRES) {
-        const float4* src = reinterpret_cast<const float4*>(P.H + P.hres_src);
-        float4* dst = reinterpret_cast<float4*>(hres);
-        for (int e = threadIdx.x; e < (int)(P.hres_elems * sizeof(T) / 16); e += blockDim.x) dst[e] = src[e];
-    }
     fence_mbar_init();
     fence_proxy_async_smem();
-    __syncthreads();
+    __syncwarp();
 
     const int group = cta * nwarps + warp;
-    if (group >= P.ngroups) return;
+    const bool active = group < P.ngroups;
 
     const uint32_t bar0 = smem_u32(bars);
     const uint32_t stg0 = smem_u32(stg);
@@ -382,8 +378,8 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
     const bool lane_full = eb + EPL <= I1p;
     const int ebc = eb < I1p ? eb : 0;               // clamped (HRES reads stay in bounds)
 
-    const int f0 = group * (int)P.L;
-    const int f1 = min(f0 + (int)P.L, (int)P.nfib);
+    const int f0 = active ? group * (int)P.L : 0;
+    const int f1 = active ? min(f0 + (int)P.L, (int)P.nfib) : 0;
     const bool has_fast = P.nred > 0;
     const int fstep = has_fast ? (int)P.fstride[P.rmode[0]] : 0;
     const int64_t xstep = (int64_t)fstep * I1p;      // elements between consecutive fibres
@@ -458,13 +454,20 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
         p_left -= nf;
         ++p_n;
     };
-    if (lane == 0)
+    if (active && lane == 0)
         for (int d = 0; d < D; ++d) produce();
-
+    if constexpr (HRES) {
+        const float4* src = reinterpret_cast<const float4*>(P.H + P.hres_src);
+        float4* dst = reinterpret_cast<float4*>(hres);
+        for (int e = threadIdx.x; e < (int)(P.hres_elems * sizeof(T) / 16); e += blockDim.x) dst[e] = src[e];
+    }
+    __syncthreads();
+    TL_STAMP(1);
     // ---- consumers (all lanes) ---------------------------------------------------------
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;  // REFILL: ‖ΔX‖², ‖X‖², ‖X_new − t‖²; OBJ: n2
     T sb[EPL], sw[EPL];                     // segment accumulators (one kept value v)
     uint32_t cn = 0;                        // next stage to consume
+    if (!active) return;
     Walker C;
     walker_init(C, P, f0, f1);
     while (walker_next(C, P)) {
@@ -670,7 +673,12 @@ __device__ __forceinline__ void fiber_pass_body(const PassParams<T>& P, unsigned
 template <typename T, int MODE, int EPL, int LPF, bool HRES>
 __global__ void __launch_bounds__(kPassThreads, kPassMinBlocks) fiber_pass(const __grid_constant__ PassParams<T> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    TL_STAMP(0);
     fiber_pass_body<T, MODE, EPL, LPF, HRES>(P, smem_raw, blockIdx.x);
+#ifdef IFCTN_EXP_TIMELINE
+    __syncthreads();
+#endif
+    TL_STAMP(2);
 }
 
 }  // namespace ifctn

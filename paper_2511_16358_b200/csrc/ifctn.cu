@@ -1789,3 +1789,14 @@ int64_t ifctn_launch_count(const ifctn_ctx* ctx) {
 }
 
 }  // extern "C"
+
+#ifdef IFCTN_EXP_TIMELINE
+extern "C" int ifctn_exp_timeline(unsigned long long* out, int n) {
+    cudaDeviceSynchronize();
+    if (n < 0) {  // clear
+        static unsigned long long z[3 * 4096] = {};
+        return (int)cudaMemcpyToSymbol(ifctn::g_tl, z, sizeof(z));
+    }
+    return (int)cudaMemcpyFromSymbol(out, ifctn::g_tl, sizeof(unsigned long long) * 3 * (size_t)(n < 4096 ? n : 4096));
+}
+#endif
