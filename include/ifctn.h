@@ -94,7 +94,21 @@ typedef struct {
      * ranks.  NULL = NCCL (nccl_unique_id required).  Disables CUDA-graph capture.          */
     void (*host_allreduce)(double* buf, size_t count, void* user);
     void* user;
+    /* exchange = IFCTN_XCHG_PEER: no NCCL.  The per-block Gram/RHS partials (and the sweep
+     * norms, RSE and metric sums) are exchanged over peer memory of one node (NVLink /
+     * NVSwitch): every rank's library-owned exchange buffer is exported with a CUDA IPC
+     * handle, and the solve kernel of each block publishes, waits for its peers and sums their
+     * partials in rank order itself (device-side all-reduce fused with the solve; see
+     * paper_2511_16358_b200/csrc/peer.cuh).  host_allgather (called once, inside
+     * ifctn_create, with this rank's 64-byte handle) must fill `all` with the world handles in
+     * rank order — a host all-gather (e.g. torch.distributed.all_gather_object).  May be NULL
+     * when world == 1.  Ranks must be on distinct GPUs of one node with peer access.        */
+    int exchange;
+    void (*host_allgather)(const void* mine, void* all, size_t bytes, void* user);
 } ifctn_dist;
+
+#define IFCTN_XCHG_NCCL 0 /* NCCL all-reduce launched on the context's stream (default)      */
+#define IFCTN_XCHG_PEER 1 /* device-side exchange over peer memory (one node)                */
 
 /* One row of the per-sweep trace (Algorithm 1 stop test P:L341-344, Lemma 2). */
 typedef struct {
@@ -185,6 +199,13 @@ ifctn_status ifctn_destroy(ifctn_ctx* ctx);
 
 const char* ifctn_status_string(ifctn_status s);
 const char* ifctn_last_error(const ifctn_ctx* ctx);
+
+/* Self-test of the peer-exchange protocol on the CURRENT device (test support): `world`
+ * (2..16) virtual ranks run `rounds` exchanges of `n` doubles in ONE cooperative launch (ranks
+ * whose kernels wait on one another must not be separate launches on one GPU), with the same
+ * publish / wait / rank-ordered sum / epoch code as the library's solve kernels.  *errors =
+ * number of mismatching sums (0 expected).  E_ARG for bad sizes, E_CUDA on launch failure. */
+ifctn_status ifctn_peer_selftest(int world, int rounds, int64_t n, int64_t* errors);
 
 /* Run ONE sweep as plain launches with a CUDA event before every kernel, on the context's
  * stream, and return each launch's device time in ms, in launch order:

@@ -34,12 +34,15 @@ class IfctnError(RuntimeError):
 
 
 HOST_ALLREDUCE = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_size_t, ctypes.c_void_p)
+HOST_ALLGATHER = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+IFCTN_XCHG_NCCL, IFCTN_XCHG_PEER = 0, 1
 
 
 class ifctn_dist(ctypes.Structure):
     _fields_ = [("nccl_unique_id", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("shard_mode", ctypes.c_int),
-                ("host_allreduce", HOST_ALLREDUCE), ("user", ctypes.c_void_p)]
+                ("host_allreduce", HOST_ALLREDUCE), ("user", ctypes.c_void_p),
+                ("exchange", ctypes.c_int), ("host_allgather", HOST_ALLGATHER)]
 
 
 class ifctn_trace_row(ctypes.Structure):
@@ -87,6 +90,7 @@ SIGNATURES = {
     "ifctn_mask_fibres": (_I, [_VP, _I, _I64P, _I, ctypes.c_int64, ctypes.c_uint64, _VP]),
     "ifctn_grid_run": (_I, [_I, _I64P, _I, _VP, _VP, _VP, ctypes.POINTER(ifctn_instance), _I, _I, _I,
                             ctypes.POINTER(ifctn_instance_result)]),
+    "ifctn_peer_selftest": (_I, [_I, _I, ctypes.c_int64, _I64P]),
 }
 
 
@@ -252,3 +256,10 @@ def ifctn_mask_uniform(mask_ptr, n, observed, seed, stream=None):
 def ifctn_mask_fibres(mask_ptr, dims, mode, missing_fibres, seed, stream=None):
     check(lib().ifctn_mask_fibres(mask_ptr, len(dims), _i64arr(dims), int(mode), int(missing_fibres),
                                   int(seed), stream))
+
+
+def ifctn_peer_selftest(world: int, rounds: int, n: int) -> int:
+    """Peer-exchange protocol self-test on the current device; returns the mismatch count."""
+    err = ctypes.c_int64(-1)
+    check(lib().ifctn_peer_selftest(world, rounds, n, ctypes.byref(err)))
+    return err.value

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <cstdio>
 
+#include "peer.cuh"
+
 #include <type_traits>
 
 namespace ifctn {
@@ -314,6 +316,8 @@ struct SolveParams {
     double* delta;       // per column ‖c_new − c_old‖²
     int* flags;          // flags[0] |= 1 on a non-positive pivot
     double* proj;        // multi-GPU: per column [Gram upper triangle, rhs] partials
+    int use_peer;        // multi-GPU over peer memory (peer.cuh): PROJECT writes the exchange
+    PeerCtx peer;        //   slot, FROM_PROJ publishes, waits and sums the ranks' slots itself
     int R;               // R_{k,i} (block_solve_big; block_solve has it as a template argument)
     int fused_reduce;    // block_solve: sum β(a,j), ω(a,j) from the a2 partial slots itself
     ReduceParams<T> red; //   (the reduce_partials launch of the block is then skipped)

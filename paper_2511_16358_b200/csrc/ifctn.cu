@@ -68,6 +68,7 @@ struct Shape {
     // distribution
     int rank = 0, world = 1, shard = 0;
     bool dpath = false;  // distributed code path (world > 1, or a 1-rank comm / hook)
+    bool peer = false;   // exchange over peer memory (peer.cuh) instead of NCCL
     int64_t sbegin = 0, send = 0;
     int64_t ld[MAXN] = {};  // local dims
     // layout
@@ -155,7 +156,12 @@ static Shape make_shape(int order, const int64_t* dims, const int32_t* ranks, if
     }
     // a single rank with a communicator (or host hook) runs the distributed code path too:
     // projections, all-reduces (1-rank NCCL) and split finalisers — used to test the path
-    s.dpath = dist && (dist->world > 1 || dist->nccl_unique_id || dist->host_allreduce);
+    s.dpath = dist && (dist->world > 1 || dist->nccl_unique_id || dist->host_allreduce ||
+                       dist->exchange == IFCTN_XCHG_PEER);
+    s.peer = s.dpath && dist->exchange == IFCTN_XCHG_PEER;
+    if (dist && dist->exchange != IFCTN_XCHG_NCCL && dist->exchange != IFCTN_XCHG_PEER)
+        fail(IFCTN_E_ARG, "dist->exchange must be IFCTN_XCHG_NCCL or IFCTN_XCHG_PEER");
+    if (s.peer && (dist->world > kPeerMax)) fail(IFCTN_E_UNSUPPORTED, "peer exchange supports at most 16 ranks");
     if (s.dpath && dist->world == 1) {
         if (dist->rank != 0) fail(IFCTN_E_ARG, "dist rank out of range");
         int sm = dist->shard_mode < 0 ? 0 : dist->shard_mode;
@@ -552,12 +558,19 @@ struct Solver : SolverBase {
     // multi-GPU (see dist.cuh notes in DESIGN.md)
     NcclLite* nccl = nullptr;
     void* comm = nullptr;
+    // peer-memory exchange (peer.cuh): own buffer, peers' mapped buffers, device context
+    double* xbuf = nullptr;
+    PeerCtx pctx{};
+    std::vector<void*> peer_open;
 
     ~Solver() override {
         for (cudaGraphExec_t e : {gexec, gexec_first, gexec_mid, gexec_last, gexec_mid_t, gexec_last_t})
             if (e) cudaGraphExecDestroy(e);
         if (trace_rows) cudaFree(trace_rows);
         if (comm && nccl) nccl->commDestroy(comm);
+        if (st) cudaStreamSynchronize(st);
+        for (void* p : peer_open) cudaIpcCloseMemHandle(p);
+        if (xbuf) cudaFree(xbuf);
         if (st) cudaStreamSynchronize(st);
         if (own_ws && ws) cudaFree(ws);
         if (hscal) cudaFreeHost(hscal);
@@ -918,6 +931,8 @@ struct Solver : SolverBase {
                                                 (int)(smem_limit - fa.sharedSizeBytes)));
                     }
                 }
+                q.use_peer = s.peer ? 1 : 0;
+                q.peer = pctx;
                 b.dist = s.dpath && k != s.shard;
                 if (b.dist) {  // Σ over ranks of the projected Gram/RHS partials (§8(e))
                     const int R = s.R(k, i);
@@ -978,9 +993,9 @@ struct Solver : SolverBase {
 
     void enqueue_solve(const BlockPlan<T>& b, const SolveParams<T>* sp = nullptr) {
         const SolveParams<T>& q = sp ? *sp : b.sol;
-        if (b.dist) {
+        if (b.dist) {  // peer exchange: the solve below publishes, waits and sums itself
             launch(b.proj_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
-            allreduce_dev(proj, (size_t)b.proj_count);
+            if (!s.peer) allreduce_dev(proj, (size_t)b.proj_count);
         }
         launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
     }
@@ -1107,6 +1122,37 @@ struct Solver : SolverBase {
                 const size_t bytes = (size_t)s.R(int_mode(k), int_mode(i)) * s.eld[k] * s.esize;
                 CU(cudaMemcpyAsync(to_internal ? dst + io : dst + eo, to_internal ? src + eo : src + io, bytes, kind, st));
             }
+    }
+
+    // Peer-memory exchange setup (IFCTN_XCHG_PEER): the exchange buffer, its IPC handle
+    // all-gathered through the caller's host callback, the peers' buffers mapped.  Called
+    // before plan() (the solve parameters carry the PeerCtx).
+    void setup_peer(const ifctn_dist* dist) {
+        const int64_t slot = std::max<int64_t>(s.proj_elems, 64);
+        const size_t bytes = sizeof(double) * (size_t)(kPeerHeader + 2 * slot + 8);
+        CU(cudaMalloc(&xbuf, bytes));
+        CU(cudaMemset(xbuf, 0, bytes));
+        CU(cudaDeviceSynchronize());  // zeroed before any peer can read the flag
+        pctx.W = s.world;
+        pctx.rank = s.rank;
+        pctx.slot_elems = slot;
+        pctx.epoch = reinterpret_cast<unsigned long long*>(xbuf + kPeerHeader + 2 * slot);
+        pctx.arrive = reinterpret_cast<unsigned*>(pctx.epoch + 1);
+        pctx.bufs[s.rank] = xbuf;
+        if (s.world > 1) {
+            if (!dist->host_allgather) fail(IFCTN_E_ARG, "dist->host_allgather must be set for IFCTN_XCHG_PEER");
+            cudaIpcMemHandle_t h;
+            CU(cudaIpcGetMemHandle(&h, xbuf));
+            std::vector<cudaIpcMemHandle_t> all((size_t)s.world);
+            dist->host_allgather(&h, all.data(), sizeof(h), dist->user);
+            for (int r = 0; r < s.world; ++r) {
+                if (r == s.rank) continue;
+                void* p = nullptr;
+                CU(cudaIpcOpenMemHandle(&p, all[(size_t)r], cudaIpcMemLazyEnablePeerAccess));
+                peer_open.push_back(p);
+                pctx.bufs[r] = (double*)p;
+            }
+        }
     }
 
     void init(const void* observed, const uint8_t* mask, const void* G0, void* workspace,
@@ -1534,7 +1580,7 @@ struct Solver : SolverBase {
 
     // all-reduce of an arbitrary-length fp64 buffer (host-callback staging is proj_elems long)
     void allreduce_dev_chunked(double* buf, size_t count) {
-        const size_t step = host_allreduce ? (size_t)s.proj_elems : count;
+        const size_t step = host_allreduce ? (size_t)s.proj_elems : s.peer ? (size_t)pctx.slot_elems : count;
         for (size_t o = 0; o < count; o += step) allreduce_dev(buf + o, std::min(step, count - o));
     }
 
@@ -1596,6 +1642,12 @@ struct Solver : SolverBase {
     // NCCL all-reduce (capturable into the sweep graph), or the caller's host_allreduce.
     void allreduce_dev(double* buf, size_t count) {
         if (!s.dpath) return;
+        if (s.peer) {  // one CTA: copy in, publish, wait, rank-ordered sum (peer.cuh)
+            if (count > (size_t)pctx.slot_elems) fail(IFCTN_E_STATE, "all-reduce larger than the exchange slot");
+            void* args[] = {(void*)&pctx, &buf, &count};
+            launch_raw((const void*)peer_allreduce, dim3(1), dim3(256), 0, args);
+            return;
+        }
         if (host_allreduce) {
             if (count > (size_t)s.proj_elems) fail(IFCTN_E_STATE, "all-reduce larger than the staging buffer");
             CU(cudaMemcpyAsync(hred, buf, count * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1690,7 +1742,9 @@ ifctn_status ifctn_create(ifctn_ctx** out, int order, const int64_t* dims, const
             sv->lay = ifctn::make_layout(s);
             sv->rho = rho;
             sv->flags = flags;
-            if (s.dpath) {
+            if (s.peer) {
+                sv->setup_peer(dist);
+            } else if (s.dpath) {
                 if (dist->host_allreduce) {
                     sv->host_allreduce = dist->host_allreduce;
                     sv->host_user = dist->user;
@@ -1770,6 +1824,54 @@ ifctn_status ifctn_destroy(ifctn_ctx* ctx) {
     if (!ctx) return IFCTN_E_ARG;
     delete ctx;
     return IFCTN_OK;
+}
+
+ifctn_status ifctn_peer_selftest(int world, int rounds, int64_t n, int64_t* errors) {
+    using namespace ifctn;
+    if (world < 2 || world > kPeerMax || rounds < 1 || n < 1 || n > (1 << 20) || !errors) return IFCTN_E_ARG;
+    std::vector<double*> bufs((size_t)world, nullptr);
+    unsigned long long* ep = nullptr;
+    unsigned* cnt = nullptr;
+    unsigned* err = nullptr;
+    ifctn_status st = IFCTN_OK;
+    auto ck = [&](cudaError_t e) {
+        if (e != cudaSuccess && st == IFCTN_OK) {
+            st = IFCTN_E_CUDA;
+            g_last_err = cudaGetErrorString(e);
+        }
+    };
+    PeerCtx X{};
+    X.W = world;
+    X.rank = 0;
+    X.slot_elems = n;
+    for (int r = 0; r < world; ++r) {
+        ck(cudaMalloc(&bufs[(size_t)r], sizeof(double) * (size_t)(kPeerHeader + 2 * n)));
+        if (st == IFCTN_OK) ck(cudaMemset(bufs[(size_t)r], 0, sizeof(double) * (size_t)(kPeerHeader + 2 * n)));
+        X.bufs[r] = bufs[(size_t)r];
+    }
+    ck(cudaMalloc(&ep, sizeof(unsigned long long) * kPeerMax));
+    ck(cudaMalloc(&cnt, sizeof(unsigned) * 2 * kPeerMax));
+    ck(cudaMalloc(&err, sizeof(unsigned)));
+    if (st == IFCTN_OK) {
+        ck(cudaMemset(ep, 0, sizeof(unsigned long long) * kPeerMax));
+        ck(cudaMemset(cnt, 0, sizeof(unsigned) * 2 * kPeerMax));
+        ck(cudaMemset(err, 0, sizeof(unsigned)));
+        X.epoch = ep;
+        X.arrive = cnt;
+        // 2 CTAs per virtual rank, all co-resident (cooperative launch guarantees it or fails)
+        void* args[] = {&X, &rounds, &n, &err};
+        ck(cudaLaunchCooperativeKernel((const void*)peer_selftest, dim3((unsigned)(2 * world)), dim3(128), args, 0, 0));
+        ck(cudaDeviceSynchronize());
+        unsigned h = 0;
+        ck(cudaMemcpy(&h, err, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        *errors = (int64_t)h;
+    }
+    for (double* b : bufs)
+        if (b) cudaFree(b);
+    if (ep) cudaFree(ep);
+    if (cnt) cudaFree(cnt);
+    if (err) cudaFree(err);
+    return st;
 }
 
 const char* ifctn_status_string(ifctn_status s) {

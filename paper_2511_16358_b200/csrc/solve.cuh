@@ -226,6 +226,13 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
     const int ntot = (int)blockDim.x;
     double* sum = red + nw * NA;
     auto sync = [&]() { __syncthreads(); };
+    // peer exchange (peer.cuh): the FROM_PROJ solve is the collective's consumer
+    unsigned long long pe = 0;
+    if constexpr (SM == SOLVE_FROM_PROJ)
+        if (P.use_peer) {
+            pe = peer_next_epoch(P.peer);
+            peer_publish_wait(P.peer, pe);
+        }
     double acc[NA];
 #pragma unroll
     for (int t = 0; t < NA; ++t) acc[t] = 0.0;
@@ -270,15 +277,17 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
         }
         sync();
         // entry t = Σ_q red[q][t], q ascending (one thread per entry)
+        double* pdst = nullptr;
+        if constexpr (SM == SOLVE_PROJECT) pdst = P.use_peer ? peer_my_slot(P.peer) : P.proj;
         for (int t = tid; t < NA; t += ntot) {
             double v = 0.0;
             for (int qw = 0; qw < nw; ++qw) v += red[qw * NA + t];
-            if constexpr (SM == SOLVE_PROJECT) P.proj[j * NA + t] = v;
+            if constexpr (SM == SOLVE_PROJECT) pdst[j * NA + t] = v;
             else sum[t] = v;
         }
         if constexpr (SM == SOLVE_PROJECT) return;
     } else {
-        for (int t = tid; t < NA; t += ntot) sum[t] = P.proj[j * NA + t];
+        for (int t = tid; t < NA; t += ntot) sum[t] = P.use_peer ? peer_sum(P.peer, pe, j * NA + t) : P.proj[j * NA + t];
     }
     sync();
     if (tid == 0) {
@@ -372,6 +381,8 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
         const int64_t o = P.k_lt_i ? (P.h_off + a * P.h_ld + j) : (P.h_off + j * P.h_ld + a);
         P.H[o] = (T)h;
     }
+    if constexpr (SM == SOLVE_FROM_PROJ)
+        if (P.use_peer) peer_retire(P.peer, pe);
 }
 
 template <typename T, int R, int SM>
@@ -430,6 +441,12 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     double* cv = rhs + Rp;
     double* cold = cv + Rp;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+    unsigned long long pe = 0;  // peer exchange (peer.cuh): FROM_PROJ is the consumer
+    if constexpr (SM == SOLVE_FROM_PROJ)
+        if (P.use_peer) {
+            pe = peer_next_epoch(P.peer);
+            peer_publish_wait(P.peer, pe);
+        }
     const int nt = Rp / 4;
     const int ntg = nt * (nt + 1) / 2;     // Gram tiles; then nt rhs tiles
     const int ntasks = ntg + nt;
@@ -535,6 +552,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         __syncthreads();
         if constexpr (SM == SOLVE_PROJECT) {
             // this rank's partial [upper triangle (r ≤ s, row-major), rhs] for the all-reduce
+            double* pdst = P.use_peer ? peer_my_slot(P.peer) : P.proj;
             for (int t = tid; t < NA; t += nthr) {
                 double v;
                 if (t < NG) {
@@ -547,7 +565,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
                 } else {
                     v = rhs[t - NG];
                 }
-                P.proj[j * NA + t] = v;
+                pdst[j * NA + t] = v;
             }
             return;
         }
@@ -557,7 +575,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     } else {
         if (one_tile) stage(0, (int)P.Ii);  // for the H refresh
         for (int t = tid; t < NA; t += nthr) {
-            const double v = P.proj[j * NA + t];
+            const double v = P.use_peer ? peer_sum(P.peer, pe, j * NA + t) : P.proj[j * NA + t];
             if (t < NG) {
                 int r = 0, q = t;
                 while (q >= R - r) {
@@ -724,6 +742,8 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         }
     }
     PHASE_CLK(5);
+    if constexpr (SM == SOLVE_FROM_PROJ)
+        if (P.use_peer) peer_retire(P.peer, pe);
 #ifdef IFCTN_EXP_PHASE_CLOCKS
     if (j == 0 && threadIdx.x == 0)
         printf("big solve R=%d phases (cycles): stage %lld  om/be+sync %lld  gram %lld  reduce+sym %lld  chol %lld  subst %lld  H %lld\n", P.R,

@@ -93,12 +93,26 @@ def gather_factors(shards, dims, ranks, mode: int, bounds):
 
 
 def make_dist(rank: int, world: int, shard_mode: int = -1, nccl_id: bytes | None = None,
-              host_allreduce=None, user=None):
-    """ifctn_dist for rank/world.  Either nccl_id (128 bytes, identical on all ranks) or a
-    Python host_allreduce(np_view) callback summing a float64 buffer across ranks in place."""
+              host_allreduce=None, user=None, peer: bool = False, allgather=None):
+    """ifctn_dist for rank/world.  Either nccl_id (128 bytes, identical on all ranks), a
+    Python host_allreduce(np_view) callback summing a float64 buffer across ranks in place, or
+    peer=True: the device-side exchange over peer memory (IFCTN_XCHG_PEER), whose CUDA IPC
+    handles are all-gathered once at create by allgather(bytes) -> [bytes per rank] (host
+    plumbing, e.g. torch_allgather below; not needed at world 1)."""
     d = _abi.ifctn_dist()
     d.rank, d.world, d.shard_mode = rank, world, shard_mode
     keep = []
+    if peer:
+        d.exchange = _abi.IFCTN_XCHG_PEER
+        if allgather is not None:
+            def _ag(mine, out, nbytes, _user):
+                got = allgather(ctypes.string_at(mine, nbytes))
+                if len(got) != world or any(len(g) != nbytes for g in got):
+                    raise RuntimeError("host_allgather: wrong result shape")
+                ctypes.memmove(out, b"".join(got), nbytes * world)
+            cbg = _abi.HOST_ALLGATHER(_ag)
+            keep.append(cbg)
+            d.host_allgather = cbg
     if nccl_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         keep.append(buf)
@@ -125,3 +139,15 @@ def nccl_unique_id_from_torch(group=None) -> bytes:
     obj = [uid]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def torch_allgather(group=None):
+    """allgather(bytes) -> [bytes per rank] over torch.distributed (host objects; gloo or
+    NCCL process groups): the IPC-handle exchange of make_dist(peer=True)."""
+    import torch.distributed as dist
+
+    def ag(b: bytes):
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, b, group=group)
+        return out
+    return ag

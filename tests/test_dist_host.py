@@ -148,3 +148,43 @@ def test_gloo_world2_sharded_sweep_equals_oracle(dist_mod, name, mode):
     assert np.allclose(s4, res[1][4]) and dg2_rep == res[1][5]   # replicated state identical
     assert abs(s4[2] - F1) <= 1e-9 * max(1, F1)                   # all-reduced objective (½ applied per rank)
     assert abs((s4[3] + dg2_rep) - row[3]) <= 1e-9 * max(1, row[3])  # ΔG² accounting
+
+
+def _peer_allgather(rank, world, q):
+    """One process: the IPC-handle all-gather of the peer exchange (make_dist(peer=True)),
+    called through the C function pointer the library calls inside ifctn_create."""
+    import ctypes
+
+    import torch.distributed as tdist
+
+    from paper_2511_16358_b200 import dist as D
+
+    tdist.init_process_group("gloo", rank=rank, world_size=world,
+                             init_method=f"tcp://127.0.0.1:{q['port']}")
+    try:
+        d = D.make_dist(rank, world, -1, peer=True, allgather=D.torch_allgather())
+        assert d.exchange == 1 and bool(d.host_allgather)
+        mine = bytes([rank * 16 + b % 16 for b in range(64)])
+        src = ctypes.create_string_buffer(mine, 64)
+        out = ctypes.create_string_buffer(64 * world)
+        d.host_allgather(ctypes.cast(src, ctypes.c_void_p), ctypes.cast(out, ctypes.c_void_p), 64, None)
+        q["res"][rank] = out.raw
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_world2_peer_handle_allgather(dist_mod):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    q = mgr.dict()
+    q["port"] = port
+    q["res"] = mgr.dict()
+    mp.spawn(_peer_allgather, args=(2, q), nprocs=2, join=True)
+    want = b"".join(bytes([r * 16 + b % 16 for b in range(64)]) for r in range(2))
+    assert q["res"][0] == want and q["res"][1] == want
