@@ -325,8 +325,12 @@ def run_ours(args):
         msk = D.shard_tensor(p.mask, p.dims, sm, sb, se)
         truth = D.shard_tensor(p.truth, p.dims, sm, sb, se)
         g0 = D.shard_factors(p.G0, p.dims, p.ranks, sm, sb, se)
-        uid = D.nccl_unique_id_from_torch()
-        mk_dist = lambda: D.make_dist(rank, world, -1, nccl_id=uid)
+        if args.exchange == "peer":  # device-side exchange fused with the solves (peer.cuh)
+            ag = D.torch_allgather()
+            mk_dist = lambda: D.make_dist(rank, world, -1, peer=True, allgather=ag)
+        else:
+            uid = D.nccl_unique_id_from_torch()
+            mk_dist = lambda: D.make_dist(rank, world, -1, nccl_id=uid)
     obs_d, mask_d, g0_d = dev(obs), dev(msk), dev(g0)
 
     def barrier():
@@ -398,7 +402,10 @@ def run_ours(args):
             "gpu_launches": launches, "clocks": clk.summary(), "rse_after_steps": rse}
     if world > 1:
         line["config"]["shard"] = {"mode": sm, "rank0_slice": [sb, se],
-                                   "exchange": "NCCL all-reduce of projected Gram/RHS partials per block k != shard mode"}
+                                   "exchange": ("peer memory: each block's solve kernel publishes, waits for and sums "
+                                                "the ranks' projected Gram/RHS partials (IFCTN_XCHG_PEER)")
+                                   if args.exchange == "peer" else
+                                   "NCCL all-reduce of projected Gram/RHS partials per block k != shard mode"}
         line["roofline"]["note"] = "per-rank a2 pass over this rank's shard"
 
     if not args.no_e2e:
@@ -586,6 +593,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="multi-GPU exchange: device-side over peer memory (default) or NCCL")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -70,6 +70,9 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
 #define IFCTN_FLAG_NO_VBLOCK 8u /* diagnostic: plain fibre walk for every block (no v-blocking) */
 #define IFCTN_FLAG_NO_SOLVE_REDUCE 64u /* diagnostic: separate a2 reduce kernel even when the
                                         * small-rank solve can absorb it                     */
+#define IFCTN_FLAG_NO_L2PASS 128u /* diagnostic: the HBM-streaming fibre walk for step a2 even
+                                     when X is L2-resident (default there: one CTA per kept
+                                     value, no partial slots; csrc/l2pass.cuh)               */
 #define IFCTN_FLAG_NO_FUSE 16u  /* diagnostic: never fuse a sweep's X update into the next
                                    sweep's first block (see ifctn_sweep)                      */
 

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "fiber_walk.cuh"
 #include "fiber_tile.cuh"
+#include "l2pass.cuh"
 #include "solve.cuh"
 #include "metrics.cuh"
 #include "nccl_lite.h"
@@ -422,6 +423,12 @@ struct BlockPlan {
     unsigned sol_threads = 128;
     size_t sol_smem = 0;
     const void* sol_fn = nullptr;
+    // L2-resident tensors: the per-kept-value contraction (l2pass.cuh) instead of pass+reduce
+    bool l2 = false;
+    L2Params<T> l2p;
+    const void* l2_fn = nullptr;
+    dim3 l2_grid;
+    size_t l2_smem = 0;
     // multi-GPU, k ≠ shard mode: project → all-reduce → solve
     bool dist = false;
     const void* proj_fn = nullptr;
@@ -853,6 +860,104 @@ struct Solver : SolverBase {
         return {(const void*)reduce_partials<T>, dim3((unsigned)r.NV, (unsigned)r.ntile, (unsigned)Z)};
     }
 
+    template <bool KEPT>
+    static const void* pick_l2(int nch) {
+        return nch == 1 ? (const void*)l2_contract<T, KEPT, 1>
+             : nch == 2 ? (const void*)l2_contract<T, KEPT, 2> : (const void*)l2_contract<T, KEPT, 4>;
+    }
+
+    // Step a2 of block (k,i) by l2pass.cuh when X is L2-resident; false = not applicable.
+    bool make_l2(BlockPlan<T>& b, int k, int i) {
+        if (flags & IFCTN_FLAG_NO_L2PASS) return false;
+        if (s.npad * s.esize > (int64_t)48 << 20) return false;
+        // Measured per block (scripts/block_split.py): faster than walk + reduce on the
+        // third-order tensors (C1, C2, C2r: every block), slower on C3/C4 (4th order: 10^4
+        // short fibres per block, one dependent L2 round trip each) — third order only.
+        if (s.N != 3) return false;
+        const int VE = 16 / (int)s.esize;
+        const int nch = (int)((s.I1p + 32 * VE - 1) / (32 * VE));
+        if (nch > 4) return false;
+        const int N = s.N;
+        L2Params<T>& P = b.l2p;
+        memset(&P, 0, sizeof(P));
+        P.X = X;
+        P.H = H;
+        P.beta = beta;
+        P.omega = omega;
+        P.I1 = (int)s.I1;
+        P.I1p = (int)s.I1p;
+        P.N = N;
+        P.Ii = s.ld[i];
+        P.Ik = s.ld[k];
+        const bool kept1 = (k == 0 || i == 0);
+        P.kept1 = kept1;
+        P.kIsMode0 = (k == 0);
+        P.m = kept1 ? std::max(k, i) : -1;
+        P.k = k;
+        P.i = i;
+        for (int q = 1; q < N; ++q) P.fstride[q] = s.fstride[q];
+        P.NV = kept1 ? s.ld[P.m] : s.ld[k] * s.ld[i];
+        P.FR = 1;
+        for (int q = 1; q < N; ++q) {
+            const bool kept = kept1 ? (q == P.m) : (q == k || q == i);
+            if (kept) continue;
+            P.rmode[P.nr] = q;
+            P.rdim[P.nr] = s.ld[q];
+            ++P.nr;
+            P.FR *= s.ld[q];
+            (void)0;
+        }
+        for (int q = 1; q < N; ++q) {
+            if (kept1 && q == P.m) continue;  // the excluded pair {0, m}
+            P.vec_off[P.nvec] = s.hoff[0][q];
+            P.vec_mode[P.nvec] = q;
+            ++P.nvec;
+        }
+        for (int p = 1; p < N; ++p)
+            for (int q = p + 1; q < N; ++q) {
+                if (!kept1 && ((p == k && q == i) || (p == i && q == k))) continue;
+                P.pair_off[P.npair] = s.hoff[p][q];
+                P.pair_ld[P.npair] = s.hld[p];
+                P.pair_p[P.npair] = p;
+                P.pair_q[P.npair] = q;
+                ++P.npair;
+            }
+        if (P.FR >= (1LL << 31) || P.NV >= (1LL << 31)) return false;
+        // work split: wpv warps per v (vpc v per CTA), Z CTAs per v.  Each warp's fibres are
+        // a dependent load chain (one L2 round trip each), so the split keeps them ≤ 4 per
+        // warp; a block that would need more than 64 CTAs per v (C3's 3-long mode, C4's
+        // 4-long mode against ~10^4 fibres) keeps the streaming walk (measured slower here:
+        // scripts/block_split.py).
+        constexpr int64_t kMaxFibresPerWarp = 4;
+        int wpv = 1;
+        while (wpv < 8 && wpv < P.FR) wpv <<= 1;
+        int vpc = 8 / wpv;
+        int64_t nblk = (P.NV + vpc - 1) / vpc;
+        int64_t Z = 1;
+        const int64_t per = kept1 ? s.I1p : 1;
+        if ((P.FR + wpv - 1) / wpv > kMaxFibresPerWarp) {
+            wpv = 8;
+            vpc = 1;
+            nblk = P.NV;
+            Z = (P.FR + 8 * kMaxFibresPerWarp - 1) / (8 * kMaxFibresPerWarp);
+            if (Z > 64 || P.NV > kRedCnt || P.NV * Z * per * 2 > kRedScr) return false;
+        }
+        P.FRz = (P.FR + Z - 1) / Z;
+        Z = (P.FR + P.FRz - 1) / P.FRz;
+        P.Z = (int)Z;
+        P.vpc = vpc;
+        P.wpv = wpv;
+        P.scr = rscr;
+        P.cnt = rcnt;
+        b.l2_fn = kept1 ? pick_l2<true>(nch) : pick_l2<false>(nch);
+        b.l2_grid = dim3((unsigned)nblk, (unsigned)Z);
+        b.l2_smem = kept1 ? (size_t)8 * 2 * s.I1p * sizeof(double) : 16 * sizeof(double);
+        if (b.l2_smem > 48 * 1024)
+            CU(cudaFuncSetAttribute(b.l2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.l2_smem));
+        b.l2 = true;
+        return true;
+    }
+
     void plan() {
         const int N = s.N;
         blocks.clear();
@@ -914,6 +1019,7 @@ struct Solver : SolverBase {
                 const int64_t chain = slots_per_v * ((s.ld[i] + 127) / 128);
                 const bool gather_ok = r.kept1 ? (i == 0 && chain <= solve_slots) : (slots_per_v <= 16 && s.ld[i] >= 16);
                 q.fused_reduce = (q.R <= MAXR_SMALL && gather_ok && !(flags & IFCTN_FLAG_NO_SOLVE_REDUCE)) ? 1 : 0;
+                if (make_l2(b, k, i)) q.fused_reduce = 0;  // β, ω written whole by l2_contract
                 b.sol_grid = dim3((unsigned)s.ld[k]);
                 if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): a CTA per column
                     b.sol_threads = kBigThreads;
@@ -986,6 +1092,11 @@ struct Solver : SolverBase {
     // ifctn_block_coefficients).  A skipped reduce keeps an empty profiling interval so that
     // ifctn_profile_sweep still reports [pass, reduce, solve] per block.
     void enqueue_contract(const BlockPlan<T>& b, bool full = false) {
+        if (b.l2) {  // one launch writes β, ω whole; an empty interval for the reduce slot
+            launch(b.l2_fn, b.l2_grid, dim3(kL2Threads), b.l2_smem, b.l2p);
+            prof_mark();
+            return;
+        }
         launch(b.pass.fn, b.pass.grid, dim3(kPassThreads), b.pass.smem, b.pass.p);
         if (full || !b.sol.fused_reduce) launch(b.red_l.fn, b.red_l.grid, dim3(256), 0, b.red);
         else prof_mark();
