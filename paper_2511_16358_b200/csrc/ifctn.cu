@@ -322,7 +322,7 @@ struct Layout {
 
 // split-slot reduce (reduce_partials with Z > 1): scratch doubles and arrival counters
 constexpr int64_t kRedScr = 2 * 2048 * 32 * 2;
-constexpr int64_t kRedCnt = 2048;
+constexpr int64_t kRedCnt = 8192;
 
 static Layout make_layout(const Shape& s) {
     Layout L{};
@@ -860,24 +860,33 @@ struct Solver : SolverBase {
         return {(const void*)reduce_partials<T>, dim3((unsigned)r.NV, (unsigned)r.ntile, (unsigned)Z)};
     }
 
-    template <bool KEPT>
-    static const void* pick_l2(int nch) {
-        return nch == 1 ? (const void*)l2_contract<T, KEPT, 1>
-             : nch == 2 ? (const void*)l2_contract<T, KEPT, 2> : (const void*)l2_contract<T, KEPT, 4>;
+    static const void* pick_l2_kept(int nr) {
+        switch (nr) {
+            case 1: return (const void*)l2_kept<T, 1>;
+            case 2: return (const void*)l2_kept<T, 2>;
+            case 3: return (const void*)l2_kept<T, 3>;
+            default: return (const void*)l2_kept<T, 4>;
+        }
+    }
+    static const void* pick_l2_red(int nch) {
+        return nch == 1 ? (const void*)l2_red<T, 1> : nch == 2 ? (const void*)l2_red<T, 2> : (const void*)l2_red<T, 4>;
+    }
+
+    // CTAs of `fn` (256 threads, static shared memory only) resident on the device at once
+    int64_t resident_ctas(const void* fn) {
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kL2Threads, 0));
+        return (int64_t)std::max(per_sm, 1) * nsm;
     }
 
     // Step a2 of block (k,i) by l2pass.cuh when X is L2-resident; false = not applicable.
     bool make_l2(BlockPlan<T>& b, int k, int i) {
         if (flags & IFCTN_FLAG_NO_L2PASS) return false;
         if (s.npad * s.esize > (int64_t)48 << 20) return false;
-        // Measured per block (scripts/block_split.py): faster than walk + reduce on the
-        // third-order tensors (C1, C2, C2r: every block), slower on C3/C4 (4th order: 10^4
-        // short fibres per block, one dependent L2 round trip each) — third order only.
-        if (s.N != 3) return false;
-        const int VE = 16 / (int)s.esize;
-        const int nch = (int)((s.I1p + 32 * VE - 1) / (32 * VE));
-        if (nch > 4) return false;
         const int N = s.N;
+        if (N < 3) return false;
+        if (s.nfib >= (1LL << 31) || s.htotal >= (1LL << 31)) return false;
+        const int VE = 16 / (int)s.esize;
         L2Params<T>& P = b.l2p;
         memset(&P, 0, sizeof(P));
         P.X = X;
@@ -902,58 +911,118 @@ struct Solver : SolverBase {
             const bool kept = kept1 ? (q == P.m) : (q == k || q == i);
             if (kept) continue;
             P.rmode[P.nr] = q;
-            P.rdim[P.nr] = s.ld[q];
+            P.rdim[P.nr] = (int)s.ld[q];
+            P.rdiv[P.nr] = (int)P.FR;
             ++P.nr;
             P.FR *= s.ld[q];
-            (void)0;
         }
-        for (int q = 1; q < N; ++q) {
-            if (kept1 && q == P.m) continue;  // the excluded pair {0, m}
-            P.vec_off[P.nvec] = s.hoff[0][q];
-            P.vec_mode[P.nvec] = q;
-            ++P.nvec;
-        }
-        for (int p = 1; p < N; ++p)
-            for (int q = p + 1; q < N; ++q) {
-                if (!kept1 && ((p == k && q == i) || (p == i && q == k))) continue;
-                P.pair_off[P.npair] = s.hoff[p][q];
-                P.pair_ld[P.npair] = s.hld[p];
-                P.pair_p[P.npair] = p;
-                P.pair_q[P.npair] = q;
-                ++P.npair;
-            }
         if (P.FR >= (1LL << 31) || P.NV >= (1LL << 31)) return false;
-        // work split: wpv warps per v (vpc v per CTA), Z CTAs per v.  Each warp's fibres are
-        // a dependent load chain (one L2 round trip each), so the split keeps them ≤ 4 per
-        // warp; a block that would need more than 64 CTAs per v (C3's 3-long mode, C4's
-        // 4-long mode against ~10^4 fibres) keeps the streaming walk (measured slower here:
-        // scripts/block_split.py).
-        constexpr int64_t kMaxFibresPerWarp = 4;
-        int wpv = 1;
-        while (wpv < 8 && wpv < P.FR) wpv <<= 1;
-        int vpc = 8 / wpv;
-        int64_t nblk = (P.NV + vpc - 1) / vpc;
-        int64_t Z = 1;
-        const int64_t per = kept1 ? s.I1p : 1;
-        if ((P.FR + wpv - 1) / wpv > kMaxFibresPerWarp) {
-            wpv = 8;
-            vpc = 1;
-            nblk = P.NV;
-            Z = (P.FR + 8 * kMaxFibresPerWarp - 1) / (8 * kMaxFibresPerWarp);
-            if (Z > 64 || P.NV > kRedCnt || P.NV * Z * per * 2 > kRedScr) return false;
-        }
-        P.FRz = (P.FR + Z - 1) / Z;
-        Z = (P.FR + P.FRz - 1) / P.FRz;
-        P.Z = (int)Z;
-        P.vpc = vpc;
-        P.wpv = wpv;
         P.scr = rscr;
         P.cnt = rcnt;
-        b.l2_fn = kept1 ? pick_l2<true>(nch) : pick_l2<false>(nch);
-        b.l2_grid = dim3((unsigned)nblk, (unsigned)Z);
-        b.l2_smem = kept1 ? (size_t)8 * 2 * s.I1p * sizeof(double) : 16 * sizeof(double);
-        if (b.l2_smem > 48 * 1024)
-            CU(cudaFuncSetAttribute(b.l2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b.l2_smem));
+        // Work split.  Cost model in L2 round trips: every CTA pays a fixed part (launch ramp,
+        // index setup, the warp/CTA combine) plus one round per U fibres of its busiest
+        // thread; CTAs beyond the resident set wait for a second wave; a split over Z CTAs
+        // adds the last-arrival combine.
+        static const int kZs[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64};
+        auto cdiv = [](int64_t a, int64_t c) { return (a + c - 1) / c; };
+        double best = 1e300;
+        if (kept1) {
+            const int NR = N - 2;
+            const int m = P.m;
+            P.kf_stride = s.fstride[m];
+            for (int j = 0; j < NR; ++j) {
+                const int q = P.rmode[j];
+                P.rfs[j] = (int)s.fstride[q];
+                P.rv_off[j] = (int)s.hoff[0][q];
+                if (m < q) {
+                    P.ks_off[j] = (int)s.hoff[m][q];
+                    P.ks_mv[j] = 1;
+                    P.ks_mj[j] = (int)s.hld[m];
+                } else {
+                    P.ks_off[j] = (int)s.hoff[q][m];
+                    P.ks_mv[j] = (int)s.hld[q];
+                    P.ks_mj[j] = 1;
+                }
+            }
+            int t = 0;
+            for (int j = 0; j < NR; ++j)
+                for (int j2 = j + 1; j2 < NR; ++j2, ++t) {
+                    const int q = P.rmode[j], q2 = P.rmode[j2];  // q < q2
+                    P.jj_off[t] = (int)s.hoff[q][q2];
+                    P.jj_ma[t] = 1;
+                    P.jj_mb[t] = (int)s.hld[q];
+                }
+            b.l2_fn = pick_l2_kept(NR);
+            const int64_t resident = resident_ctas(b.l2_fn);
+            const int NC = (int)(s.I1p / VE);
+            for (int CG = 1; CG <= 32; CG <<= 1) {
+                if (CG < 4 && CG < NC) continue;      // ≥ 64 contiguous bytes per fibre piece
+                if (CG > 4 && CG >= 2 * NC) continue;
+                const int FL = 32 / CG;
+                const int64_t NCG = cdiv(NC, CG);
+                const double waste = (double)(NCG * CG) / NC;
+                for (int wpi = 1; wpi <= 8; wpi <<= 1) {
+                    const int ipc = 8 / wpi;
+                    const int64_t nbx = cdiv(P.NV * NCG, ipc);
+                    const int64_t slots = (int64_t)wpi * FL;
+                    for (int Z : kZs) {
+                        if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * ipc * 2 * CG * VE > kRedScr)) continue;
+                        const int64_t FRz = cdiv(P.FR, Z), Ze = cdiv(P.FR, FRz);
+                        const int64_t rounds = cdiv(cdiv(FRz, slots), kL2U);
+                        const int64_t waves = cdiv(nbx * Ze, resident);
+                        const double cost = waves * (1.5 + rounds * waste) + (Ze > 1 ? 1.0 : 0.0) +
+                                            1e-3 * (double)(nbx * Ze) / resident;
+                        if (cost < best) {
+                            best = cost;
+                            P.CG = CG;
+                            P.NCG = (int)NCG;
+                            P.ipc = ipc;
+                            P.wpi = wpi;
+                            P.FRz = FRz;
+                            P.Z = (int)Ze;
+                            b.l2_grid = dim3((unsigned)nbx, (unsigned)Ze);
+                        }
+                    }
+                }
+            }
+        } else {
+            const int nch = (int)((s.I1p + 32 * VE - 1) / (32 * VE));
+            if (nch > 4) return false;
+            P.nvec = N - 1;
+            for (int q = 1; q < N; ++q) P.vec_off[q - 1] = (int)s.hoff[0][q];
+            for (int p = 1; p < N; ++p)
+                for (int q = p + 1; q < N; ++q) {
+                    if ((p == k && q == i) || (p == i && q == k)) continue;
+                    P.pair_off[P.npair] = (int)s.hoff[p][q];
+                    P.pair_ld[P.npair] = (int)s.hld[p];
+                    P.pair_p[P.npair] = p;
+                    P.pair_q[P.npair] = q;
+                    ++P.npair;
+                }
+            b.l2_fn = pick_l2_red(nch);
+            const int64_t resident = resident_ctas(b.l2_fn);
+            for (int wpv = 1; wpv <= 8; wpv <<= 1) {
+                const int vpc = 8 / wpv;
+                const int64_t nbx = cdiv(P.NV, vpc);
+                for (int Z : kZs) {
+                    if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * vpc * 2 > kRedScr)) continue;
+                    const int64_t FRz = cdiv(P.FR, Z), Ze = cdiv(P.FR, FRz);
+                    const int64_t rounds = cdiv(cdiv(FRz, wpv), kL2U);
+                    const int64_t waves = cdiv(nbx * Ze, resident);
+                    const double cost = waves * (1.5 + rounds) + (Ze > 1 ? 1.0 : 0.0) + 1e-3 * (double)(nbx * Ze) / resident;
+                    if (cost < best) {
+                        best = cost;
+                        P.vpc = vpc;
+                        P.wpv = wpv;
+                        P.FRz = FRz;
+                        P.Z = (int)Ze;
+                        b.l2_grid = dim3((unsigned)nbx, (unsigned)Ze);
+                    }
+                }
+            }
+        }
+        if (best >= 1e300) return false;
+        b.l2_smem = 0;
         b.l2 = true;
         return true;
     }
