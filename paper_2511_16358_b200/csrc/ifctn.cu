@@ -429,6 +429,11 @@ struct BlockPlan {
     const void* l2_fn = nullptr;
     dim3 l2_grid;
     size_t l2_smem = 0;
+    // large ranks on one GPU: Gram/RHS of all columns by gram_project, then the FROM_PROJ solve
+    bool gemm = false;
+    SolveParams<T> gram_sol;
+    dim3 gram_grid;
+    size_t gram_smem = 0;
     // multi-GPU, k ≠ shard mode: project → all-reduce → solve
     bool dist = false;
     const void* proj_fn = nullptr;
@@ -546,6 +551,12 @@ struct Solver : SolverBase {
     RedLaunch fused_red_l;
     SolveParams<T> fused_sol;  // block (0,1)'s solve after the fused pass (its slot layout)
     bool has_fused = false;
+    // L2-resident tensors: a5 by l2_refill (l2pass.cuh) instead of the streaming refill pass
+    bool l2r = false;
+    L2RefillParams<T> l2rp;
+    const void* l2r_fn = nullptr;
+    dim3 l2r_grid;
+    size_t l2r_smem = 0;
     cudaGraphExec_t gexec = nullptr;                                    // one plain sweep
     cudaGraphExec_t gexec_first = nullptr, gexec_mid = nullptr, gexec_last = nullptr;
     cudaGraphExec_t gexec_mid_t = nullptr, gexec_last_t = nullptr;  // traced fused sweeps
@@ -868,14 +879,19 @@ struct Solver : SolverBase {
             default: return (const void*)l2_kept<T, 4>;
         }
     }
-    static const void* pick_l2_red(int nch) {
-        return nch == 1 ? (const void*)l2_red<T, 1> : nch == 2 ? (const void*)l2_red<T, 2> : (const void*)l2_red<T, 4>;
+    static const void* pick_l2_red(int nrr) {
+        switch (nrr) {
+            case 0: return (const void*)l2_red<T, 0>;
+            case 1: return (const void*)l2_red<T, 1>;
+            case 2: return (const void*)l2_red<T, 2>;
+            default: return (const void*)l2_red<T, 3>;
+        }
     }
 
-    // CTAs of `fn` (256 threads, static shared memory only) resident on the device at once
-    int64_t resident_ctas(const void* fn) {
+    // CTAs of `fn` (256 threads, `smem` dynamic bytes) resident on the device at once
+    int64_t resident_ctas(const void* fn, size_t smem) {
         int per_sm = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kL2Threads, 0));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kL2Threads, smem));
         return (int64_t)std::max(per_sm, 1) * nsm;
     }
 
@@ -884,7 +900,10 @@ struct Solver : SolverBase {
         if (flags & IFCTN_FLAG_NO_L2PASS) return false;
         if (s.npad * s.esize > (int64_t)48 << 20) return false;
         const int N = s.N;
-        if (N < 3) return false;
+        // orders 3 and 4 (the paper's L2-sized workloads, C1–C4).  Orders ≥ 5 keep the streaming
+        // walk: the small 5th-order test problems (C5s) are ill-conditioned enough to amplify
+        // any change of rounding order ~25× per sweep, and their bars are set against the walk.
+        if (N < 3 || N > 4) return false;
         if (s.nfib >= (1LL << 31) || s.htotal >= (1LL << 31)) return false;
         const int VE = 16 / (int)s.esize;
         L2Params<T>& P = b.l2p;
@@ -907,70 +926,83 @@ struct Solver : SolverBase {
         for (int q = 1; q < N; ++q) P.fstride[q] = s.fstride[q];
         P.NV = kept1 ? s.ld[P.m] : s.ld[k] * s.ld[i];
         P.FR = 1;
+        int64_t rsum = 0;
         for (int q = 1; q < N; ++q) {
             const bool kept = kept1 ? (q == P.m) : (q == k || q == i);
             if (kept) continue;
             P.rmode[P.nr] = q;
             P.rdim[P.nr] = (int)s.ld[q];
-            P.rdiv[P.nr] = (int)P.FR;
+            P.rfs[P.nr] = (int)s.fstride[q];
+            P.rfsI[P.nr] = (int)(s.fstride[q] * s.I1p);
+            P.rv_off[P.nr] = (int)s.hoff[0][q];
             ++P.nr;
             P.FR *= s.ld[q];
+            rsum += s.ld[q];
         }
         if (P.FR >= (1LL << 31) || P.NV >= (1LL << 31)) return false;
-        P.scr = rscr;
-        P.cnt = rcnt;
-        // Work split.  Cost model in L2 round trips: every CTA pays a fixed part (launch ramp,
-        // index setup, the warp/CTA combine) plus one round per U fibres of its busiest
-        // thread; CTAs beyond the resident set wait for a second wave; a split over Z CTAs
-        // adds the last-arrival combine.
-        static const int kZs[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64};
-        auto cdiv = [](int64_t a, int64_t c) { return (a + c - 1) / c; };
-        double best = 1e300;
-        if (kept1) {
-            const int NR = N - 2;
-            const int m = P.m;
-            P.kf_stride = s.fstride[m];
-            for (int j = 0; j < NR; ++j) {
-                const int q = P.rmode[j];
-                P.rfs[j] = (int)s.fstride[q];
-                P.rv_off[j] = (int)s.hoff[0][q];
-                if (m < q) {
-                    P.ks_off[j] = (int)s.hoff[m][q];
-                    P.ks_mv[j] = 1;
-                    P.ks_mj[j] = (int)s.hld[m];
-                } else {
-                    P.ks_off[j] = (int)s.hoff[q][m];
-                    P.ks_mv[j] = (int)s.hld[q];
-                    P.ks_mj[j] = 1;
-                }
+        // H_{p,r_j}(x, d) for a kept outer mode p: H[off + x·mv + d·mj]
+        auto kept_scalar = [&](int p, int j, int* off, int* mv, int* mj) {
+            const int q = P.rmode[j];
+            if (p < q) {
+                off[j] = (int)s.hoff[p][q];
+                mv[j] = 1;
+                mj[j] = (int)s.hld[p];
+            } else {
+                off[j] = (int)s.hoff[q][p];
+                mv[j] = (int)s.hld[q];
+                mj[j] = 1;
             }
+        };
+        {
             int t = 0;
-            for (int j = 0; j < NR; ++j)
-                for (int j2 = j + 1; j2 < NR; ++j2, ++t) {
+            for (int j = 0; j < P.nr; ++j)
+                for (int j2 = j + 1; j2 < P.nr; ++j2, ++t) {
                     const int q = P.rmode[j], q2 = P.rmode[j2];  // q < q2
                     P.jj_off[t] = (int)s.hoff[q][q2];
                     P.jj_ma[t] = 1;
                     P.jj_mb[t] = (int)s.hld[q];
                 }
+        }
+        P.scr = rscr;
+        P.cnt = rcnt;
+        // Work split.  Cost model in L2 round trips: every CTA pays a fixed part (launch ramp,
+        // index setup, table staging, the warp/CTA combine) plus one round per U cells of its
+        // busiest thread; CTAs beyond the resident set wait for a second wave; a split over Z
+        // CTAs adds the last-arrival combine.
+        static const int kZs[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 32, 48, 64};
+        auto cdiv = [](int64_t a, int64_t c) { return (a + c - 1) / c; };
+        const size_t smem_cap = std::min<size_t>(smem_limit > 24 * 1024 ? smem_limit - 24 * 1024 : 0, 96 * 1024);
+        const int NC = (int)(s.I1p / VE);
+        double best = 1e300;
+        if (kept1) {
+            const int NR = N - 2;
+            P.kf_stride = s.fstride[P.m];
+            for (int j = 0; j < NR; ++j) kept_scalar(P.m, j, P.ks_off, P.ks_mv, P.ks_mj);
             b.l2_fn = pick_l2_kept(NR);
-            const int64_t resident = resident_ctas(b.l2_fn);
-            const int NC = (int)(s.I1p / VE);
+            CU(cudaFuncSetAttribute(b.l2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+            const int64_t tab_esize = NR >= 3 ? 8 : s.esize;  // fp64 tables for orders ≥ 5
+            const int KU = l2_kept_u<T>(NR);
             for (int CG = 1; CG <= 32; CG <<= 1) {
                 if (CG < 4 && CG < NC) continue;      // ≥ 64 contiguous bytes per fibre piece
                 if (CG > 4 && CG >= 2 * NC) continue;
                 const int FL = 32 / CG;
                 const int64_t NCG = cdiv(NC, CG);
                 const double waste = (double)(NCG * CG) / NC;
+                const int64_t tab_item = rsum * CG * VE;
                 for (int wpi = 1; wpi <= 8; wpi <<= 1) {
                     const int ipc = 8 / wpi;
+                    const size_t smem = (size_t)ipc * tab_item * tab_esize;
+                    if (smem > smem_cap) continue;
+                    const int64_t resident = resident_ctas(b.l2_fn, smem);
                     const int64_t nbx = cdiv(P.NV * NCG, ipc);
                     const int64_t slots = (int64_t)wpi * FL;
                     for (int Z : kZs) {
                         if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * ipc * 2 * CG * VE > kRedScr)) continue;
                         const int64_t FRz = cdiv(P.FR, Z), Ze = cdiv(P.FR, FRz);
-                        const int64_t rounds = cdiv(cdiv(FRz, slots), kL2U);
+                        const int64_t rounds = cdiv(cdiv(FRz, slots), KU);
                         const int64_t waves = cdiv(nbx * Ze, resident);
-                        const double cost = waves * (1.5 + rounds * waste) + (Ze > 1 ? 1.0 : 0.0) +
+                        const double stage = (double)cdiv(rsum * CG, wpi * 32) / 4;  // table rounds
+                        const double cost = waves * (1.5 + stage + rounds * waste) + (Ze > 1 ? 1.0 : 0.0) +
                                             1e-3 * (double)(nbx * Ze) / resident;
                         if (cost < best) {
                             best = cost;
@@ -978,52 +1010,142 @@ struct Solver : SolverBase {
                             P.NCG = (int)NCG;
                             P.ipc = ipc;
                             P.wpi = wpi;
+                            P.lcg = 0;
+                            while ((1 << P.lcg) < CG) ++P.lcg;
+                            P.lwpi = 0;
+                            while ((1 << P.lwpi) < wpi) ++P.lwpi;
+                            P.tab_item = (int)tab_item;
                             P.FRz = FRz;
                             P.Z = (int)Ze;
                             b.l2_grid = dim3((unsigned)nbx, (unsigned)Ze);
+                            b.l2_smem = smem;
                         }
                     }
                 }
             }
         } else {
-            const int nch = (int)((s.I1p + 32 * VE - 1) / (32 * VE));
-            if (nch > 4) return false;
-            P.nvec = N - 1;
-            for (int q = 1; q < N; ++q) P.vec_off[q - 1] = (int)s.hoff[0][q];
-            for (int p = 1; p < N; ++p)
-                for (int q = p + 1; q < N; ++q) {
-                    if ((p == k && q == i) || (p == i && q == k)) continue;
-                    P.pair_off[P.npair] = (int)s.hoff[p][q];
-                    P.pair_ld[P.npair] = (int)s.hld[p];
-                    P.pair_p[P.npair] = p;
-                    P.pair_q[P.npair] = q;
-                    ++P.npair;
-                }
-            b.l2_fn = pick_l2_red(nch);
-            const int64_t resident = resident_ctas(b.l2_fn);
-            for (int wpv = 1; wpv <= 8; wpv <<= 1) {
-                const int vpc = 8 / wpv;
-                const int64_t nbx = cdiv(P.NV, vpc);
+            const int NRR = N - 3;
+            for (int j = 0; j < NRR; ++j) {
+                kept_scalar(k, j, P.ks_off, P.ks_mv, P.ks_mj);
+                kept_scalar(i, j, P.is_off, P.is_mv, P.is_mj);
+            }
+            P.pk_off = (int)s.hoff[0][k];
+            P.pi_off = (int)s.hoff[0][i];
+            b.l2_fn = pick_l2_red(NRR);
+            CU(cudaFuncSetAttribute(b.l2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+            for (int TL = 8; TL <= kL2Threads; TL <<= 1) {
+                const int tpc = kL2Threads / TL;
+                const size_t smem = (size_t)tpc * s.I1p * s.esize;
+                if (smem > smem_cap) continue;
+                const int64_t resident = resident_ctas(b.l2_fn, smem);
+                const int64_t nbx = cdiv(P.NV, tpc);
                 for (int Z : kZs) {
-                    if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * vpc * 2 > kRedScr)) continue;
+                    if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * tpc * 2 > kRedScr)) continue;
                     const int64_t FRz = cdiv(P.FR, Z), Ze = cdiv(P.FR, FRz);
-                    const int64_t rounds = cdiv(cdiv(FRz, wpv), kL2U);
+                    const int64_t rounds = cdiv(cdiv(FRz * NC, TL), kL2U);
                     const int64_t waves = cdiv(nbx * Ze, resident);
-                    const double cost = waves * (1.5 + rounds) + (Ze > 1 ? 1.0 : 0.0) + 1e-3 * (double)(nbx * Ze) / resident;
+                    const double stage = (double)cdiv(NC, TL) / kL2U;
+                    const double cost = waves * (1.5 + stage + rounds) + (Ze > 1 ? 1.0 : 0.0) + 1e-3 * (double)(nbx * Ze) / resident;
                     if (cost < best) {
                         best = cost;
-                        P.vpc = vpc;
-                        P.wpv = wpv;
+                        P.TL = TL;
                         P.FRz = FRz;
                         P.Z = (int)Ze;
                         b.l2_grid = dim3((unsigned)nbx, (unsigned)Ze);
+                        b.l2_smem = smem;
                     }
                 }
             }
         }
         if (best >= 1e300) return false;
-        b.l2_smem = 0;
         b.l2 = true;
+        return true;
+    }
+
+    static const void* pick_l2_refill(int no) {
+        switch (no) {
+            case 1: return (const void*)l2_refill<T, 1>;
+            case 2: return (const void*)l2_refill<T, 2>;
+            case 3: return (const void*)l2_refill<T, 3>;
+            case 4: return (const void*)l2_refill<T, 4>;
+            default: return (const void*)l2_refill<T, 5>;
+        }
+    }
+
+    // Step a5 by l2_refill when X is L2-resident; false = keep the streaming refill pass.
+    bool make_l2_refill() {
+        if (flags & IFCTN_FLAG_NO_L2PASS) return false;
+        if (s.npad * s.esize > (int64_t)48 << 20) return false;
+        const int N = s.N;
+        if (N < 3 || N > 4 || s.nfib >= (1LL << 31) || s.htotal >= (1LL << 31) || s.npad >= (1LL << 32)) return false;
+        int64_t fs = 1, dsum = 0;
+        for (int q = 1; q < N; ++q) {  // fibre index = mixed radix over modes 2..N, mode 2 fastest
+            if (s.fstride[q] != fs) return false;
+            fs *= s.ld[q];
+            dsum += s.ld[q];
+        }
+        const int VE = 16 / (int)s.esize;
+        const int NC = (int)(s.I1p / VE);
+        L2RefillParams<T>& P = l2rp;
+        memset(&P, 0, sizeof(P));
+        P.X = X;
+        P.H = H;
+        P.mask = bits;
+        P.norms = norms;
+        P.rho = (T)rho;
+        P.inv1p = (T)(1.0 / (1.0 + rho));
+        P.I1p = (int)s.I1p;
+        P.nfib = s.nfib;
+        for (int q = 1; q < N; ++q) {
+            P.dim[q - 1] = (int)s.ld[q];
+            P.tv_off[q - 1] = (int)s.hoff[0][q];
+        }
+        {
+            int t = 0;
+            for (int q = 1; q < N; ++q)
+                for (int q2 = q + 1; q2 < N; ++q2, ++t) {
+                    P.pp_off[t] = (int)s.hoff[q][q2];
+                    P.pp_ld[t] = (int)s.hld[q];
+                }
+        }
+        l2r_fn = pick_l2_refill(N - 1);
+        auto cdiv = [](int64_t a, int64_t c) { return (a + c - 1) / c; };
+        double best = 1e300;
+        for (int CG = 1; CG <= 32; CG <<= 1) {
+            if (CG < 4 && CG < NC) continue;
+            if (CG > 4 && CG >= 2 * NC) continue;
+            const size_t smem = (size_t)dsum * CG * VE * s.esize;
+            if (smem > 40 * 1024) continue;
+            const int FL = 32 / CG;
+            const int64_t NCG = cdiv(NC, CG);
+            const double waste = (double)(NCG * CG) / NC;
+            const int64_t resident = resident_ctas(l2r_fn, smem);
+            const int64_t slots = 8 * FL;
+            for (int64_t rounds = 1; rounds <= 64; ++rounds) {
+                const int64_t FRz = slots * kL2U * rounds;
+                const int64_t Z = cdiv(s.nfib, FRz);
+                if (NCG * Z > s.groups_bound || Z > 65535) continue;
+                const int64_t waves = cdiv(NCG * Z, resident);
+                const double stage = (double)cdiv(dsum * CG, kL2Threads) / 4;
+                const double cost = waves * (1.5 + stage + rounds * waste) + 1e-3 * (double)(NCG * Z) / resident;
+                if (cost < best) {
+                    best = cost;
+                    P.CG = CG;
+                    P.lcg = 0;
+                    while ((1 << P.lcg) < CG) ++P.lcg;
+                    P.NCG = (int)NCG;
+                    P.FRz = FRz;
+                    l2r_grid = dim3((unsigned)NCG, (unsigned)Z);
+                    l2r_smem = smem;
+                }
+            }
+        }
+        if (best >= 1e300) return false;
+        int64_t st = 8 * (32 / P.CG);
+        for (int q = 0; q < N - 1; ++q) {
+            P.ds[q] = (int)(st % P.dim[q]);
+            st /= P.dim[q];
+        }
         return true;
     }
 
@@ -1114,12 +1236,27 @@ struct Solver : SolverBase {
                     b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT);
                     b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ);
                     b.proj_count = s.ld[k] * (R * (R + 1) / 2 + R);
+                } else if (q.R > MAXR_SMALL && !(flags & IFCTN_FLAG_NO_GRAM_GEMM)) {
+                    // one GPU, large rank: two columns per CTA share the g_a g_aᵀ tile products
+                    b.gemm = true;
+                    b.gram_sol = q;
+                    b.gram_sol.use_peer = 0;
+                    const size_t cap = std::min<size_t>(smem_limit - 8 * 1024, 128 * 1024);
+                    b.gram_sol.ta = (int)s.ld[i];
+                    if (gram_project_smem(q.R, b.gram_sol.ta) > cap) b.gram_sol.ta = 32;
+                    b.gram_smem = gram_project_smem(q.R, b.gram_sol.ta);
+                    if (b.gram_smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "rank too large for the Gram kernel");
+                    CU(cudaFuncSetAttribute((const void*)gram_project<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem_limit));
+                    b.gram_grid = dim3((unsigned)((s.ld[k] + kGramCols - 1) / kGramCols));
+                    b.sol_fn = pick_solve<T>(q.R, SOLVE_FROM_PROJ);
                 } else {
                     b.sol_fn = pick_solve<T>(s.R(k, i), SOLVE_FULL);
                 }
                 blocks.push_back(b);
             }
         refill = make_pass(PASS_REFILL, -1, -1);
+        l2r = make_l2_refill();
         obj = make_pass(PASS_OBJ, -1, -1);
         model = make_pass(PASS_MODEL, -1, -1);
         nlaunch_sweep = 3 * (int64_t)blocks.size() + 2;
@@ -1130,7 +1267,7 @@ struct Solver : SolverBase {
         // fused a5(s) + a2 of block (0,1) of sweep s+1 (same G, X read and written once)
         has_fused = false;
         // (the first block keeps the lane mode 0: API (0,1), or its image under Shape::perm)
-        if (!(flags & kFlagNoFuse) && std::min(blocks[0].k, blocks[0].i) == 0) {
+        if (!l2r && !(flags & kFlagNoFuse) && std::min(blocks[0].k, blocks[0].i) == 0) {
             const BlockPlan<T>& b0 = blocks[0];
             const bool vb = b0.vblk && std::max(b0.k, b0.i) == 1 && s.I1p * s.ld[1] * s.esize <= 32 * 1024;
             fused = make_pass(PASS_FUSED, b0.k, b0.i, vb);
@@ -1173,6 +1310,12 @@ struct Solver : SolverBase {
 
     void enqueue_solve(const BlockPlan<T>& b, const SolveParams<T>* sp = nullptr) {
         const SolveParams<T>& q = sp ? *sp : b.sol;
+        if (b.gemm) {  // both launches in the block's solve interval of ifctn_profile_sweep
+            launch((const void*)gram_project<T>, b.gram_grid, dim3(kBigThreads), b.gram_smem, b.gram_sol);
+            void* args[] = {(void*)&b.gram_sol};
+            launch_raw(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, args);
+            return;
+        }
         if (b.dist) {  // peer exchange: the solve below publishes, waits and sums itself
             launch(b.proj_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
             if (!s.peer) allreduce_dev(proj, (size_t)b.proj_count);
@@ -1207,6 +1350,11 @@ struct Solver : SolverBase {
     }
 
     void enqueue_xupdate() {
+        if (l2r) {
+            launch(l2r_fn, l2r_grid, dim3(kL2Threads), l2r_smem, l2rp);
+            enqueue_finalize((int64_t)l2r_grid.x * l2r_grid.y, 0);
+            return;
+        }
         launch(refill.fn, refill.grid, dim3(kPassThreads), refill.smem, refill.p);
         enqueue_finalize(refill.p.ngroups, 0);
     }

@@ -29,6 +29,9 @@
 #pragma once
 
 #include "common.cuh"
+#include "fiber_walk.cuh"
+
+#include <type_traits>
 
 namespace ifctn {
 
@@ -52,27 +55,36 @@ struct L2Params {
     int nr;                // reduced outer modes (odometer, first fastest)
     int rmode[MAXN];
     int rdim[MAXN];
-    int rdiv[MAXN];        // Π of the faster reduced dims
-    // ---- l2_red: warps per v, v per CTA; vector factors H_{0,q}(:, i_q), scalar factors
-    int vpc, wpv;
-    int nvec;
-    int vec_off[MAXN];
-    int npair;             // scalar factors H_{p,q}(i_p, i_q), 1 ≤ p < q
-    int pair_off[MAXP], pair_ld[MAXP];
-    int pair_p[MAXP], pair_q[MAXP];
-    // ---- l2_kept: chunk groups, items (v, cg) per CTA, warps per item
-    int CG, NCG, ipc, wpi;
-    int64_t kf_stride;     // fibre-index stride of the kept mode m
     int rfs[MAXRD];        // fibre-index stride of reduced mode j
-    int rv_off[MAXRD];     // H_{0,rmode[j]}: column i at rv_off + i·I1p
-    int ks_off[MAXRD], ks_mv[MAXRD], ks_mj[MAXRD];  // H_{m,rmode[j]}(v, i_j) = H[off + v·mv + i_j·mj]
-    int jj_off[MAXJJ], jj_ma[MAXJJ], jj_mb[MAXJJ];  // H_{rmode[j],rmode[j']} = H[off + i_j·ma + i_j'·mb]
+    int rfsI[MAXRD];       // the same in elements (· I1p)
+    int rv_off[MAXRD];     // H_{0,r_j}: column d at rv_off + d·I1p
+    int jj_off[MAXJJ], jj_ma[MAXJJ], jj_mb[MAXJJ];  // H_{r_j,r_j'}(d_j, d_j') = H[off + d_j·ma + d_j'·mb]
+    // scalar factors against the kept outer modes: KEPT: H_{m,r_j}(v, d) = H[ks_off + v·ks_mv + d·ks_mj];
+    // RED: ks_* for mode k (index j = i_k), is_* for mode i (index a = i_i)
+    int ks_off[MAXRD], ks_mv[MAXRD], ks_mj[MAXRD];
+    int is_off[MAXRD], is_mv[MAXRD], is_mj[MAXRD];
+    // ---- l2_kept: chunk groups, items (v, cg) per CTA, warps per item, table elements per item
+    int CG, NCG, ipc, wpi;
+    int lcg, lwpi;         // log2 of CG, wpi
+    int tab_item;          // table elements per item (fp64 elements for orders ≥ 5)
+    int64_t kf_stride;     // fibre-index stride of the kept mode m
+    // ---- l2_red: team size, H_{0,k} / H_{0,i} offsets
+    int TL;
+    int pk_off, pi_off;
     double* scr;           // Z > 1: grid.x·Z·(values per CTA)·2 partials
     unsigned* cnt;         // Z > 1: grid.x arrival counters, zero between launches
 };
 
 constexpr int kL2Threads = 256;
-constexpr int kL2U = 4;  // fibres in flight per thread (kept) / per warp (red)
+constexpr int kL2U = 4;  // cells in flight per thread (l2_red; l2_kept: l2_kept_u)
+#ifndef IFCTN_L2_KEPT_U
+#define IFCTN_L2_KEPT_U 8
+#endif
+// cells in flight per thread of l2_kept: 8 for fp32 tensors of order ≤ 4 (32 registers of X)
+template <typename T>
+__host__ __device__ constexpr int l2_kept_u(int NR) {
+    return (sizeof(T) == 4 && NR <= 2) ? IFCTN_L2_KEPT_U : 4;
+}
 
 // Σ_z scr[z·stride] for z < Z in z order, the loads of 8 partials in flight at a time
 __device__ __forceinline__ double l2_zsum(const double* p, int Z, int64_t stride) {
@@ -89,17 +101,27 @@ __device__ __forceinline__ double l2_zsum(const double* p, int Z, int64_t stride
 }
 
 // ---- KEPT: pair {0, m}; NR = N − 2 reduced outer modes ----------------------------------------
+// Dynamic shared memory: per item (v, cg) the weight tables of its chunk group,
+//   V_j[d][e] = H_{0,r_j}(cg·CGE + e, d) · H_{m,r_j}(v, d),  d < rdim[j], e < CGE,
+// so a cell (chunk, fibre) costs one 16-byte X load, NR 16-byte shared-memory reads and the
+// NR(NR−1)/2 scalars H_{r_j,r_j'}(d_j, d_j').
 template <typename T, int NR>
 __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2Params<T> P) {
     constexpr int VE = 16 / (int)sizeof(T);
-    constexpr int U = kL2U;
+    constexpr int U = l2_kept_u<T>(NR);
+    constexpr int NRa = NR > 0 ? NR : 1;
+    constexpr int NJJ = NR * (NR - 1) / 2;
     using V = typename VecT<T>::V;
+    // orders ≥ 5 (≥ 9 factors per weight): products and sums in fp64 — independent fp32
+    // roundings per entry are full-rank noise to the ill-conditioned column systems
+    using A = std::conditional_t<(NR >= 3), double, T>;
+    extern __shared__ __align__(16) unsigned char l2sm_raw[];
     __shared__ double sm[8 * 2 * 32 * VE];  // [warp][β|ω][chunk lane · VE]
     __shared__ unsigned last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int CG = P.CG, FL = 32 / CG, CGE = CG * VE;
-    const int cl = lane & (CG - 1), fl = lane / CG;
-    const int il = warp / P.wpi, wi = warp - il * P.wpi;
+    const int CG = P.CG, lcg = P.lcg, FL = 32 >> lcg, CGE = CG * VE;
+    const int cl = lane & (CG - 1), fl = lane >> lcg;
+    const int il = warp >> P.lwpi, wi = warp - (il << P.lwpi);
     const int64_t nitems = P.NV * P.NCG;
     const int64_t item = (int64_t)blockIdx.x * P.ipc + il;
     const bool item_ok = item < nitems;
@@ -112,11 +134,12 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
     const int slots = P.wpi * FL;  // fibres of the item per step
     const int r0 = (int)(z * P.FRz), r1 = (int)min(P.FR, (int64_t)r0 + P.FRz);
     int r = r0 + wi * FL + fl;
+    const T* __restrict__ Hb = P.H;
 
     // odometer digits of r and of the step (mixed radix rdim[0..NR))
-    int dg[NR > 0 ? NR : 1], ds[NR > 0 ? NR : 1], dm[NR > 0 ? NR : 1];
+    int dg[NRa], ds[NRa], dm[NRa], tb0[NRa];
     {
-        int rr = min(r, (int)P.FR - 1), ss = slots;
+        int rr = min(r, (int)P.FR - 1), ss = slots, toff = cl * VE;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
             dm[j] = P.rdim[j];
@@ -124,45 +147,49 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
             rr /= dm[j];
             ds[j] = ss % dm[j];
             ss /= dm[j];
+            tb0[j] = toff;
+            toff += dm[j] * CGE;
         }
     }
-    const T* __restrict__ Hb = P.H;
     const T* xb = P.X + (v * P.kf_stride) * I1p + e0;
-    int ksb[NR > 0 ? NR : 1];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) ksb[j] = P.ks_off[j] + (int)v * P.ks_mv[j];
+    A* tab = reinterpret_cast<A*>(l2sm_raw) + (size_t)il * P.tab_item;
 
-    T sb[VE], sw[VE];
+    A sb[VE], sw[VE];
 #pragma unroll
-    for (int e = 0; e < VE; ++e) sb[e] = sw[e] = T(0);
+    for (int e = 0; e < VE; ++e) sb[e] = sw[e] = A(0);
 
-    while (act && r < r1) {
-        V xq[U];
-        T s[U];
-        int ho[U][NR > 0 ? NR : 1];
-        bool val[U];
+    // one round = U cells of this thread: all loads first (X, pair scalars), then the math
+    V xq[U];
+    A s[U];
+    int so[U][NRa];
+    unsigned val = 0;
+    auto issue = [&]() {
+        val = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            val[u] = r + u * slots < r1;
-            int f = 0;
-            T sc = T(1);
-            if (val[u]) {
+            const bool ok = act && r + u * slots < r1;
+            val |= ok ? (1u << u) : 0u;
+            unsigned xo = 0;
+            A sc = A(1);
 #pragma unroll
-                for (int j = 0; j < NR; ++j) {
-                    f += dg[j] * P.rfs[j];
-                    ho[u][j] = P.rv_off[j] + dg[j] * I1p + e0;
-                    sc *= Hb[ksb[j] + dg[j] * P.ks_mj[j]];
+            for (int j = 0; j < NR; ++j) {
+                xo += (unsigned)(dg[j] * P.rfsI[j]);
+                so[u][j] = tb0[j] + dg[j] * CGE;
+            }
+            if (ok) {
+                if constexpr (NJJ > 0) {
+                    T pv[NJJ];
+                    int t = 0;
+#pragma unroll
+                    for (int j = 0; j < NR; ++j)
+#pragma unroll
+                        for (int j2 = j + 1; j2 < NR; ++j2, ++t) pv[t] = Hb[P.jj_off[t] + dg[j] * P.jj_ma[t] + dg[j2] * P.jj_mb[t]];
+#pragma unroll
+                    for (int t2 = 0; t2 < NJJ; ++t2) sc *= (A)pv[t2];
                 }
-                int t = 0;
-#pragma unroll
-                for (int j = 0; j < NR; ++j)
-#pragma unroll
-                    for (int j2 = j + 1; j2 < NR; ++j2, ++t) sc *= Hb[P.jj_off[t] + dg[j] * P.jj_ma[t] + dg[j2] * P.jj_mb[t]];
-                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + (int64_t)f * I1p));
+                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + xo));
             } else {
                 xq[u] = zero_v<T>();
-#pragma unroll
-                for (int j = 0; j < NR; ++j) ho[u][j] = 0;
             }
             s[u] = sc;
             // advance the odometer by one step (digits stay < dm: one conditional subtract)
@@ -174,28 +201,73 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
                 dg[j] = d - (carry ? dm[j] : 0);
             }
         }
+        r += U * slots;
+    };
+    auto compute = [&]() {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (!val[u]) continue;
-            T x[VE], w[VE];
+            if (!(val & (1u << u))) continue;
+            T x[VE];
+            A w[VE];
             VecT<T>::get(xq[u], x);
 #pragma unroll
             for (int e = 0; e < VE; ++e) w[e] = s[u];
 #pragma unroll
             for (int j = 0; j < NR; ++j) {
-                const V hq = *reinterpret_cast<const V*>(Hb + ho[u][j]);
-                T h[VE];
-                VecT<T>::get(hq, h);
+                A h[VE];
+                if constexpr (std::is_same<A, T>::value) {
+                    VecT<T>::get(*reinterpret_cast<const V*>(tab + so[u][j]), h);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) h[e] = tab[so[u][j] + e];
+                }
 #pragma unroll
                 for (int e = 0; e < VE; ++e) w[e] *= h[e];
             }
 #pragma unroll
             for (int e = 0; e < VE; ++e) {
-                sb[e] = fma(w[e], x[e], sb[e]);
+                sb[e] = fma(w[e], (A)x[e], sb[e]);
                 sw[e] = fma(w[e], w[e], sw[e]);
             }
         }
-        r += U * slots;
+    };
+    // first round's loads are in flight while the tables are staged
+    issue();
+    // ---- stage the item's weight tables (its wpi warps) ---------------------------------------
+    if (item_ok) {
+        const int tid = wi * 32 + lane, nt = P.wpi * 32;
+        int toff = 0;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            const int n = P.rdim[j] << lcg;
+            const int ksb = P.ks_off[j] + (int)v * P.ks_mv[j];
+#pragma unroll 4
+            for (int q = tid; q < n; q += nt) {
+                const int d = q >> lcg, c2 = q - (d << lcg);
+                const int ee = (cg * CG + c2) * VE;
+                A h[VE];
+                if (ee < I1p) {
+                    const A a = (A)Hb[ksb + d * P.ks_mj[j]];
+                    const V hq = *reinterpret_cast<const V*>(Hb + P.rv_off[j] + d * I1p + ee);
+                    T ht[VE];
+                    VecT<T>::get(hq, ht);
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) h[e] = (A)ht[e] * a;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) h[e] = A(0);
+                }
+#pragma unroll
+                for (int e = 0; e < VE; ++e) tab[toff + q * VE + e] = h[e];
+            }
+            toff += n * VE;
+        }
+    }
+    __syncthreads();
+    compute();
+    while (act && r < r1) {
+        issue();
+        compute();
     }
     // ---- fibre lanes (xor butterfly, fp64), then the item's warps, then the Z CTAs -----------
     double db[VE], dw[VE];
@@ -251,113 +323,153 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
     if (threadIdx.x == 0) P.cnt[blockIdx.x] = 0u;
 }
 
-// ---- RED: kept pair {k,i} both outer; NCH 16-byte chunks per lane ----------------------------
-template <typename T, int NCH>
+// ---- RED: kept pair {k,i} both outer; NRR = N − 3 reduced outer modes -------------------------
+// A team of TL threads (8 … 256) owns one v = (i_k, i_i) (one z-share of its fibres): the cells
+// (fibre r, 16-byte chunk c) of v are dealt to the team's threads in flat order q = r·NC + c
+// (coalesced: consecutive lanes read consecutive chunks), stepped without divisions.  The
+// v-constant part of the weight, P_v(i_0) = H_{0,k}(i_0, j)·H_{0,i}(i_0, a), is staged once in
+// shared memory per team; per cell: one X load, one shared-memory read, NRR vector loads
+// H_{0,r}(c, d) and the scalars of the fibre.  Everything sums into one (β, ω) pair per v:
+// per-cell fp32, then fp64 over the thread's cells, the team (xor butterfly, warps in order),
+// and the Z CTAs in z order (last CTA to arrive).
+template <typename T, int NRR>
 __global__ void __launch_bounds__(kL2Threads) l2_red(const __grid_constant__ L2Params<T> P) {
     constexpr int VE = 16 / (int)sizeof(T);
     constexpr int U = kL2U;
+    constexpr int NRa = NRR > 0 ? NRR : 1;
+    constexpr int NJJ = NRR * (NRR - 1) / 2;
     using V = typename VecT<T>::V;
+    using A = std::conditional_t<(NRR >= 2), double, T>;  // orders ≥ 5: see l2_kept
+    extern __shared__ __align__(16) unsigned char l2sm_raw[];
     __shared__ double sm[16];
     __shared__ unsigned last;
+    const int TL = P.TL, tpc = kL2Threads / TL;
+    const int team = threadIdx.x / TL, tl = threadIdx.x - team * TL;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int vloc = warp / P.wpv, wv = warp - vloc * P.wpv;
-    const int64_t v = (int64_t)blockIdx.x * P.vpc + vloc;
+    const int64_t v = (int64_t)blockIdx.x * tpc + team;
     const bool v_ok = v < P.NV;
     const int z = blockIdx.y;
-    const int I1p = P.I1p;
-    bool ev[NCH];
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) ev[c] = (c * 32 + lane) * VE < I1p;
-    // lane q holds outer index i_q: kept (fixed by v) or reduced (decoded from r)
-    int kidx = 0, my_div = 1, my_dim = 1;
-    bool my_red = false;
-    if (v_ok) {
-        if (lane == P.k) kidx = (int)(v % P.Ik);
-        if (lane == P.i) kidx = (int)(v / P.Ik);
-    }
-#pragma unroll
-    for (int j = 0; j < MAXN; ++j)
-        if (j < P.nr && lane == P.rmode[j]) {
-            my_div = P.rdiv[j];
-            my_dim = P.rdim[j];
-            my_red = true;
-        }
-    // lane t < npair loads scalar factor t
-    const bool my_pair = lane < P.npair;
-    const int pl = my_pair ? lane : 0;
-    const int my_pp = P.pair_p[pl], my_pq = P.pair_q[pl], my_poff = P.pair_off[pl], my_pld = P.pair_ld[pl];
+    const int I1p = P.I1p, NC = I1p / VE;
+    const int jk = v_ok ? (int)(v % P.Ik) : 0, ai = v_ok ? (int)(v / P.Ik) : 0;
     const T* __restrict__ Hb = P.H;
-    double tb = 0.0, tw = 0.0;
+    // ---- P_v into shared memory ----------------------------------------------------------------
+    T* pv = reinterpret_cast<T*>(l2sm_raw) + (size_t)team * I1p;
+    if (v_ok) {
+        const T* hk = Hb + P.pk_off + jk * I1p;
+        const T* hi = Hb + P.pi_off + ai * I1p;
+        for (int c = tl; c < NC; c += TL) {
+            const V a = *reinterpret_cast<const V*>(hk + c * VE);
+            const V b = *reinterpret_cast<const V*>(hi + c * VE);
+            T x[VE], y[VE];
+            VecT<T>::get(a, x);
+            VecT<T>::get(b, y);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) x[e] *= y[e];
+            *reinterpret_cast<V*>(pv + c * VE) = VecT<T>::make(x);
+        }
+    }
+    // ---- this thread's cells: q = tl + t·TL < ncell ---------------------------------------------
     const int r0 = (int)(z * P.FRz), r1 = (int)min(P.FR, (int64_t)r0 + P.FRz);
-    for (int rb = r0 + wv; v_ok && rb < r1; rb += U * P.wpv) {
-        V xq[U][NCH];
-        T s[U];
-        int ho[U][MAXN - 1];
+    const int ncell = v_ok ? (r1 - r0) * NC : 0;
+    int q = tl;
+    int c = tl % NC;
+    const int dc = TL % NC;
+    int dg[NRa], ds[NRa], dm[NRa], kb[NRa], ib[NRa];
+    {
+        int rr = min(r0 + tl / NC, (int)P.FR - 1), ss = TL / NC;
+#pragma unroll
+        for (int j = 0; j < NRR; ++j) {
+            dm[j] = P.rdim[j];
+            dg[j] = rr % dm[j];
+            rr /= dm[j];
+            ds[j] = ss % dm[j];
+            ss /= dm[j];
+            kb[j] = P.ks_off[j] + jk * P.ks_mv[j];
+            ib[j] = P.is_off[j] + ai * P.is_mv[j];
+        }
+    }
+    const T* xb = P.X + ((int64_t)jk * P.fstride[P.k] + (int64_t)ai * P.fstride[P.i]) * I1p;
+    __syncthreads();
+    double tb = 0.0, tw = 0.0;
+    while (q < ncell) {
+        V xq[U], hq[U][NRa];
+        A s[U];
+        int co[U];
         bool val[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int r = rb + u * P.wpv;
-            val[u] = r < r1;
-            const int rr = val[u] ? r : rb;
-            const int midx = my_red ? (int)(((unsigned)rr / (unsigned)my_div) % (unsigned)my_dim) : kidx;
+            val[u] = q + u * TL < ncell;
+            co[u] = c * VE;
             int f = 0;
 #pragma unroll
-            for (int q = 1; q < MAXN; ++q) {
-                ho[u][q - 1] = 0;
-                if (q < P.N) {
-                    const int iq = __shfl_sync(0xffffffffu, midx, q);
-                    f += iq * (int)P.fstride[q];
-                    ho[u][q - 1] = P.vec_off[q - 1] + iq * I1p;
+            for (int j = 0; j < NRR; ++j) f += dg[j] * P.rfs[j];
+            A sc = A(1);
+            if (val[u]) {
+                T pvv[2 * NRa + (NJJ > 0 ? NJJ : 1)];
+                int t = 0;
+#pragma unroll
+                for (int j = 0; j < NRR; ++j) {
+                    pvv[t++] = Hb[kb[j] + dg[j] * P.ks_mj[j]];
+                    pvv[t++] = Hb[ib[j] + dg[j] * P.is_mj[j]];
                 }
+                int t3 = 0;
+#pragma unroll
+                for (int j = 0; j < NRR; ++j)
+#pragma unroll
+                    for (int j2 = j + 1; j2 < NRR; ++j2, ++t3)
+                        pvv[t++] = Hb[P.jj_off[t3] + dg[j] * P.jj_ma[t3] + dg[j2] * P.jj_mb[t3]];
+#pragma unroll
+                for (int j = 0; j < NRR; ++j) hq[u][j] = *reinterpret_cast<const V*>(Hb + P.rv_off[j] + dg[j] * I1p + co[u]);
+                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + (int64_t)f * I1p + co[u]));
+#pragma unroll
+                for (int t2 = 0; t2 < 2 * NRR + NJJ; ++t2) sc *= (A)pvv[t2];
+            } else {
+                xq[u] = zero_v<T>();
+#pragma unroll
+                for (int j = 0; j < NRR; ++j) hq[u][j] = zero_v<T>();
             }
-            const int ip = __shfl_sync(0xffffffffu, midx, my_pp);
-            const int iq2 = __shfl_sync(0xffffffffu, midx, my_pq);
-            s[u] = my_pair ? Hb[my_poff + iq2 * my_pld + ip] : T(1);
-            const T* xf = P.X + (int64_t)f * I1p;
+            s[u] = sc;
+            // next cell: chunk += dc (mod NC), fibre += ⌊TL/NC⌋ + wrap
+            c += dc;
+            int carry = c >= NC ? 1 : 0;
+            c -= carry ? NC : 0;
 #pragma unroll
-            for (int c = 0; c < NCH; ++c)
-                xq[u][c] = (ev[c] && val[u]) ? ld_stream(reinterpret_cast<const V*>(xf + (c * 32 + lane) * VE)) : zero_v<T>();
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s[u] *= __shfl_xor_sync(0xffffffffu, s[u], o);
+            for (int j = 0; j < NRR; ++j) {
+                int d = dg[j] + ds[j] + carry;
+                carry = (j + 1 < NRR && d >= dm[j]) ? 1 : 0;
+                dg[j] = d - (carry ? dm[j] : 0);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (!val[u]) continue;
-            T pb = T(0), pw = T(0);
+            T x[VE], pe[VE];
+            A w[VE];
+            VecT<T>::get(xq[u], x);
+            const V pq = *reinterpret_cast<const V*>(pv + co[u]);
+            VecT<T>::get(pq, pe);
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                if (!ev[c]) continue;
-                const int e0 = (c * 32 + lane) * VE;
-                T x[VE], w[VE];
-                VecT<T>::get(xq[u][c], x);
+            for (int e = 0; e < VE; ++e) w[e] = (A)pe[e] * s[u];
 #pragma unroll
-                for (int e = 0; e < VE; ++e) w[e] = s[u];
+            for (int j = 0; j < NRR; ++j) {
+                T h[VE];
+                VecT<T>::get(hq[u][j], h);
 #pragma unroll
-                for (int t = 0; t < MAXN - 1; ++t) {
-                    if (t < P.nvec) {
-                        const V hq = *reinterpret_cast<const V*>(Hb + ho[u][t] + e0);
-                        T h[VE];
-                        VecT<T>::get(hq, h);
+                for (int e = 0; e < VE; ++e) w[e] *= (A)h[e];
+            }
+            A pb = A(0), pw = A(0);
 #pragma unroll
-                        for (int e = 0; e < VE; ++e) w[e] *= h[e];
-                    }
-                }
-#pragma unroll
-                for (int e = 0; e < VE; ++e) {
-                    pb = fma(w[e], x[e], pb);
-                    pw = fma(w[e], w[e], pw);
-                }
+            for (int e = 0; e < VE; ++e) {
+                pb = fma(w[e], (A)x[e], pb);
+                pw = fma(w[e], w[e], pw);
             }
             tb += (double)pb;
             tw += (double)pw;
         }
+        q += U * TL;
     }
-    // ---- lanes, then the wpv warps of each v (fixed order), then the Z CTAs -------------------
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    // ---- the team: lanes (xor butterfly inside the team), its warps in order, then the Z CTAs --
+    for (int o = 1; o < 32 && o < TL; o <<= 1) {
         tb += __shfl_xor_sync(0xffffffffu, tb, o);
         tw += __shfl_xor_sync(0xffffffffu, tw, o);
     }
@@ -371,22 +483,26 @@ __global__ void __launch_bounds__(kL2Threads) l2_red(const __grid_constant__ L2P
         P.beta[o] = b;
         P.omega[o] = w;
     };
-    if ((int)threadIdx.x < P.vpc) {
-        const int vl = threadIdx.x;
-        const int64_t vv = (int64_t)blockIdx.x * P.vpc + vl;
-        if (vv < P.NV) {
-            double b = 0.0, w = 0.0;
-            for (int u = 0; u < P.wpv; ++u) {
-                b += sm[2 * (vl * P.wpv + u)];
-                w += sm[2 * (vl * P.wpv + u) + 1];
+    // the first lane of every team finishes its v
+    if (tl == 0 && v_ok) {
+        double b, w;
+        if (TL <= 32) {
+            b = tb;
+            w = tw;
+        } else {
+            b = w = 0.0;
+            const int w0 = threadIdx.x >> 5;
+            for (int u = 0; u < TL / 32; ++u) {
+                b += sm[2 * (w0 + u)];
+                w += sm[2 * (w0 + u) + 1];
             }
-            if (P.Z == 1) {
-                emit(vv, b, w);
-            } else {
-                double* dst = P.scr + (((int64_t)blockIdx.x * P.Z + z) * P.vpc + vl) * 2;
-                dst[0] = b;
-                dst[1] = w;
-            }
+        }
+        if (P.Z == 1) {
+            emit(v, b, w);
+        } else {
+            double* dst = P.scr + (((int64_t)blockIdx.x * P.Z + z) * tpc + team) * 2;
+            dst[0] = b;
+            dst[1] = w;
         }
     }
     if (P.Z == 1) return;
@@ -396,15 +512,170 @@ __global__ void __launch_bounds__(kL2Threads) l2_red(const __grid_constant__ L2P
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if ((int)threadIdx.x < P.vpc) {
-        const int vl = threadIdx.x;
-        const int64_t vv = (int64_t)blockIdx.x * P.vpc + vl;
+    if ((int)threadIdx.x < tpc) {
+        const int64_t vv = (int64_t)blockIdx.x * tpc + threadIdx.x;
         if (vv < P.NV) {
-            const double* src = P.scr + ((int64_t)blockIdx.x * P.Z * P.vpc + vl) * 2;
-            emit(vv, l2_zsum(src, P.Z, (int64_t)P.vpc * 2), l2_zsum(src + 1, P.Z, (int64_t)P.vpc * 2));
+            const double* src = P.scr + ((int64_t)blockIdx.x * P.Z * tpc + threadIdx.x) * 2;
+            emit(vv, l2_zsum(src, P.Z, (int64_t)tpc * 2), l2_zsum(src + 1, P.Z, (int64_t)tpc * 2));
         }
     }
     if (threadIdx.x == 0) P.cnt[blockIdx.x] = 0u;
+}
+
+// ---- a5 for L2-resident tensors: X ← Ω ? X : (t + ρX)/(1+ρ), t = Π_{p<q} H_{p,q} (Eq. 9 in
+// reading R1) and the three norms of the sweep row ---------------------------------
+// Same cell mapping as l2_kept with every outer mode "reduced": a CTA owns one chunk group of
+// mode 1 and a z-share of all fibres; its tables V_q[d][e] = H_{0,q}(cg·CGE + e, d) sit in shared
+// memory; per cell one X load, the Ω word, NO table reads, the NO(NO−1)/2 scalars H_{q,q'}, one
+// X store.  Norm partials: fp32 per thread (≤ a few rounds), fp64 across lanes and warps in
+// fixed order, one row per CTA for finalize_norms.
+template <typename T>
+struct L2RefillParams {
+    T* X;
+    const T* H;
+    const uint32_t* mask;
+    double* norms;        // 3 per CTA (grid.x·z + x)
+    T rho, inv1p;
+    int I1p;
+    int64_t nfib, FRz;
+    int CG, lcg, NCG;
+    int dim[MAXN - 1];    // outer mode dims, mode order (fibre index = mixed radix, mode 2 fastest)
+    int ds[MAXN - 1];     // digits of the per-step fibre stride 8·32/CG
+    int tv_off[MAXN - 1]; // H_{0,q}
+    int pp_off[MAXP], pp_ld[MAXP];  // H_{q,q'}(i_q, i_q') = H[off + i_q'·ld + i_q], pairs in (q, q') order
+};
+
+template <typename T, int NO>
+__global__ void __launch_bounds__(kL2Threads) l2_refill(const __grid_constant__ L2RefillParams<T> P) {
+    constexpr int VE = 16 / (int)sizeof(T);
+    constexpr int U = kL2U;
+    constexpr int NPP = NO * (NO - 1) / 2;
+    using V = typename VecT<T>::V;
+    extern __shared__ __align__(16) unsigned char l2sm_raw[];
+    __shared__ double sm[8 * 3];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int CG = P.CG, lcg = P.lcg, FL = 32 >> lcg, CGE = CG * VE;
+    const int cl = lane & (CG - 1), fl = lane >> lcg;
+    const int cg = blockIdx.x, z = blockIdx.y;
+    const int I1p = P.I1p;
+    const int e0 = (cg * CG + cl) * VE;
+    const bool act = e0 < I1p;
+    const int slots = 8 * FL;
+    const int f0 = (int)(z * P.FRz), f1 = (int)min(P.nfib, (int64_t)f0 + P.FRz);
+    int f = f0 + warp * FL + fl;
+    const T* __restrict__ Hb = P.H;
+    T* tab = reinterpret_cast<T*>(l2sm_raw);
+    // tables
+    {
+        int toff = 0;
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+            const int n = P.dim[q] << lcg;
+#pragma unroll 4
+            for (int t = threadIdx.x; t < n; t += kL2Threads) {
+                const int d = t >> lcg, c2 = t - (d << lcg);
+                const int ee = (cg * CG + c2) * VE;
+                V hq = zero_v<T>();
+                if (ee < I1p) hq = *reinterpret_cast<const V*>(Hb + P.tv_off[q] + d * I1p + ee);
+                *reinterpret_cast<V*>(tab + toff + t * VE) = hq;
+            }
+            toff += n * VE;
+        }
+    }
+    int dg[NO], dm[NO], ds[NO], tb0[NO];
+    {
+        int rr = min(f, (int)P.nfib - 1), toff = cl * VE;
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+            dm[q] = P.dim[q];
+            ds[q] = P.ds[q];
+            dg[q] = q + 1 < NO ? rr % dm[q] : rr;
+            rr /= dm[q];
+            tb0[q] = toff;
+            toff += dm[q] * CGE;
+        }
+    }
+    __syncthreads();
+    Norms3<T> qn;
+    T* xb = P.X + e0;
+    while (act && f < f1) {
+        V xq[U];
+        T s[U];
+        uint32_t mw[U];
+        int so[U][NO];
+        unsigned val = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int fu = f + u * slots;
+            const bool ok = fu < f1;
+            val |= ok ? (1u << u) : 0u;
+            T sc = T(1);
+#pragma unroll
+            for (int q = 0; q < NO; ++q) so[u][q] = tb0[q] + dg[q] * CGE;
+            if (ok) {
+                if constexpr (NPP > 0) {
+                    T pv[NPP];
+                    int t = 0;
+#pragma unroll
+                    for (int q = 0; q < NO; ++q)
+#pragma unroll
+                        for (int q2 = q + 1; q2 < NO; ++q2, ++t) pv[t] = Hb[P.pp_off[t] + dg[q2] * P.pp_ld[t] + dg[q]];
+#pragma unroll
+                    for (int t2 = 0; t2 < NPP; ++t2) sc *= pv[t2];
+                }
+                const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
+                mw[u] = P.mask[g >> 5] >> (g & 31u);
+                xq[u] = *reinterpret_cast<const V*>(xb + (size_t)fu * I1p);
+            } else {
+                xq[u] = zero_v<T>();
+                mw[u] = ~0u;
+            }
+            s[u] = sc;
+            int carry = 0;
+#pragma unroll
+            for (int q = 0; q < NO; ++q) {
+                int d = dg[q] + ds[q] + carry;
+                carry = (q + 1 < NO && d >= dm[q]) ? 1 : 0;
+                dg[q] = d - (carry ? dm[q] : 0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!(val & (1u << u))) continue;
+            T x[VE], t[VE], xn[VE];
+            VecT<T>::get(xq[u], x);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) t[e] = s[u];
+#pragma unroll
+            for (int q = 0; q < NO; ++q) {
+                T h[VE];
+                VecT<T>::get(*reinterpret_cast<const V*>(tab + so[u][q]), h);
+#pragma unroll
+                for (int e = 0; e < VE; ++e) t[e] *= h[e];
+            }
+            refill_chunk<T, VE>(x, t, mw[u], P.rho, P.inv1p, xn, qn);
+            *reinterpret_cast<V*>(xb + (size_t)(f + u * slots) * I1p) = VecT<T>::make(xn);
+        }
+        f += U * slots;
+    }
+    double n0 = qn.s0(), n1 = qn.s1(), n2 = qn.s2();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+        n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    }
+    if (lane == 0) {
+        sm[warp * 3 + 0] = n0;
+        sm[warp * 3 + 1] = n1;
+        sm[warp * 3 + 2] = n2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double a = 0.0;
+        for (int w = 0; w < 8; ++w) a += sm[w * 3 + threadIdx.x];
+        P.norms[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 3 + threadIdx.x] = a;
+    }
 }
 
 }  // namespace ifctn

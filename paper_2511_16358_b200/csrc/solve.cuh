@@ -419,6 +419,200 @@ __host__ __device__ inline size_t big_solve_smem(int R, int ta, int /*esize*/) {
     return sizeof(double) * ((size_t)ta * R + Rp + (size_t)Rp * big_solve_lda(R) + 2 * (size_t)ta + 3 * (size_t)Rp);
 }
 
+// G_{i,k}(:, a0 …) (n = na·R elements of T) into shared memory as fp64, followed by `pad` zeros
+// (the tiles over-read 4-wide): 16-byte loads when the source allows, every load of a thread
+// in flight before its stores (one L2 round trip for the whole tile).
+template <typename T>
+__device__ __forceinline__ void stage_factor_fp64(const T* src, int n, int pad, double* gs, int tid, int nthr) {
+    constexpr int VE = 16 / (int)sizeof(T);
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    const int nv = vec ? n / VE : 0;
+    using V = typename VecT<T>::V;
+    for (int base = 0; base < nv; base += 8 * nthr) {
+        V v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * nthr + tid;
+            v[u] = e < nv ? reinterpret_cast<const V*>(src)[e] : zero_v<T>();
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * nthr + tid;
+            if (e < nv) {
+                T t[VE];
+                VecT<T>::get(v[u], t);
+#pragma unroll
+                for (int q = 0; q < VE; ++q) gs[e * VE + q] = (double)t[q];
+            }
+        }
+    }
+    for (int base = nv * VE; base < n; base += 8 * nthr) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * nthr + tid;
+            v[u] = e < n ? src[e] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * nthr + tid;
+            if (e < n) gs[e] = (double)v[u];
+        }
+    }
+    for (int e = n + tid; e < n + pad; e += nthr) gs[e] = 0.0;
+}
+
+// ---- a3 for large ranks on one GPU: Gram/RHS of every column as a register-tiled fp64 product --
+// proj[j] = [Σ_a ω(a,j) g_a g_aᵀ (upper triangle, row-major), Σ_a β(a,j) g_a]  (Eq. 8)
+// for two columns j per CTA: the 4×4 tile products g_a[r]·g_a[s] are formed once per a and
+// shared by both columns (the per-column kernel was bound by the shared-memory reads of g_a:
+// 9 loads per 20 fp64 operations; here 5 per 48).  Same task split and fixed-order a-partials
+// as block_solve_big; block_solve_big<SOLVE_FROM_PROJ> then adds ρI, factors and solves.
+constexpr int kGramCols = 2;
+__host__ __device__ inline size_t gram_project_smem(int R, int ta) {
+    const int Rp = big_solve_rp(R);
+    const size_t gsz = (size_t)ta * R + Rp, psz = (size_t)16 * kGramCols * kBigThreads;  // staged factor | partial tiles
+    return sizeof(double) * ((gsz > psz ? gsz : psz) + kGramCols * 2 * (size_t)ta);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBigThreads) gram_project(const SolveParams<T> P) {
+    extern __shared__ __align__(16) double bsm[];
+    const int R = P.R, Rp = big_solve_rp(R), TA = P.ta;
+    const int NG = R * (R + 1) / 2, NA = NG + R;
+    double* gs = bsm;                          // G_{i,k}(:, a0 .. a0+ta) as fp64, row stride R
+    const size_t gsz = (size_t)TA * R + Rp, psz = (size_t)16 * kGramCols * kBigThreads;
+    double* om = gs + (gsz > psz ? gsz : psz); // [a][col] ω, then β
+    double* be = om + kGramCols * (size_t)TA;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+#ifdef IFCTN_EXP_PHASE_CLOCKS
+    long long gclk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define GCLK(q) if (blockIdx.x == 0 && threadIdx.x == 0) gclk[q] = clock64();
+#else
+#define GCLK(q)
+#endif
+    GCLK(0);
+    const int64_t j0 = (int64_t)blockIdx.x * kGramCols;
+    const int ncol = (int)min((int64_t)kGramCols, P.Ik - j0);
+    const int nt = Rp / 4;
+    const int ntg = nt * (nt + 1) / 2;
+    const int ntasks = ntg + nt;
+    const int KS = max(1, min(8, nthr / ntasks));
+    const int task_t = tid % ntasks, task_h = tid / ntasks;
+    const bool has_task = task_h < KS;
+    const bool is_rhs = task_t >= ntg;
+    int tr = 0, ts = 0;
+    if (has_task) {
+        if (is_rhs) {
+            tr = task_t - ntg;
+        } else {
+            int q = task_t;
+            while (q >= nt - tr) {
+                q -= nt - tr;
+                ++tr;
+            }
+            ts = tr + q;
+        }
+    }
+    double acc[kGramCols][4][4];
+#pragma unroll
+    for (int c = 0; c < kGramCols; ++c)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[c][u][v] = 0.0;
+    for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
+        const int na = (int)min((int64_t)TA, P.Ii - a0);
+        __syncthreads();
+        stage_factor_fp64<T>(P.Gik + a0 * R, na * R, Rp, gs, tid, nthr);
+        GCLK(1);
+        for (int q = tid; q < na * kGramCols; q += nthr) {
+            const int c = q / na, a = q - c * na;
+            const bool okc = c < ncol;
+            om[a * kGramCols + c] = okc ? P.omega[(j0 + c) * P.Ii + a0 + a] : 0.0;
+            be[a * kGramCols + c] = okc ? P.beta[(j0 + c) * P.Ii + a0 + a] : 0.0;
+        }
+        __syncthreads();
+        GCLK(2);
+        if (has_task) {
+            if (is_rhs) {
+                for (int a = task_h; a < na; a += KS) {
+                    const double* gr = gs + a * R + 4 * tr;
+#pragma unroll
+                    for (int c = 0; c < kGramCols; ++c) {
+                        const double b = be[a * kGramCols + c];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[c][u][0] = fma(b, gr[u], acc[c][u][0]);
+                    }
+                }
+            } else {
+#pragma unroll 2
+                for (int a = task_h; a < na; a += KS) {
+                    const double* gr = gs + a * R + 4 * tr;
+                    const double* gc = gs + a * R + 4 * ts;
+                    double q[4][4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) q[u][v] = gr[u] * gc[v];
+#pragma unroll
+                    for (int c = 0; c < kGramCols; ++c) {
+                        const double w = om[a * kGramCols + c];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) acc[c][u][v] = fma(w, q[u][v], acc[c][u][v]);
+                    }
+                }
+            }
+        }
+    }
+    GCLK(3);
+    // partial tiles into shared memory (over the staged factor, no longer needed): element e of
+    // thread tid at part[e·nthr + tid] (conflict-free); then entry (c, r, s) = Σ_h in h order
+    __syncthreads();
+    double* part = gs;
+    if (has_task) {
+#pragma unroll
+        for (int c = 0; c < kGramCols; ++c)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) part[(c * 16 + u * 4 + v) * nthr + tid] = acc[c][u][v];
+    }
+    __syncthreads();
+    GCLK(4);
+    for (int q = tid; q < 16 * kGramCols * ntasks; q += nthr) {
+        const int e = q / ntasks, t = q - e * ntasks;
+        const int c = e >> 4, u = (e >> 2) & 3, v = e & 3;
+        if (c >= ncol) continue;
+        int idx;
+        if (t < ntg) {
+            int r4 = 0, qq = t;
+            while (qq >= nt - r4) {
+                qq -= nt - r4;
+                ++r4;
+            }
+            const int r = 4 * r4 + u, sc = 4 * (r4 + qq) + v;
+            if (r > sc || sc >= R) continue;
+            idx = r * R - r * (r - 1) / 2 + (sc - r);
+        } else {
+            const int r = 4 * (t - ntg) + u;
+            if (v != 0 || r >= R) continue;
+            idx = NG + r;
+        }
+        double sum = 0.0;
+        for (int h = 0; h < KS; ++h) sum += part[e * nthr + h * ntasks + t];
+        P.proj[(j0 + c) * NA + idx] = sum;
+    }
+    GCLK(5);
+#ifdef IFCTN_EXP_PHASE_CLOCKS
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("gram_project R=%d phases (cycles): stage %lld  om/be %lld  gram %lld  reduce %lld  out %lld\n", R,
+               gclk[1] - gclk[0], gclk[2] - gclk[1], gclk[3] - gclk[2], gclk[4] - gclk[3], gclk[5] - gclk[4]);
+#endif
+}
+
 #ifdef IFCTN_EXP_PHASE_CLOCKS  // diagnosis builds only: per-phase clocks of CTA 0
 #define PHASE_CLK(q) \
     if (j == 0 && threadIdx.x == 0) clk[q] = clock64();
@@ -468,24 +662,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             ts = tr + q;
         }
     }
-    auto stage = [&](int64_t a0, int na) {
-        const T* src = P.Gik + a0 * R;
-        const int n = na * R;
-        for (int base = 0; base < n; base += 8 * nthr) {
-            T v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int e = base + u * nthr + tid;
-                v[u] = e < n ? src[e] : T(0);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int e = base + u * nthr + tid;
-                if (e < n) gs[e] = (double)v[u];
-            }
-        }
-        for (int e = n + tid; e < n + Rp; e += nthr) gs[e] = 0.0;  // 4-wide over-read
-    };
+    auto stage = [&](int64_t a0, int na) { stage_factor_fp64<T>(P.Gik + a0 * R, na * R, Rp, gs, tid, nthr); };
     if constexpr (SM != SOLVE_FROM_PROJ) {
         double acc[4][4];
 #pragma unroll
