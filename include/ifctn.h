@@ -75,9 +75,15 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
                                      value, no partial slots; csrc/l2pass.cuh)               */
 #define IFCTN_FLAG_NO_FUSE 16u  /* diagnostic: never fuse a sweep's X update into the next
                                    sweep's first block (see ifctn_sweep)                      */
-#define IFCTN_FLAG_NO_GRAM_GEMM 256u /* diagnostic: large ranks (R > 9) build Gram_j and rhs_j
-                                        inside the per-column solve instead of the two-column
-                                        register-tiled gram_project kernel                    */
+#define IFCTN_FLAG_NO_PDL 512u /* diagnostic: plain stream order for every launch (default: the
+                                  L2-pass, solve and finaliser kernels are launched with
+                                  programmatic stream serialization and wait for their
+                                  predecessor themselves, griddepcontrol.wait)              */
+#define IFCTN_FLAG_GRAM_GEMM 256u /* experiment: large ranks (R > 9) build Gram_j and rhs_j of
+                                     two columns per CTA in a separate register-tiled kernel
+                                     (gram_project), then the FROM_PROJ solve; measured slower
+                                     than the per-column solve on one GPU (C2r: 46.6 vs 42.0 us
+                                     per block), so off by default                          */
 
 /* Multi-GPU description (one process per GPU).  NULL or world == 1: single GPU.
  * Sharding: X and Ω are split along the shard mode s; the factor chains

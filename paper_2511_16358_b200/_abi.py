@@ -20,7 +20,8 @@ IFCTN_FLAG_NONE, IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_X_FULL, IFCTN_FLAG_NO_VBLOCK = 
 IFCTN_FLAG_NO_FUSE = 16
 IFCTN_FLAG_NO_SOLVE_REDUCE = 64
 IFCTN_FLAG_NO_L2PASS = 128
-IFCTN_FLAG_NO_GRAM_GEMM = 256
+IFCTN_FLAG_GRAM_GEMM = 256
+IFCTN_FLAG_NO_PDL = 512
 IFCTN_MAX_ORDER, IFCTN_MAX_RANK = 6, 64
 
 STATUS = ["IFCTN_OK", "IFCTN_E_ARG", "IFCTN_E_SHAPE", "IFCTN_E_RANKS", "IFCTN_E_WORKSPACE",

@@ -215,6 +215,16 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
     } while (!done);
 }
 
+// ---- programmatic dependent launch (sm_90+): a kernel launched with the programmatic stream
+// serialization attribute starts while its predecessor still runs; pdl_wait() blocks until the
+// predecessor grid has completed and its memory is visible, pdl_launch() lets the successor's
+// CTAs be scheduled.  Rule used here: wait FIRST, then launch — so everything older than the
+// direct predecessor is complete when a kernel passes its wait, and only work that does not
+// touch the predecessor's outputs (index arithmetic) sits before the wait.  Without the launch
+// attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // One fiber pass = one streaming sweep over the (local) X in fibre order.  A "fibre" is a
 // mode-1 line X(:, i_2, …, i_N) stored contiguously with I1p ≥ I1 padded entries (pad = 0).
 // Fibres are enumerated as pos = v·FR + r, v over the kept outer modes, r over the reduced

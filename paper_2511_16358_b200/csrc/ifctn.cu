@@ -620,15 +620,32 @@ struct Solver : SolverBase {
         prof_ev.push_back(e);
     }
 
+    // pdl: the kernel calls pdl_wait() before it touches its predecessor's outputs, so it may be
+    // launched with programmatic stream serialization (its launch and index prologue overlap the
+    // predecessor's tail; captured into the sweep graphs as programmatic edges)
     template <typename P>
-    void launch(const void* fn, dim3 g, dim3 b, size_t smem, const P& p) {
+    void launch(const void* fn, dim3 g, dim3 b, size_t smem, const P& p, bool pdl = false) {
         prof_mark();
         void* args[] = {(void*)&p};
-        launch_raw(fn, g, b, smem, args);
+        launch_raw(fn, g, b, smem, args, pdl);
     }
 
-    void launch_raw(const void* fn, dim3 g, dim3 b, size_t smem, void** args) {
-        CU(cudaLaunchKernel(fn, g, b, args, smem, st));
+    void launch_raw(const void* fn, dim3 g, dim3 b, size_t smem, void** args, bool pdl = false) {
+        if (pdl && !(flags & IFCTN_FLAG_NO_PDL)) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = g;
+            cfg.blockDim = b;
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute at{};
+            at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at.val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = &at;
+            cfg.numAttrs = 1;
+            CU(cudaLaunchKernelExC(&cfg, fn, args));
+        } else {
+            CU(cudaLaunchKernel(fn, g, b, args, smem, st));
+        }
         ++ctr;
     }
 
@@ -874,17 +891,13 @@ struct Solver : SolverBase {
     static const void* pick_l2_kept(int nr) {
         switch (nr) {
             case 1: return (const void*)l2_kept<T, 1>;
-            case 2: return (const void*)l2_kept<T, 2>;
-            case 3: return (const void*)l2_kept<T, 3>;
-            default: return (const void*)l2_kept<T, 4>;
+            default: return (const void*)l2_kept<T, 2>;
         }
     }
     static const void* pick_l2_red(int nrr) {
         switch (nrr) {
             case 0: return (const void*)l2_red<T, 0>;
-            case 1: return (const void*)l2_red<T, 1>;
-            case 2: return (const void*)l2_red<T, 2>;
-            default: return (const void*)l2_red<T, 3>;
+            default: return (const void*)l2_red<T, 1>;
         }
     }
 
@@ -927,17 +940,29 @@ struct Solver : SolverBase {
         P.NV = kept1 ? s.ld[P.m] : s.ld[k] * s.ld[i];
         P.FR = 1;
         int64_t rsum = 0;
-        for (int q = 1; q < N; ++q) {
-            const bool kept = kept1 ? (q == P.m) : (q == k || q == i);
-            if (kept) continue;
-            P.rmode[P.nr] = q;
-            P.rdim[P.nr] = (int)s.ld[q];
-            P.rfs[P.nr] = (int)s.fstride[q];
-            P.rfsI[P.nr] = (int)(s.fstride[q] * s.I1p);
-            P.rv_off[P.nr] = (int)s.hoff[0][q];
-            ++P.nr;
-            P.FR *= s.ld[q];
-            rsum += s.ld[q];
+        {
+            int rm[MAXN], nrm = 0;
+            for (int q = 1; q < N; ++q) {
+                const bool kept = kept1 ? (q == P.m) : (q == k || q == i);
+                if (!kept) rm[nrm++] = q;
+            }
+            // odometer order: mode order (first fastest), except that the longest reduced mode
+            // leads (l2_kept walks it in runs of kL2RunU cells)
+            int lead = 0;
+            for (int t = 1; t < nrm; ++t)
+                if (s.ld[rm[t]] > s.ld[rm[lead]]) lead = t;
+            if (nrm > 0) std::rotate(rm, rm + lead, rm + lead + 1);
+            for (int t = 0; t < nrm; ++t) {
+                const int q = rm[t];
+                P.rmode[P.nr] = q;
+                P.rdim[P.nr] = (int)s.ld[q];
+                P.rfs[P.nr] = (int)s.fstride[q];
+                P.rfsI[P.nr] = (int)(s.fstride[q] * s.I1p);
+                P.rv_off[P.nr] = (int)s.hoff[0][q];
+                ++P.nr;
+                P.FR *= s.ld[q];
+                rsum += s.ld[q];
+            }
         }
         if (P.FR >= (1LL << 31) || P.NV >= (1LL << 31)) return false;
         // H_{p,r_j}(x, d) for a kept outer mode p: H[off + x·mv + d·mj]
@@ -957,10 +982,16 @@ struct Solver : SolverBase {
             int t = 0;
             for (int j = 0; j < P.nr; ++j)
                 for (int j2 = j + 1; j2 < P.nr; ++j2, ++t) {
-                    const int q = P.rmode[j], q2 = P.rmode[j2];  // q < q2
-                    P.jj_off[t] = (int)s.hoff[q][q2];
-                    P.jj_ma[t] = 1;
-                    P.jj_mb[t] = (int)s.hld[q];
+                    const int q = P.rmode[j], q2 = P.rmode[j2];
+                    if (q < q2) {
+                        P.jj_off[t] = (int)s.hoff[q][q2];
+                        P.jj_ma[t] = 1;
+                        P.jj_mb[t] = (int)s.hld[q];
+                    } else {
+                        P.jj_off[t] = (int)s.hoff[q2][q];
+                        P.jj_ma[t] = (int)s.hld[q2];
+                        P.jj_mb[t] = 1;
+                    }
                 }
         }
         P.scr = rscr;
@@ -974,32 +1005,41 @@ struct Solver : SolverBase {
         const size_t smem_cap = std::min<size_t>(smem_limit > 24 * 1024 ? smem_limit - 24 * 1024 : 0, 96 * 1024);
         const int NC = (int)(s.I1p / VE);
         double best = 1e300;
+        // diagnosis: IFCTN_L2_KEPT="CG,wpi,Z" / IFCTN_L2_RED="TL,Z" pin the split (0 = free)
+        int pin[3] = {0, 0, 0};
+        if (const char* e = getenv(kept1 ? "IFCTN_L2_KEPT" : "IFCTN_L2_RED")) sscanf(e, "%d,%d,%d", &pin[0], &pin[1], &pin[2]);
         if (kept1) {
             const int NR = N - 2;
             P.kf_stride = s.fstride[P.m];
             for (int j = 0; j < NR; ++j) kept_scalar(P.m, j, P.ks_off, P.ks_mv, P.ks_mj);
             b.l2_fn = pick_l2_kept(NR);
             CU(cudaFuncSetAttribute(b.l2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
-            const int64_t tab_esize = NR >= 3 ? 8 : s.esize;  // fp64 tables for orders ≥ 5
-            const int KU = l2_kept_u<T>(NR);
+            const int64_t tab_esize = s.esize;
+            // work units of a kept value: runs of kL2RunU cells along reduced mode r_0
+            P.nb0 = (int)cdiv(P.rdim[0], kL2RunU);
+            P.FR = (P.FR / P.rdim[0]) * P.nb0;
             for (int CG = 1; CG <= 32; CG <<= 1) {
                 if (CG < 4 && CG < NC) continue;      // ≥ 64 contiguous bytes per fibre piece
                 if (CG > 4 && CG >= 2 * NC) continue;
+                if (pin[0] && CG != pin[0]) continue;
                 const int FL = 32 / CG;
                 const int64_t NCG = cdiv(NC, CG);
                 const double waste = (double)(NCG * CG) / NC;
                 const int64_t tab_item = rsum * CG * VE;
                 for (int wpi = 1; wpi <= 8; wpi <<= 1) {
+                    if (pin[1] && wpi != pin[1]) continue;
                     const int ipc = 8 / wpi;
                     const size_t smem = (size_t)ipc * tab_item * tab_esize;
                     if (smem > smem_cap) continue;
                     const int64_t resident = resident_ctas(b.l2_fn, smem);
+                    if (P.NV * NCG >= (1LL << 30)) continue;
                     const int64_t nbx = cdiv(P.NV * NCG, ipc);
                     const int64_t slots = (int64_t)wpi * FL;
                     for (int Z : kZs) {
+                        if (pin[2] && Z != pin[2]) continue;
                         if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * ipc * 2 * CG * VE > kRedScr)) continue;
                         const int64_t FRz = cdiv(P.FR, Z), Ze = cdiv(P.FR, FRz);
-                        const int64_t rounds = cdiv(cdiv(FRz, slots), KU);
+                        const int64_t rounds = cdiv(FRz, slots);
                         const int64_t waves = cdiv(nbx * Ze, resident);
                         const double stage = (double)cdiv(rsum * CG, wpi * 32) / 4;  // table rounds
                         const double cost = waves * (1.5 + stage + rounds * waste) + (Ze > 1 ? 1.0 : 0.0) +
@@ -1034,12 +1074,14 @@ struct Solver : SolverBase {
             b.l2_fn = pick_l2_red(NRR);
             CU(cudaFuncSetAttribute(b.l2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
             for (int TL = 8; TL <= kL2Threads; TL <<= 1) {
+                if (pin[0] && TL != pin[0]) continue;
                 const int tpc = kL2Threads / TL;
                 const size_t smem = (size_t)tpc * s.I1p * s.esize;
                 if (smem > smem_cap) continue;
                 const int64_t resident = resident_ctas(b.l2_fn, smem);
                 const int64_t nbx = cdiv(P.NV, tpc);
                 for (int Z : kZs) {
+                    if (pin[1] && Z != pin[1]) continue;
                     if (Z > 1 && (Z > P.FR || nbx > kRedCnt || nbx * Z * tpc * 2 > kRedScr)) continue;
                     const int64_t FRz = cdiv(P.FR, Z), Ze = cdiv(P.FR, FRz);
                     const int64_t rounds = cdiv(cdiv(FRz * NC, TL), kL2U);
@@ -1058,6 +1100,18 @@ struct Solver : SolverBase {
             }
         }
         if (best >= 1e300) return false;
+        if (getenv("IFCTN_L2_VERBOSE"))
+            fprintf(stderr, "l2 block (%d,%d) %s NV %lld FR %lld: CG %d wpi %d TL %d Z %d grid %u x %u smem %zu\n", k, i,
+                    kept1 ? "kept" : "red", (long long)P.NV, (long long)P.FR, P.CG, P.wpi, P.TL, P.Z, b.l2_grid.x,
+                    b.l2_grid.y, b.l2_smem);
+        if (kept1) {  // digits of the per-step run stride
+            int64_t st = (int64_t)P.wpi * (32 / P.CG);
+            for (int j = 0; j < P.nr; ++j) {
+                const int64_t radix = j == 0 ? P.nb0 : P.rdim[j];
+                P.dsr[j] = (int)(st % radix);
+                st /= radix;
+            }
+        }
         b.l2 = true;
         return true;
     }
@@ -1066,9 +1120,7 @@ struct Solver : SolverBase {
         switch (no) {
             case 1: return (const void*)l2_refill<T, 1>;
             case 2: return (const void*)l2_refill<T, 2>;
-            case 3: return (const void*)l2_refill<T, 3>;
-            case 4: return (const void*)l2_refill<T, 4>;
-            default: return (const void*)l2_refill<T, 5>;
+            default: return (const void*)l2_refill<T, 3>;
         }
     }
 
@@ -1236,7 +1288,7 @@ struct Solver : SolverBase {
                     b.proj_fn = pick_solve<T>(R, SOLVE_PROJECT);
                     b.sol_fn = pick_solve<T>(R, SOLVE_FROM_PROJ);
                     b.proj_count = s.ld[k] * (R * (R + 1) / 2 + R);
-                } else if (q.R > MAXR_SMALL && !(flags & IFCTN_FLAG_NO_GRAM_GEMM)) {
+                } else if (q.R > MAXR_SMALL && (flags & IFCTN_FLAG_GRAM_GEMM)) {
                     // one GPU, large rank: two columns per CTA share the g_a g_aᵀ tile products
                     b.gemm = true;
                     b.gram_sol = q;
@@ -1299,7 +1351,7 @@ struct Solver : SolverBase {
     // ifctn_profile_sweep still reports [pass, reduce, solve] per block.
     void enqueue_contract(const BlockPlan<T>& b, bool full = false) {
         if (b.l2) {  // one launch writes β, ω whole; an empty interval for the reduce slot
-            launch(b.l2_fn, b.l2_grid, dim3(kL2Threads), b.l2_smem, b.l2p);
+            launch(b.l2_fn, b.l2_grid, dim3(kL2Threads), b.l2_smem, b.l2p, true);
             prof_mark();
             return;
         }
@@ -1313,14 +1365,14 @@ struct Solver : SolverBase {
         if (b.gemm) {  // both launches in the block's solve interval of ifctn_profile_sweep
             launch((const void*)gram_project<T>, b.gram_grid, dim3(kBigThreads), b.gram_smem, b.gram_sol);
             void* args[] = {(void*)&b.gram_sol};
-            launch_raw(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, args);
+            launch_raw(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, args, true);
             return;
         }
         if (b.dist) {  // peer exchange: the solve below publishes, waits and sums itself
             launch(b.proj_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
             if (!s.peer) allreduce_dev(proj, (size_t)b.proj_count);
         }
-        launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q);
+        launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q, !b.dist);
     }
 
     void enqueue_block(const BlockPlan<T>& b) {
@@ -1338,7 +1390,7 @@ struct Solver : SolverBase {
             int64_t a1 = ngroups, a3 = obj_only ? 0 : s.ndelta, a4 = sh_off, a5 = sh_len;
             int a9 = obj_only, a10 = multi ? 0 : 1;
             void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5, &p5, &scal, &dflags, &a9, &a10};
-            launch_raw((const void*)finalize_norms, dim3(1), dim3(1024), 0, args);
+            launch_raw((const void*)finalize_norms, dim3(1), dim3(1024), 0, args, true);
         }
         if (multi) {
             allreduce_dev(p5, 4);
@@ -1351,7 +1403,7 @@ struct Solver : SolverBase {
 
     void enqueue_xupdate() {
         if (l2r) {
-            launch(l2r_fn, l2r_grid, dim3(kL2Threads), l2r_smem, l2rp);
+            launch(l2r_fn, l2r_grid, dim3(kL2Threads), l2r_smem, l2rp, true);
             enqueue_finalize((int64_t)l2r_grid.x * l2r_grid.y, 0);
             return;
         }

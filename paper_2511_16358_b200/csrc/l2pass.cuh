@@ -57,6 +57,8 @@ struct L2Params {
     int rdim[MAXN];
     int rfs[MAXRD];        // fibre-index stride of reduced mode j
     int rfsI[MAXRD];       // the same in elements (· I1p)
+    int nb0;               // l2_kept: runs along reduced mode r_0, ⌈rdim[0] / kL2RunU⌉
+    int dsr[MAXRD];        // l2_kept: digits of the per-step run stride (radix nb0, rdim[1], …)
     int rv_off[MAXRD];     // H_{0,r_j}: column d at rv_off + d·I1p
     int jj_off[MAXJJ], jj_ma[MAXJJ], jj_mb[MAXJJ];  // H_{r_j,r_j'}(d_j, d_j') = H[off + d_j·ma + d_j'·mb]
     // scalar factors against the kept outer modes: KEPT: H_{m,r_j}(v, d) = H[ks_off + v·ks_mv + d·ks_mj];
@@ -77,14 +79,13 @@ struct L2Params {
 
 constexpr int kL2Threads = 256;
 constexpr int kL2U = 4;  // cells in flight per thread (l2_red; l2_kept: l2_kept_u)
-#ifndef IFCTN_L2_KEPT_U
-#define IFCTN_L2_KEPT_U 8
+#ifndef IFCTN_L2_RUN_U
+#define IFCTN_L2_RUN_U 8
 #endif
-// cells in flight per thread of l2_kept: 8 for fp32 tensors of order ≤ 4 (32 registers of X)
-template <typename T>
-__host__ __device__ constexpr int l2_kept_u(int NR) {
-    return (sizeof(T) == 4 && NR <= 2) ? IFCTN_L2_KEPT_U : 4;
-}
+constexpr int kL2RunU = IFCTN_L2_RUN_U;
+#ifndef IFCTN_L2_MINB
+#define IFCTN_L2_MINB 2
+#endif
 
 // Σ_z scr[z·stride] for z < Z in z order, the loads of 8 partials in flight at a time
 __device__ __forceinline__ double l2_zsum(const double* p, int Z, int64_t stride) {
@@ -106,15 +107,12 @@ __device__ __forceinline__ double l2_zsum(const double* p, int Z, int64_t stride
 // so a cell (chunk, fibre) costs one 16-byte X load, NR 16-byte shared-memory reads and the
 // NR(NR−1)/2 scalars H_{r_j,r_j'}(d_j, d_j').
 template <typename T, int NR>
-__global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2Params<T> P) {
+__global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __grid_constant__ L2Params<T> P) {
     constexpr int VE = 16 / (int)sizeof(T);
-    constexpr int U = l2_kept_u<T>(NR);
+    constexpr int U = kL2RunU;
     constexpr int NRa = NR > 0 ? NR : 1;
-    constexpr int NJJ = NR * (NR - 1) / 2;
+    static_assert(NR >= 1 && NR <= 2, "l2_kept serves orders 3 and 4");
     using V = typename VecT<T>::V;
-    // orders ≥ 5 (≥ 9 factors per weight): products and sums in fp64 — independent fp32
-    // roundings per entry are full-rank noise to the ill-conditioned column systems
-    using A = std::conditional_t<(NR >= 3), double, T>;
     extern __shared__ __align__(16) unsigned char l2sm_raw[];
     __shared__ double sm[8 * 2 * 32 * VE];  // [warp][β|ω][chunk lane · VE]
     __shared__ unsigned last;
@@ -122,11 +120,11 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
     const int CG = P.CG, lcg = P.lcg, FL = 32 >> lcg, CGE = CG * VE;
     const int cl = lane & (CG - 1), fl = lane >> lcg;
     const int il = warp >> P.lwpi, wi = warp - (il << P.lwpi);
-    const int64_t nitems = P.NV * P.NCG;
-    const int64_t item = (int64_t)blockIdx.x * P.ipc + il;
+    const int nitems = (int)P.NV * P.NCG;  // < 2^31 (host check)
+    const int item = (int)blockIdx.x * P.ipc + il;
     const bool item_ok = item < nitems;
-    const int64_t v = item_ok ? item / P.NCG : 0;
-    const int cg = item_ok ? (int)(item - v * P.NCG) : 0;
+    const int v = item_ok ? item / P.NCG : 0;
+    const int cg = item_ok ? item - v * P.NCG : 0;
     const int z = blockIdx.y;
     const int I1p = P.I1p;
     const int e0 = (cg * CG + cl) * VE;
@@ -136,103 +134,27 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
     int r = r0 + wi * FL + fl;
     const T* __restrict__ Hb = P.H;
 
-    // odometer digits of r and of the step (mixed radix rdim[0..NR))
+    // A thread's unit of work is a RUN: U consecutive values d0 = b·U + u of reduced mode r_0 (the
+    // longest one, host order) at fixed higher digits — everything but the X cell, the V_0 row
+    // and the scalars H_{r_0,r_j}(d0, d_j) is per run, and the cell addresses are base + u·stride.
+    // Runs are numbered in mixed radix (nb0 = ⌈rdim[0]/U⌉, rdim[1], …) and walked by odometer.
     int dg[NRa], ds[NRa], dm[NRa], tb0[NRa];
     {
-        int rr = min(r, (int)P.FR - 1), ss = slots, toff = cl * VE;
+        int rr = min(r, (int)P.FR - 1), toff = cl * VE;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-            dm[j] = P.rdim[j];
-            dg[j] = rr % dm[j];
+            dm[j] = j == 0 ? P.nb0 : P.rdim[j];
+            dg[j] = j + 1 < NR ? rr % dm[j] : rr;
             rr /= dm[j];
-            ds[j] = ss % dm[j];
-            ss /= dm[j];
+            ds[j] = P.dsr[j];
             tb0[j] = toff;
-            toff += dm[j] * CGE;
+            toff += P.rdim[j] * CGE;
         }
     }
-    const T* xb = P.X + (v * P.kf_stride) * I1p + e0;
-    A* tab = reinterpret_cast<A*>(l2sm_raw) + (size_t)il * P.tab_item;
-
-    A sb[VE], sw[VE];
-#pragma unroll
-    for (int e = 0; e < VE; ++e) sb[e] = sw[e] = A(0);
-
-    // one round = U cells of this thread: all loads first (X, pair scalars), then the math
-    V xq[U];
-    A s[U];
-    int so[U][NRa];
-    unsigned val = 0;
-    auto issue = [&]() {
-        val = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const bool ok = act && r + u * slots < r1;
-            val |= ok ? (1u << u) : 0u;
-            unsigned xo = 0;
-            A sc = A(1);
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                xo += (unsigned)(dg[j] * P.rfsI[j]);
-                so[u][j] = tb0[j] + dg[j] * CGE;
-            }
-            if (ok) {
-                if constexpr (NJJ > 0) {
-                    T pv[NJJ];
-                    int t = 0;
-#pragma unroll
-                    for (int j = 0; j < NR; ++j)
-#pragma unroll
-                        for (int j2 = j + 1; j2 < NR; ++j2, ++t) pv[t] = Hb[P.jj_off[t] + dg[j] * P.jj_ma[t] + dg[j2] * P.jj_mb[t]];
-#pragma unroll
-                    for (int t2 = 0; t2 < NJJ; ++t2) sc *= (A)pv[t2];
-                }
-                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + xo));
-            } else {
-                xq[u] = zero_v<T>();
-            }
-            s[u] = sc;
-            // advance the odometer by one step (digits stay < dm: one conditional subtract)
-            int carry = 0;
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                int d = dg[j] + ds[j] + carry;
-                carry = (j + 1 < NR && d >= dm[j]) ? 1 : 0;
-                dg[j] = d - (carry ? dm[j] : 0);
-            }
-        }
-        r += U * slots;
-    };
-    auto compute = [&]() {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (!(val & (1u << u))) continue;
-            T x[VE];
-            A w[VE];
-            VecT<T>::get(xq[u], x);
-#pragma unroll
-            for (int e = 0; e < VE; ++e) w[e] = s[u];
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                A h[VE];
-                if constexpr (std::is_same<A, T>::value) {
-                    VecT<T>::get(*reinterpret_cast<const V*>(tab + so[u][j]), h);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) h[e] = tab[so[u][j] + e];
-                }
-#pragma unroll
-                for (int e = 0; e < VE; ++e) w[e] *= h[e];
-            }
-#pragma unroll
-            for (int e = 0; e < VE; ++e) {
-                sb[e] = fma(w[e], (A)x[e], sb[e]);
-                sw[e] = fma(w[e], w[e], sw[e]);
-            }
-        }
-    };
-    // first round's loads are in flight while the tables are staged
-    issue();
+    const T* xb = P.X + ((int64_t)v * P.kf_stride) * I1p + e0;
+    T* tab = reinterpret_cast<T*>(l2sm_raw) + (size_t)il * P.tab_item;
+    pdl_wait();
+    pdl_launch();
     // ---- stage the item's weight tables (its wpi warps) ---------------------------------------
     if (item_ok) {
         const int tid = wi * 32 + lane, nt = P.wpi * 32;
@@ -240,34 +162,83 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
             const int n = P.rdim[j] << lcg;
-            const int ksb = P.ks_off[j] + (int)v * P.ks_mv[j];
+            const int ksb = P.ks_off[j] + v * P.ks_mv[j];
 #pragma unroll 4
             for (int q = tid; q < n; q += nt) {
                 const int d = q >> lcg, c2 = q - (d << lcg);
                 const int ee = (cg * CG + c2) * VE;
-                A h[VE];
+                T h[VE];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) h[e] = T(0);
                 if (ee < I1p) {
-                    const A a = (A)Hb[ksb + d * P.ks_mj[j]];
+                    const T a = Hb[ksb + d * P.ks_mj[j]];
                     const V hq = *reinterpret_cast<const V*>(Hb + P.rv_off[j] + d * I1p + ee);
-                    T ht[VE];
-                    VecT<T>::get(hq, ht);
+                    VecT<T>::get(hq, h);
 #pragma unroll
-                    for (int e = 0; e < VE; ++e) h[e] = (A)ht[e] * a;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) h[e] = A(0);
+                    for (int e = 0; e < VE; ++e) h[e] *= a;
                 }
-#pragma unroll
-                for (int e = 0; e < VE; ++e) tab[toff + q * VE + e] = h[e];
+                *reinterpret_cast<V*>(tab + toff + q * VE) = VecT<T>::make(h);
             }
             toff += n * VE;
         }
     }
     __syncthreads();
-    compute();
+
+    T sb[VE], sw[VE];
+#pragma unroll
+    for (int e = 0; e < VE; ++e) sb[e] = sw[e] = T(0);
+    const int rdim0 = NR > 0 ? P.rdim[0] : 1;
+    const unsigned xst = NR > 0 ? (unsigned)P.rfsI[0] : 0u;  // X elements between cells of a run
     while (act && r < r1) {
-        issue();
-        compute();
+        const int d0s = dg[0] * U;
+        const int nv = min(U, rdim0 - d0s);
+        unsigned xo = (unsigned)d0s * xst;
+#pragma unroll
+        for (int j = 1; j < NR; ++j) xo += (unsigned)(dg[j] * P.rfsI[j]);
+        // loads of the run: X cells and the scalars H_{r_0,r_1}(d0, d_1)
+        V xq[U];
+        T p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            xq[u] = zero_v<T>();
+            p[u] = T(1);
+            if (u < nv) {
+                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + xo + (unsigned)u * xst));
+                if constexpr (NR == 2) p[u] = Hb[P.jj_off[0] + (d0s + u) * P.jj_ma[0] + dg[1] * P.jj_mb[0]];
+            }
+        }
+        // run-constant part of the weight: V_1[d_1]
+        T bv[VE];
+#pragma unroll
+        for (int e = 0; e < VE; ++e) bv[e] = T(1);
+        if constexpr (NR == 2) VecT<T>::get(*reinterpret_cast<const V*>(tab + tb0[1] + dg[1] * CGE), bv);
+        const T* t0 = tab + tb0[0] + d0s * CGE;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u < nv) {
+                T x[VE], h[VE], w[VE];
+                VecT<T>::get(xq[u], x);
+                VecT<T>::get(*reinterpret_cast<const V*>(t0 + u * CGE), h);
+                if constexpr (NR == 2) {
+                    T bp[VE];
+                    scale<T, VE>(bv, p[u], bp);
+                    mul<T, VE>(h, bp, w);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) w[e] = h[e];
+                }
+                accumulate<T, VE>(w, x, sb, sw);
+            }
+        }
+        // next run of this thread
+        int carry = 0;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            int d = dg[j] + ds[j] + carry;
+            carry = (j + 1 < NR && d >= dm[j]) ? 1 : 0;
+            dg[j] = d - (carry ? dm[j] : 0);
+        }
+        r += slots;
     }
     // ---- fibre lanes (xor butterfly, fp64), then the item's warps, then the Z CTAs -----------
     double db[VE], dw[VE];
@@ -293,19 +264,20 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
     __syncthreads();
     // thread q: item-local il2, β|ω, element el of the chunk group
     const int nout = P.ipc * 2 * CGE;
+    const int lce = lcg + (VE == 4 ? 2 : 1);  // log2 CGE
     auto emit = [&](int q, double val) {
-        const int il2 = q / (2 * CGE), rem = q - il2 * 2 * CGE;
-        const int bw = rem / CGE, el = rem - bw * CGE;
-        const int64_t it2 = (int64_t)blockIdx.x * P.ipc + il2;
+        const int il2 = q >> (lce + 1), rem = q - (il2 << (lce + 1));
+        const int bw = rem >> lce, el = rem - (bw << lce);
+        const int it2 = (int)blockIdx.x * P.ipc + il2;
         if (it2 >= nitems) return;
-        const int64_t v2 = it2 / P.NCG;
-        const int e = (int)(it2 - v2 * P.NCG) * CGE + el;
+        const int v2 = it2 / P.NCG;
+        const int e = (it2 - v2 * P.NCG) * CGE + el;
         if (e >= P.I1) return;
-        const int64_t o = P.kIsMode0 ? ((int64_t)e * P.Ii + v2) : (v2 * P.Ii + e);
+        const int64_t o = P.kIsMode0 ? ((int64_t)e * P.Ii + v2) : ((int64_t)v2 * P.Ii + e);
         (bw ? P.omega : P.beta)[o] = val;
     };
     for (int q = threadIdx.x; q < nout; q += kL2Threads) {
-        const int il2 = q / (2 * CGE), rem = q - il2 * 2 * CGE;
+        const int il2 = q >> (lce + 1), rem = q - (il2 << (lce + 1));
         double a = 0.0;
         for (int u = 0; u < P.wpi; ++u) a += sm[(il2 * P.wpi + u) * 2 * CGE + rem];
         if (P.Z == 1) emit(q, a);
@@ -333,7 +305,7 @@ __global__ void __launch_bounds__(kL2Threads) l2_kept(const __grid_constant__ L2
 // per-cell fp32, then fp64 over the thread's cells, the team (xor butterfly, warps in order),
 // and the Z CTAs in z order (last CTA to arrive).
 template <typename T, int NRR>
-__global__ void __launch_bounds__(kL2Threads) l2_red(const __grid_constant__ L2Params<T> P) {
+__global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid_constant__ L2Params<T> P) {
     constexpr int VE = 16 / (int)sizeof(T);
     constexpr int U = kL2U;
     constexpr int NRa = NRR > 0 ? NRR : 1;
@@ -352,6 +324,8 @@ __global__ void __launch_bounds__(kL2Threads) l2_red(const __grid_constant__ L2P
     const int I1p = P.I1p, NC = I1p / VE;
     const int jk = v_ok ? (int)(v % P.Ik) : 0, ai = v_ok ? (int)(v / P.Ik) : 0;
     const T* __restrict__ Hb = P.H;
+    pdl_wait();
+    pdl_launch();
     // ---- P_v into shared memory ----------------------------------------------------------------
     T* pv = reinterpret_cast<T*>(l2sm_raw) + (size_t)team * I1p;
     if (v_ok) {
@@ -546,7 +520,7 @@ struct L2RefillParams {
 };
 
 template <typename T, int NO>
-__global__ void __launch_bounds__(kL2Threads) l2_refill(const __grid_constant__ L2RefillParams<T> P) {
+__global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __grid_constant__ L2RefillParams<T> P) {
     constexpr int VE = 16 / (int)sizeof(T);
     constexpr int U = kL2U;
     constexpr int NPP = NO * (NO - 1) / 2;
@@ -565,6 +539,8 @@ __global__ void __launch_bounds__(kL2Threads) l2_refill(const __grid_constant__ 
     int f = f0 + warp * FL + fl;
     const T* __restrict__ Hb = P.H;
     T* tab = reinterpret_cast<T*>(l2sm_raw);
+    pdl_wait();
+    pdl_launch();
     // tables
     {
         int toff = 0;

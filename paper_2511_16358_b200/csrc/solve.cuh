@@ -390,6 +390,8 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     constexpr int NA = R * (R + 1) / 2 + R;
     __shared__ double red[5 * NA];
     __shared__ double cs[R];
+    pdl_wait();
+    pdl_launch();
     block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs);
 }
 
@@ -932,6 +934,8 @@ template <typename T, int SM>
 __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
     extern __shared__ __align__(16) double bsm[];
     __shared__ int ok;
+    pdl_wait();
+    pdl_launch();
     block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok);
 }
 
@@ -1009,6 +1013,8 @@ static __global__ void __launch_bounds__(1024) finalize_norms(const double* norm
                                                        double* scal, int* flags, int obj_only,
                                                        int combine) {
     __shared__ double s[5 * 32];
+    pdl_wait();
+    pdl_launch();
     finalize_norms_body(norms, ngroups, delta, ndelta, sh_off, sh_len, p5, scal, flags, obj_only, combine, s);
 }
 

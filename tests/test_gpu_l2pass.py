@@ -11,7 +11,7 @@ from gpu_util import make_solver, oracle_state, rel, requires_cuda, tol_for
 
 pytestmark = [pytest.mark.gpu, requires_cuda]
 
-# the L2 pass serves third-order tensors (csrc/ifctn.cu make_l2); the others check the switch
+# the L2 pass serves orders 3 and 4 (csrc/ifctn.cu make_l2); C5s (order 5) checks the switch
 SMALL = ["C1", "C2s", "C3s", "C4s", "C5s", "C2rs"]
 
 
@@ -39,7 +39,7 @@ def test_l2pass_block_coefficients_match_fibre_walk_and_oracle(name):
                 assert np.max(np.abs(wa - wo)) <= 1e-5 * sc + 1e-300, (k, i)
 
 
-@pytest.mark.parametrize("name", ["C2s", "C2rs", "C1"])
+@pytest.mark.parametrize("name", ["C2s", "C2rs", "C1", "C3s", "C4s"])
 def test_l2pass_one_sweep_matches_oracle(name):
     p = make_config(name)
     s = make_solver(p)
@@ -54,9 +54,52 @@ def test_l2pass_one_sweep_matches_oracle(name):
 def test_l2pass_split_partials_are_deterministic():
     """Blocks with few kept values split each v over Z CTAs (last-arriving CTA sums in z
     order): repeated calls are bit-identical."""
-    p = make_config("C2")
-    s = make_solver(p)
-    for (k, i) in ((0, 2), (2, 0), (2, 1)):
-        b1, w1 = s.block_coefficients(k, i)
-        b2, w2 = s.block_coefficients(k, i)
-        assert np.array_equal(b1, b2) and np.array_equal(w1, w2)
+    for name, blocks in (("C2", ((0, 2), (2, 0), (2, 1))), ("C3", ((0, 2), (2, 0), (2, 3))), ("C4", ((0, 3), (3, 0), (1, 3)))):
+        p = make_config(name)
+        s = make_solver(p)
+        for (k, i) in blocks:
+            b1, w1 = s.block_coefficients(k, i)
+            b2, w2 = s.block_coefficients(k, i)
+            assert np.array_equal(b1, b2) and np.array_equal(w1, w2)
+        s.close()
+
+
+def test_gram_gemm_flag_matches_default_and_oracle():
+    """IFCTN_FLAG_GRAM_GEMM (large ranks: gram_project, two columns per CTA, then the FROM_PROJ
+    solve) gives the per-column solve's factors up to summation order and meets the one-sweep
+    bar against the oracle (C2rs: R_{1,2} = 36)."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_GRAM_GEMM
+    p = make_config("C2rs")
+    a = make_solver(p)
+    b = make_solver(p, flags=IFCTN_FLAG_GRAM_GEMM)
+    assert b.launch_count() == a.launch_count()
+    sh, G, X = oracle_state(p)
+    st, _, _ = O.sweep(sh, G, X, p.mask, p.rho, O.objective(sh, G, X), True)
+    assert st == 0
+    for s in (a, b):
+        s.sweep(1, trace=True)
+    assert b.launch_count() > a.launch_count()  # the extra Gram launches ran
+    assert rel(b.factors().cpu().numpy(), a.factors().cpu().numpy()) <= 1e-6
+    assert rel(b.factors().cpu().numpy(), G) <= tol_for(p)
+    assert rel(b.reconstruct().cpu().numpy(), X) <= tol_for(p)
+
+
+@pytest.mark.parametrize("name", ["C2s", "C3s", "C4s", "C2rs", "C1"])
+def test_programmatic_dependent_launch_is_bit_identical(name):
+    """The L2-pass, solve and finaliser kernels are launched with programmatic stream
+    serialization and wait for their predecessor themselves (griddepcontrol.wait before the
+    first dependent access): graph-replayed and plain-launch sweeps are bit-identical to plain
+    stream order (IFCTN_FLAG_NO_PDL)."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_GRAPH, IFCTN_FLAG_NO_PDL
+    p = make_config(name)
+    ref = make_solver(p, flags=IFCTN_FLAG_NO_PDL)
+    ref.sweep(3)
+    ref.sweep(2, trace=True)
+    Xr, Gr = ref.reconstruct().cpu().numpy(), ref.factors().cpu().numpy()
+    for fl in (0, IFCTN_FLAG_NO_GRAPH):
+        s = make_solver(p, flags=fl)
+        s.sweep(3)
+        s.sweep(2, trace=True)
+        assert np.array_equal(s.reconstruct().cpu().numpy(), Xr)
+        assert np.array_equal(s.factors().cpu().numpy(), Gr)
+        s.close()
