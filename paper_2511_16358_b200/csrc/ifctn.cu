@@ -1025,7 +1025,8 @@ struct Solver : SolverBase {
                 const int FL = 32 / CG;
                 const int64_t NCG = cdiv(NC, CG);
                 const double waste = (double)(NCG * CG) / NC;
-                const int64_t tab_item = rsum * CG * VE;
+                const int64_t asc_item = (rsum + VE - 1) / VE * VE;
+                const int64_t tab_item = rsum * CG * VE + asc_item;
                 for (int wpi = 1; wpi <= 8; wpi <<= 1) {
                     if (pin[1] && wpi != pin[1]) continue;
                     const int ipc = 8 / wpi;
@@ -1055,6 +1056,7 @@ struct Solver : SolverBase {
                             P.lwpi = 0;
                             while ((1 << P.lwpi) < wpi) ++P.lwpi;
                             P.tab_item = (int)tab_item;
+                            P.asc_item = (int)asc_item;
                             P.FRz = FRz;
                             P.Z = (int)Ze;
                             b.l2_grid = dim3((unsigned)nbx, (unsigned)Ze);

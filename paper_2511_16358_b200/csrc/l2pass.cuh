@@ -68,7 +68,8 @@ struct L2Params {
     // ---- l2_kept: chunk groups, items (v, cg) per CTA, warps per item, table elements per item
     int CG, NCG, ipc, wpi;
     int lcg, lwpi;         // log2 of CG, wpi
-    int tab_item;          // table elements per item (fp64 elements for orders ≥ 5)
+    int tab_item;          // shared-memory elements per item: tables V_j, then the scalars A_j
+    int asc_item;          // … of which scalars (Σ rdim, rounded up to a 16-byte multiple)
     int64_t kf_stride;     // fibre-index stride of the kept mode m
     // ---- l2_red: team size, H_{0,k} / H_{0,i} offsets
     int TL;
@@ -86,6 +87,19 @@ constexpr int kL2RunU = IFCTN_L2_RUN_U;
 #ifndef IFCTN_L2_MINB
 #define IFCTN_L2_MINB 2
 #endif
+
+// per-thread asynchronous global → shared copies (LDGSTS)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_scalar(uint32_t dst, const T* src) {
+    if constexpr (sizeof(T) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
 // Σ_z scr[z·stride] for z < Z in z order, the loads of 8 partials in flight at a time
 __device__ __forceinline__ double l2_zsum(const double* p, int Z, int64_t stride) {
@@ -138,9 +152,9 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
     // longest one, host order) at fixed higher digits — everything but the X cell, the V_0 row
     // and the scalars H_{r_0,r_j}(d0, d_j) is per run, and the cell addresses are base + u·stride.
     // Runs are numbered in mixed radix (nb0 = ⌈rdim[0]/U⌉, rdim[1], …) and walked by odometer.
-    int dg[NRa], ds[NRa], dm[NRa], tb0[NRa];
+    int dg[NRa], ds[NRa], dm[NRa], tb0[NRa], ab0[NRa];
     {
-        int rr = min(r, (int)P.FR - 1), toff = cl * VE;
+        int rr = min(r, (int)P.FR - 1), toff = cl * VE, aoff = P.tab_item - P.asc_item;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
             dm[j] = j == 0 ? P.nb0 : P.rdim[j];
@@ -149,39 +163,38 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
             ds[j] = P.dsr[j];
             tb0[j] = toff;
             toff += P.rdim[j] * CGE;
+            ab0[j] = aoff;
+            aoff += P.rdim[j];
         }
     }
     const T* xb = P.X + ((int64_t)v * P.kf_stride) * I1p + e0;
     T* tab = reinterpret_cast<T*>(l2sm_raw) + (size_t)il * P.tab_item;
     pdl_wait();
     pdl_launch();
-    // ---- stage the item's weight tables (its wpi warps) ---------------------------------------
+    // ---- stage the item's tables (its wpi warps): asynchronous global → shared copies (LDGSTS,
+    // all in flight at once), V_j[d][·] = H_{0,r_j}(chunk group, d) and A_j[d] = H_{m,r_j}(v, d)
+#ifdef IFCTN_EXP_L2_SKIP_STAGE
+    if (P.I1 < 0)
+#endif
     if (item_ok) {
         const int tid = wi * 32 + lane, nt = P.wpi * 32;
-        int toff = 0;
+        int toff = 0, aoff = P.tab_item - P.asc_item;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
             const int n = P.rdim[j] << lcg;
-            const int ksb = P.ks_off[j] + v * P.ks_mv[j];
-#pragma unroll 4
             for (int q = tid; q < n; q += nt) {
                 const int d = q >> lcg, c2 = q - (d << lcg);
                 const int ee = (cg * CG + c2) * VE;
-                T h[VE];
-#pragma unroll
-                for (int e = 0; e < VE; ++e) h[e] = T(0);
-                if (ee < I1p) {
-                    const T a = Hb[ksb + d * P.ks_mj[j]];
-                    const V hq = *reinterpret_cast<const V*>(Hb + P.rv_off[j] + d * I1p + ee);
-                    VecT<T>::get(hq, h);
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) h[e] *= a;
-                }
-                *reinterpret_cast<V*>(tab + toff + q * VE) = VecT<T>::make(h);
+                if (ee < I1p) cp_async16(smem_u32(tab + toff + q * VE), Hb + P.rv_off[j] + d * I1p + ee);
+                else *reinterpret_cast<V*>(tab + toff + q * VE) = zero_v<T>();
             }
+            const int ksb = P.ks_off[j] + v * P.ks_mv[j];
+            for (int d = tid; d < P.rdim[j]; d += nt) cp_async_scalar<T>(smem_u32(tab + aoff + d), Hb + ksb + d * P.ks_mj[j]);
             toff += n * VE;
+            aoff += P.rdim[j];
         }
     }
+    cp_async_wait_all();
     __syncthreads();
 
     T sb[VE], sw[VE];
@@ -189,6 +202,9 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
     for (int e = 0; e < VE; ++e) sb[e] = sw[e] = T(0);
     const int rdim0 = NR > 0 ? P.rdim[0] : 1;
     const unsigned xst = NR > 0 ? (unsigned)P.rfsI[0] : 0u;  // X elements between cells of a run
+#ifdef IFCTN_EXP_L2_SKIP_MAIN  // timing experiments only (wrong results): fixed cost of the kernel
+    if (P.I1 < 0)
+#endif
     while (act && r < r1) {
         const int d0s = dg[0] * U;
         const int nv = min(U, rdim0 - d0s);
@@ -207,12 +223,17 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
                 if constexpr (NR == 2) p[u] = Hb[P.jj_off[0] + (d0s + u) * P.jj_ma[0] + dg[1] * P.jj_mb[0]];
             }
         }
-        // run-constant part of the weight: V_1[d_1]
+        // run-constant part of the weight: V_1[d_1] · A_1[d_1]
         T bv[VE];
 #pragma unroll
         for (int e = 0; e < VE; ++e) bv[e] = T(1);
-        if constexpr (NR == 2) VecT<T>::get(*reinterpret_cast<const V*>(tab + tb0[1] + dg[1] * CGE), bv);
+        if constexpr (NR == 2) {
+            T h1[VE];
+            VecT<T>::get(*reinterpret_cast<const V*>(tab + tb0[1] + dg[1] * CGE), h1);
+            scale<T, VE>(h1, tab[ab0[1] + dg[1]], bv);
+        }
         const T* t0 = tab + tb0[0] + d0s * CGE;
+        const T* a0 = tab + ab0[0] + d0s;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (u < nv) {
@@ -221,11 +242,10 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
                 VecT<T>::get(*reinterpret_cast<const V*>(t0 + u * CGE), h);
                 if constexpr (NR == 2) {
                     T bp[VE];
-                    scale<T, VE>(bv, p[u], bp);
+                    scale<T, VE>(bv, p[u] * a0[u], bp);
                     mul<T, VE>(h, bp, w);
                 } else {
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) w[e] = h[e];
+                    scale<T, VE>(h, a0[u], w);
                 }
                 accumulate<T, VE>(w, x, sb, sw);
             }
@@ -547,16 +567,15 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
 #pragma unroll
         for (int q = 0; q < NO; ++q) {
             const int n = P.dim[q] << lcg;
-#pragma unroll 4
             for (int t = threadIdx.x; t < n; t += kL2Threads) {
                 const int d = t >> lcg, c2 = t - (d << lcg);
                 const int ee = (cg * CG + c2) * VE;
-                V hq = zero_v<T>();
-                if (ee < I1p) hq = *reinterpret_cast<const V*>(Hb + P.tv_off[q] + d * I1p + ee);
-                *reinterpret_cast<V*>(tab + toff + t * VE) = hq;
+                if (ee < I1p) cp_async16(smem_u32(tab + toff + t * VE), Hb + P.tv_off[q] + d * I1p + ee);
+                else *reinterpret_cast<V*>(tab + toff + t * VE) = zero_v<T>();
             }
             toff += n * VE;
         }
+        cp_async_wait_all();
     }
     int dg[NO], dm[NO], ds[NO], tb0[NO];
     {
