@@ -7,7 +7,7 @@ import sys
 
 lines = [ln for ln in open(sys.argv[1]) if ln.startswith('"')]  # drop ncu's ==WARNING== lines
 rows = [r for r in csv.DictReader(lines) if r.get("Metric Name") == "gpu__time_duration.sum"]
-names = [re.sub(r"\(.*", "", r["Kernel Name"]).replace("void ", "") for r in rows]
+names = [re.sub(r"\(.*", "", r["Kernel Name"]).replace("void ", "").replace("ifctn::", "") for r in rows]
 t = [float(r["Metric Value"]) for r in rows]
 # timed region = launches of the last context's sweeps: after the last pack_input
 last = max(i for i, n in enumerate(names) if n.startswith("pack_input"))

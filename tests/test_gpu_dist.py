@@ -181,7 +181,7 @@ def test_sharded_metrics_match_single_gpu(mode):
             assert g[key] == pytest.approx(want[key], rel=rt)
         assert g["missing"] == want["missing"]
         if mode == 2:
-            assert g["ssim"] == pytest.approx(want["ssim"], rel=1e-9)
+            assert g["ssim"] == pytest.approx(want["ssim"], rel=rt)  # a function of the same X
         else:
             assert np.isnan(g["ssim"])
 
