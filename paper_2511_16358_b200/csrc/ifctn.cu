@@ -1351,9 +1351,12 @@ struct Solver : SolverBase {
     // (small ranks: block_solve sums its column's slots itself; `full` forces the reduce for
     // ifctn_block_coefficients).  A skipped reduce keeps an empty profiling interval so that
     // ifctn_profile_sweep still reports [pass, reduce, solve] per block.
-    void enqueue_contract(const BlockPlan<T>& b, bool full = false) {
+    // after_solve: the previous launch in the stream is a solve of this sweep (see L2Params::x_early)
+    void enqueue_contract(const BlockPlan<T>& b, bool full = false, bool after_solve = false) {
         if (b.l2) {  // one launch writes β, ω whole; an empty interval for the reduce slot
-            launch(b.l2_fn, b.l2_grid, dim3(kL2Threads), b.l2_smem, b.l2p, true);
+            L2Params<T> lp = b.l2p;
+            lp.x_early = after_solve ? 1 : 0;
+            launch(b.l2_fn, b.l2_grid, dim3(kL2Threads), b.l2_smem, lp, true);
             prof_mark();
             return;
         }
@@ -1377,8 +1380,8 @@ struct Solver : SolverBase {
         launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q, !b.dist);
     }
 
-    void enqueue_block(const BlockPlan<T>& b) {
-        enqueue_contract(b);
+    void enqueue_block(const BlockPlan<T>& b, bool after_solve = false) {
+        enqueue_contract(b, false, after_solve);
         enqueue_solve(b);
     }
 
@@ -1403,9 +1406,11 @@ struct Solver : SolverBase {
         }
     }
 
-    void enqueue_xupdate() {
+    void enqueue_xupdate(bool after_solve = false) {
         if (l2r) {
-            launch(l2r_fn, l2r_grid, dim3(kL2Threads), l2r_smem, l2rp, true);
+            L2RefillParams<T> rp = l2rp;
+            rp.x_early = after_solve ? 1 : 0;
+            launch(l2r_fn, l2r_grid, dim3(kL2Threads), l2r_smem, rp, true);
             enqueue_finalize((int64_t)l2r_grid.x * l2r_grid.y, 0);
             return;
         }
@@ -1414,8 +1419,8 @@ struct Solver : SolverBase {
     }
 
     void enqueue_sweep() {
-        for (const auto& b : blocks) enqueue_block(b);
-        enqueue_xupdate();
+        for (size_t b = 0; b < blocks.size(); ++b) enqueue_block(blocks[b], b > 0);
+        enqueue_xupdate(true);
     }
 
     // Fused sweep sequence for a fixed sweep count (eps ≤ 0, no trace):

@@ -76,6 +76,10 @@ struct L2Params {
     int pk_off, pi_off;
     double* scr;           // Z > 1: grid.x·Z·(values per CTA)·2 partials
     unsigned* cnt;         // Z > 1: grid.x arrival counters, zero between launches
+    // launch-time: the predecessor in the stream is a solve of the same sweep (it waits for ITS
+    // predecessor before it lets this grid start, and writes no X), so nothing still running can
+    // write X: the first round's X loads are issued before pdl_wait()
+    int x_early;
 };
 
 constexpr int kL2Threads = 256;
@@ -169,6 +173,29 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
     }
     const T* xb = P.X + ((int64_t)v * P.kf_stride) * I1p + e0;
     T* tab = reinterpret_cast<T*>(l2sm_raw) + (size_t)il * P.tab_item;
+    const int rdim0 = NR > 0 ? P.rdim[0] : 1;
+    const unsigned xst = NR > 0 ? (unsigned)P.rfsI[0] : 0u;  // X elements between cells of a run
+    // X cells of the run the odometer stands on
+    auto load_run = [&](V (&dst)[U]) {
+        const int d0s = dg[0] * U;
+        const int nv = min(U, rdim0 - d0s);
+        unsigned xo = (unsigned)d0s * xst;
+#pragma unroll
+        for (int j = 1; j < NR; ++j) xo += (unsigned)(dg[j] * P.rfsI[j]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            dst[u] = zero_v<T>();
+            if (u < nv) dst[u] = ld_stream(reinterpret_cast<const V*>(xb + xo + (unsigned)u * xst));
+        }
+    };
+    V xpre[U];
+    bool pre = false;
+#ifndef IFCTN_EXP_NO_XEARLY
+    if (P.x_early && act && r < r1) {  // X is not written by anything still running (L2Params::x_early)
+        load_run(xpre);
+        pre = true;
+    }
+#endif
     pdl_wait();
     pdl_launch();
     // ---- stage the item's tables (its wpi warps): asynchronous global → shared copies (LDGSTS,
@@ -200,28 +227,24 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
     T sb[VE], sw[VE];
 #pragma unroll
     for (int e = 0; e < VE; ++e) sb[e] = sw[e] = T(0);
-    const int rdim0 = NR > 0 ? P.rdim[0] : 1;
-    const unsigned xst = NR > 0 ? (unsigned)P.rfsI[0] : 0u;  // X elements between cells of a run
-#ifdef IFCTN_EXP_L2_SKIP_MAIN  // timing experiments only (wrong results): fixed cost of the kernel
-    if (P.I1 < 0)
-#endif
-    while (act && r < r1) {
+    // one run; first = its X cells were loaded before the wait (xpre)
+    auto do_run = [&](auto first) {
         const int d0s = dg[0] * U;
         const int nv = min(U, rdim0 - d0s);
-        unsigned xo = (unsigned)d0s * xst;
-#pragma unroll
-        for (int j = 1; j < NR; ++j) xo += (unsigned)(dg[j] * P.rfsI[j]);
         // loads of the run: X cells and the scalars H_{r_0,r_1}(d0, d_1)
         V xq[U];
         T p[U];
+        if constexpr (decltype(first)::value) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) xq[u] = xpre[u];
+        } else {
+            load_run(xq);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            xq[u] = zero_v<T>();
             p[u] = T(1);
-            if (u < nv) {
-                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + xo + (unsigned)u * xst));
-                if constexpr (NR == 2) p[u] = Hb[P.jj_off[0] + (d0s + u) * P.jj_ma[0] + dg[1] * P.jj_mb[0]];
-            }
+            if constexpr (NR == 2)
+                if (u < nv) p[u] = Hb[P.jj_off[0] + (d0s + u) * P.jj_ma[0] + dg[1] * P.jj_mb[0]];
         }
         // run-constant part of the weight: V_1[d_1] · A_1[d_1]
         T bv[VE];
@@ -259,6 +282,13 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
             dg[j] = d - (carry ? dm[j] : 0);
         }
         r += slots;
+    };
+#ifdef IFCTN_EXP_L2_SKIP_MAIN  // timing experiments only (wrong results): fixed cost of the kernel
+    if (P.I1 < 0)
+#endif
+    {
+        if (pre) do_run(std::true_type{});
+        while (act && r < r1) do_run(std::false_type{});
     }
     // ---- fibre lanes (xor butterfly, fp64), then the item's warps, then the Z CTAs -----------
     double db[VE], dw[VE];
@@ -344,24 +374,6 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
     const int I1p = P.I1p, NC = I1p / VE;
     const int jk = v_ok ? (int)(v % P.Ik) : 0, ai = v_ok ? (int)(v / P.Ik) : 0;
     const T* __restrict__ Hb = P.H;
-    pdl_wait();
-    pdl_launch();
-    // ---- P_v into shared memory ----------------------------------------------------------------
-    T* pv = reinterpret_cast<T*>(l2sm_raw) + (size_t)team * I1p;
-    if (v_ok) {
-        const T* hk = Hb + P.pk_off + jk * I1p;
-        const T* hi = Hb + P.pi_off + ai * I1p;
-        for (int c = tl; c < NC; c += TL) {
-            const V a = *reinterpret_cast<const V*>(hk + c * VE);
-            const V b = *reinterpret_cast<const V*>(hi + c * VE);
-            T x[VE], y[VE];
-            VecT<T>::get(a, x);
-            VecT<T>::get(b, y);
-#pragma unroll
-            for (int e = 0; e < VE; ++e) x[e] *= y[e];
-            *reinterpret_cast<V*>(pv + c * VE) = VecT<T>::make(x);
-        }
-    }
     // ---- this thread's cells: q = tl + t·TL < ncell ---------------------------------------------
     const int r0 = (int)(z * P.FRz), r1 = (int)min(P.FR, (int64_t)r0 + P.FRz);
     const int ncell = v_ok ? (r1 - r0) * NC : 0;
@@ -383,9 +395,61 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
         }
     }
     const T* xb = P.X + ((int64_t)jk * P.fstride[P.k] + (int64_t)ai * P.fstride[P.i]) * I1p;
+    // next cell of this thread: chunk += dc (mod NC), fibre += ⌊TL/NC⌋ + wrap
+    auto advance = [&](int& cc, int (&dd)[NRa]) {
+        cc += dc;
+        int carry = cc >= NC ? 1 : 0;
+        cc -= carry ? NC : 0;
+#pragma unroll
+        for (int j = 0; j < NRR; ++j) {
+            int d = dd[j] + ds[j] + carry;
+            carry = (j + 1 < NRR && d >= dm[j]) ? 1 : 0;
+            dd[j] = d - (carry ? dm[j] : 0);
+        }
+    };
+    auto x_of = [&](int cc, const int (&dd)[NRa]) {
+        int f = 0;
+#pragma unroll
+        for (int j = 0; j < NRR; ++j) f += dd[j] * P.rfs[j];
+        return ld_stream(reinterpret_cast<const V*>(xb + (int64_t)f * I1p + cc * VE));
+    };
+    V xpre[U];
+    bool pre = false;
+#ifndef IFCTN_EXP_NO_XEARLY
+    if (P.x_early && q < ncell) {  // first round's X cells before the wait (L2Params::x_early)
+        int c2 = c, d2[NRa];
+#pragma unroll
+        for (int j = 0; j < NRa; ++j) d2[j] = j < NRR ? dg[j] : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            xpre[u] = zero_v<T>();
+            if (q + u * TL < ncell) xpre[u] = x_of(c2, d2);
+            advance(c2, d2);
+        }
+        pre = true;
+    }
+#endif
+    pdl_wait();
+    pdl_launch();
+    // ---- P_v into shared memory ----------------------------------------------------------------
+    T* pv = reinterpret_cast<T*>(l2sm_raw) + (size_t)team * I1p;
+    if (v_ok) {
+        const T* hk = Hb + P.pk_off + jk * I1p;
+        const T* hi = Hb + P.pi_off + ai * I1p;
+        for (int c = tl; c < NC; c += TL) {
+            const V a = *reinterpret_cast<const V*>(hk + c * VE);
+            const V b = *reinterpret_cast<const V*>(hi + c * VE);
+            T x[VE], y[VE];
+            VecT<T>::get(a, x);
+            VecT<T>::get(b, y);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) x[e] *= y[e];
+            *reinterpret_cast<V*>(pv + c * VE) = VecT<T>::make(x);
+        }
+    }
     __syncthreads();
     double tb = 0.0, tw = 0.0;
-    while (q < ncell) {
+    auto do_round = [&](auto first) {
         V xq[U], hq[U][NRa];
         A s[U];
         int co[U];
@@ -394,9 +458,6 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
         for (int u = 0; u < U; ++u) {
             val[u] = q + u * TL < ncell;
             co[u] = c * VE;
-            int f = 0;
-#pragma unroll
-            for (int j = 0; j < NRR; ++j) f += dg[j] * P.rfs[j];
             A sc = A(1);
             if (val[u]) {
                 T pvv[2 * NRa + (NJJ > 0 ? NJJ : 1)];
@@ -414,7 +475,8 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
                         pvv[t++] = Hb[P.jj_off[t3] + dg[j] * P.jj_ma[t3] + dg[j2] * P.jj_mb[t3]];
 #pragma unroll
                 for (int j = 0; j < NRR; ++j) hq[u][j] = *reinterpret_cast<const V*>(Hb + P.rv_off[j] + dg[j] * I1p + co[u]);
-                xq[u] = ld_stream(reinterpret_cast<const V*>(xb + (int64_t)f * I1p + co[u]));
+                if constexpr (decltype(first)::value) xq[u] = xpre[u];
+                else xq[u] = x_of(c, dg);
 #pragma unroll
                 for (int t2 = 0; t2 < 2 * NRR + NJJ; ++t2) sc *= (A)pvv[t2];
             } else {
@@ -423,16 +485,7 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
                 for (int j = 0; j < NRR; ++j) hq[u][j] = zero_v<T>();
             }
             s[u] = sc;
-            // next cell: chunk += dc (mod NC), fibre += ⌊TL/NC⌋ + wrap
-            c += dc;
-            int carry = c >= NC ? 1 : 0;
-            c -= carry ? NC : 0;
-#pragma unroll
-            for (int j = 0; j < NRR; ++j) {
-                int d = dg[j] + ds[j] + carry;
-                carry = (j + 1 < NRR && d >= dm[j]) ? 1 : 0;
-                dg[j] = d - (carry ? dm[j] : 0);
-            }
+            advance(c, dg);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -461,7 +514,9 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
             tw += (double)pw;
         }
         q += U * TL;
-    }
+    };
+    if (pre) do_round(std::true_type{});
+    while (q < ncell) do_round(std::false_type{});
     // ---- the team: lanes (xor butterfly inside the team), its warps in order, then the Z CTAs --
     for (int o = 1; o < 32 && o < TL; o <<= 1) {
         tb += __shfl_xor_sync(0xffffffffu, tb, o);
@@ -537,6 +592,7 @@ struct L2RefillParams {
     int ds[MAXN - 1];     // digits of the per-step fibre stride 8·32/CG
     int tv_off[MAXN - 1]; // H_{0,q}
     int pp_off[MAXP], pp_ld[MAXP];  // H_{q,q'}(i_q, i_q') = H[off + i_q'·ld + i_q], pairs in (q, q') order
+    int x_early;          // launch-time, as L2Params::x_early: first round's X and Ω loads before pdl_wait()
 };
 
 template <typename T, int NO>
@@ -559,6 +615,26 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
     int f = f0 + warp * FL + fl;
     const T* __restrict__ Hb = P.H;
     T* tab = reinterpret_cast<T*>(l2sm_raw);
+    T* xb = P.X + e0;
+    V xpre[U];
+    uint32_t mpre[U];
+    bool pre = false;
+#ifndef IFCTN_EXP_NO_XEARLY
+    if (P.x_early && act && f < f1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int fu = f + u * slots;
+            xpre[u] = zero_v<T>();
+            mpre[u] = ~0u;
+            if (fu < f1) {
+                const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
+                mpre[u] = P.mask[g >> 5] >> (g & 31u);
+                xpre[u] = *reinterpret_cast<const V*>(xb + (size_t)fu * I1p);
+            }
+        }
+        pre = true;
+    }
+#endif
     pdl_wait();
     pdl_launch();
     // tables
@@ -592,8 +668,7 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
     }
     __syncthreads();
     Norms3<T> qn;
-    T* xb = P.X + e0;
-    while (act && f < f1) {
+    auto do_round = [&](auto first) {
         V xq[U];
         T s[U];
         uint32_t mw[U];
@@ -618,9 +693,14 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
 #pragma unroll
                     for (int t2 = 0; t2 < NPP; ++t2) sc *= pv[t2];
                 }
-                const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
-                mw[u] = P.mask[g >> 5] >> (g & 31u);
-                xq[u] = *reinterpret_cast<const V*>(xb + (size_t)fu * I1p);
+                if constexpr (decltype(first)::value) {
+                    mw[u] = mpre[u];
+                    xq[u] = xpre[u];
+                } else {
+                    const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
+                    mw[u] = P.mask[g >> 5] >> (g & 31u);
+                    xq[u] = *reinterpret_cast<const V*>(xb + (size_t)fu * I1p);
+                }
             } else {
                 xq[u] = zero_v<T>();
                 mw[u] = ~0u;
@@ -652,7 +732,9 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
             *reinterpret_cast<V*>(xb + (size_t)(f + u * slots) * I1p) = VecT<T>::make(xn);
         }
         f += U * slots;
-    }
+    };
+    if (pre) do_round(std::true_type{});
+    while (act && f < f1) do_round(std::false_type{});
     double n0 = qn.s0(), n1 = qn.s1(), n2 = qn.s2();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

@@ -217,7 +217,7 @@ template <typename T, int R, int SM>
 // nthr (a multiple of 32, ≤ blockDim.x) threads take part; the others only pass the barriers.
 // red: (nthr/32)·NA + NA doubles of shared scratch, cs: R.
 __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_t j, int nthr,
-                                                 double* red, double* cs) {
+                                                 double* red, double* cs, const T* cold_pre = nullptr) {
     constexpr int NG = R * (R + 1) / 2;
     constexpr int NA = NG + R;
     constexpr int KEEP = 2;  // columns a of G_{i,k} kept in registers for the H refresh
@@ -307,7 +307,7 @@ __device__ __forceinline__ void block_solve_body(const SolveParams<T>& P, int64_
         double rhs[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            cold[r] = (double)P.Gki[j * R + r];
+            cold[r] = (double)(cold_pre ? cold_pre[r] : P.Gki[j * R + r]);
             A[r][r] += P.rho;
             rhs[r] = sum[NG + r] + P.rho * cold[r];
         }
@@ -390,9 +390,17 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
     constexpr int NA = R * (R + 1) / 2 + R;
     __shared__ double red[5 * NA];
     __shared__ double cs[R];
+    // the column's old coefficients were written by this block's solve of the previous sweep (or
+    // at create): at least two kernels back, complete before this grid could start — loaded
+    // ahead of the wait, off the critical path
+    T cold_pre[R];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) cold_pre[r] = P.Gki[(int64_t)blockIdx.x * R + r];
+    }
     pdl_wait();
     pdl_launch();
-    block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs);
+    block_solve_body<T, R, SM>(P, blockIdx.x, 128, red, cs, cold_pre);
 }
 
 // ---- a3 + a4 for large ranks (the paper's grids reach R_{1,2} = 36) --------
