@@ -1351,11 +1351,24 @@ struct Solver : SolverBase {
     // (small ranks: block_solve sums its column's slots itself; `full` forces the reduce for
     // ifctn_block_coefficients).  A skipped reduce keeps an empty profiling interval so that
     // ifctn_profile_sweep still reports [pass, reduce, solve] per block.
-    // after_solve: the previous launch in the stream is a solve of this sweep (see L2Params::x_early)
-    void enqueue_contract(const BlockPlan<T>& b, bool full = false, bool after_solve = false) {
+    // prev: the previous launch in the stream is the solve of that block of this sweep (see
+    // L2Params::x_early: X and the tables of every pair but {prev.k, prev.i} are final)
+    void enqueue_contract(const BlockPlan<T>& b, bool full = false, const BlockPlan<T>* prev = nullptr) {
         if (b.l2) {  // one launch writes β, ω whole; an empty interval for the reduce slot
             L2Params<T> lp = b.l2p;
-            lp.x_early = after_solve ? 1 : 0;
+            lp.x_early = 0;
+            if (prev) {
+                auto same = [&](int a, int c) { return (a == prev->k && c == prev->i) || (a == prev->i && c == prev->k); };
+                lp.x_early = 1;
+                if (lp.kept1) {
+                    for (int j = 0; j < lp.nr; ++j) {
+                        if (!same(0, lp.rmode[j])) lp.x_early |= 2 << j;
+                        if (!same(lp.m, lp.rmode[j])) lp.x_early |= 16 << j;
+                    }
+                } else if (!same(0, lp.k) && !same(0, lp.i)) {
+                    lp.x_early |= 2;
+                }
+            }
             launch(b.l2_fn, b.l2_grid, dim3(kL2Threads), b.l2_smem, lp, true);
             prof_mark();
             return;
@@ -1380,8 +1393,8 @@ struct Solver : SolverBase {
         launch(b.sol_fn, b.sol_grid, dim3(b.sol_threads), b.sol_smem, q, !b.dist);
     }
 
-    void enqueue_block(const BlockPlan<T>& b, bool after_solve = false) {
-        enqueue_contract(b, false, after_solve);
+    void enqueue_block(const BlockPlan<T>& b, const BlockPlan<T>* prev = nullptr) {
+        enqueue_contract(b, false, prev);
         enqueue_solve(b);
     }
 
@@ -1406,10 +1419,10 @@ struct Solver : SolverBase {
         }
     }
 
-    void enqueue_xupdate(bool after_solve = false) {
+    void enqueue_xupdate(const BlockPlan<T>* prev = nullptr) {
         if (l2r) {
             L2RefillParams<T> rp = l2rp;
-            rp.x_early = after_solve ? 1 : 0;
+            rp.x_early = prev ? (prev->k != 0 && prev->i != 0 ? 3 : 1) : 0;
             launch(l2r_fn, l2r_grid, dim3(kL2Threads), l2r_smem, rp, true);
             enqueue_finalize((int64_t)l2r_grid.x * l2r_grid.y, 0);
             return;
@@ -1419,8 +1432,8 @@ struct Solver : SolverBase {
     }
 
     void enqueue_sweep() {
-        for (size_t b = 0; b < blocks.size(); ++b) enqueue_block(blocks[b], b > 0);
-        enqueue_xupdate(true);
+        for (size_t b = 0; b < blocks.size(); ++b) enqueue_block(blocks[b], b > 0 ? &blocks[b - 1] : nullptr);
+        enqueue_xupdate(&blocks.back());
     }
 
     // Fused sweep sequence for a fixed sweep count (eps ≤ 0, no trace):

@@ -76,9 +76,12 @@ struct L2Params {
     int pk_off, pi_off;
     double* scr;           // Z > 1: grid.x·Z·(values per CTA)·2 partials
     unsigned* cnt;         // Z > 1: grid.x arrival counters, zero between launches
-    // launch-time: the predecessor in the stream is a solve of the same sweep (it waits for ITS
-    // predecessor before it lets this grid start, and writes no X), so nothing still running can
-    // write X: the first round's X loads are issued before pdl_wait()
+    // launch-time: bit 0 — the predecessor in the stream is a solve of the same sweep (it waits
+    // for ITS predecessor before it lets this grid start, and writes no X), so nothing still
+    // running can write X: the first rounds' X loads are issued before pdl_wait().  That solve
+    // rewrites one pair matrix H_{k',i'} only; tables built from other pairs are staged before
+    // the wait too: l2_kept bit 1+j — V_j (pair {0,r_j}), bit 4+j — A_j (pair {m,r_j});
+    // l2_red bit 1 — P_v (pairs {0,k}, {0,i}).
     int x_early;
 };
 
@@ -90,6 +93,15 @@ constexpr int kL2U = 4;  // cells in flight per thread (l2_red; l2_kept: l2_kept
 constexpr int kL2RunU = IFCTN_L2_RUN_U;
 #ifndef IFCTN_L2_MINB
 #define IFCTN_L2_MINB 2
+#endif
+// rounds of X loads issued before griddepcontrol.wait (x_early): 2 for third-order tensors, 1 for
+// fourth-order ones (A/B: the second round's 32 registers cost C4 188 -> 192 µs per sweep, and
+// gain C2 58 -> 56, C2r 133 -> 130)
+#ifndef IFCTN_L2_PRE3
+#define IFCTN_L2_PRE3 2
+#endif
+#ifndef IFCTN_L2_PRE4
+#define IFCTN_L2_PRE4 1
 #endif
 
 // per-thread asynchronous global → shared copies (LDGSTS)
@@ -130,6 +142,7 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
     constexpr int U = kL2RunU;
     constexpr int NRa = NR > 0 ? NR : 1;
     static_assert(NR >= 1 && NR <= 2, "l2_kept serves orders 3 and 4");
+    constexpr int kL2Pre = NR == 1 ? IFCTN_L2_PRE3 : IFCTN_L2_PRE4;
     using V = typename VecT<T>::V;
     extern __shared__ __align__(16) unsigned char l2sm_raw[];
     __shared__ double sm[8 * 2 * 32 * VE];  // [warp][β|ω][chunk lane · VE]
@@ -188,55 +201,85 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
             if (u < nv) dst[u] = ld_stream(reinterpret_cast<const V*>(xb + xo + (unsigned)u * xst));
         }
     };
-    V xpre[U];
-    bool pre = false;
+    // next run of this thread
+    auto next_run = [&]() {
+        int carry = 0;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            int d = dg[j] + ds[j] + carry;
+            carry = (j + 1 < NR && d >= dm[j]) ? 1 : 0;
+            dg[j] = d - (carry ? dm[j] : 0);
+        }
+    };
+    V xpre[kL2Pre][U];
+    int npre = 0;
 #ifndef IFCTN_EXP_NO_XEARLY
-    if (P.x_early && act && r < r1) {  // X is not written by anything still running (L2Params::x_early)
-        load_run(xpre);
-        pre = true;
+    if (P.x_early && act) {  // X is not written by anything still running (L2Params::x_early)
+        int sv[NRa];
+#pragma unroll
+        for (int j = 0; j < NR; ++j) sv[j] = dg[j];
+#pragma unroll
+        for (int t = 0; t < kL2Pre; ++t)
+            if (r + t * slots < r1) {
+                load_run(xpre[t]);
+                next_run();
+                npre = t + 1;
+            }
+#pragma unroll
+        for (int j = 0; j < NR; ++j) dg[j] = sv[j];
     }
 #endif
-    pdl_wait();
-    pdl_launch();
     // ---- stage the item's tables (its wpi warps): asynchronous global → shared copies (LDGSTS,
-    // all in flight at once), V_j[d][·] = H_{0,r_j}(chunk group, d) and A_j[d] = H_{m,r_j}(v, d)
-#ifdef IFCTN_EXP_L2_SKIP_STAGE
-    if (P.I1 < 0)
-#endif
-    if (item_ok) {
+    // all in flight at once), V_j[d][·] = H_{0,r_j}(chunk group, d) and A_j[d] = H_{m,r_j}(v, d);
+    // phase 1 = the tables the running predecessor does not write (x_early), before the wait
+    auto stage_tables = [&](int phase) {
+        if (!item_ok) return;
         const int tid = wi * 32 + lane, nt = P.wpi * 32;
         int toff = 0, aoff = P.tab_item - P.asc_item;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
             const int n = P.rdim[j] << lcg;
-            for (int q = tid; q < n; q += nt) {
-                const int d = q >> lcg, c2 = q - (d << lcg);
-                const int ee = (cg * CG + c2) * VE;
-                if (ee < I1p) cp_async16(smem_u32(tab + toff + q * VE), Hb + P.rv_off[j] + d * I1p + ee);
-                else *reinterpret_cast<V*>(tab + toff + q * VE) = zero_v<T>();
+            if (((P.x_early >> (1 + j)) & 1) == phase)
+                for (int q = tid; q < n; q += nt) {
+                    const int d = q >> lcg, c2 = q - (d << lcg);
+                    const int ee = (cg * CG + c2) * VE;
+                    if (ee < I1p) cp_async16(smem_u32(tab + toff + q * VE), Hb + P.rv_off[j] + d * I1p + ee);
+                    else *reinterpret_cast<V*>(tab + toff + q * VE) = zero_v<T>();
+                }
+            if (((P.x_early >> (4 + j)) & 1) == phase) {
+                const int ksb = P.ks_off[j] + v * P.ks_mv[j];
+                for (int d = tid; d < P.rdim[j]; d += nt) cp_async_scalar<T>(smem_u32(tab + aoff + d), Hb + ksb + d * P.ks_mj[j]);
             }
-            const int ksb = P.ks_off[j] + v * P.ks_mv[j];
-            for (int d = tid; d < P.rdim[j]; d += nt) cp_async_scalar<T>(smem_u32(tab + aoff + d), Hb + ksb + d * P.ks_mj[j]);
             toff += n * VE;
             aoff += P.rdim[j];
         }
-    }
+    };
+#ifdef IFCTN_EXP_L2_SKIP_STAGE
+    if (P.I1 < 0)
+#endif
+    if (P.x_early >> 1) stage_tables(1);
+    pdl_wait();
+    pdl_launch();
+#ifdef IFCTN_EXP_L2_SKIP_STAGE
+    if (P.I1 < 0)
+#endif
+    stage_tables(0);
     cp_async_wait_all();
     __syncthreads();
 
     T sb[VE], sw[VE];
 #pragma unroll
     for (int e = 0; e < VE; ++e) sb[e] = sw[e] = T(0);
-    // one run; first = its X cells were loaded before the wait (xpre)
+    // one run; first > 0: its X cells were loaded before the wait (xpre[first − 1])
     auto do_run = [&](auto first) {
         const int d0s = dg[0] * U;
         const int nv = min(U, rdim0 - d0s);
         // loads of the run: X cells and the scalars H_{r_0,r_1}(d0, d_1)
         V xq[U];
         T p[U];
-        if constexpr (decltype(first)::value) {
+        if constexpr (decltype(first)::value > 0) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) xq[u] = xpre[u];
+            for (int u = 0; u < U; ++u) xq[u] = xpre[decltype(first)::value - 1][u];
         } else {
             load_run(xq);
         }
@@ -273,22 +316,17 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_kept(const __gri
                 accumulate<T, VE>(w, x, sb, sw);
             }
         }
-        // next run of this thread
-        int carry = 0;
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-            int d = dg[j] + ds[j] + carry;
-            carry = (j + 1 < NR && d >= dm[j]) ? 1 : 0;
-            dg[j] = d - (carry ? dm[j] : 0);
-        }
+        next_run();
         r += slots;
     };
 #ifdef IFCTN_EXP_L2_SKIP_MAIN  // timing experiments only (wrong results): fixed cost of the kernel
     if (P.I1 < 0)
 #endif
     {
-        if (pre) do_run(std::true_type{});
-        while (act && r < r1) do_run(std::false_type{});
+        if (npre > 0) do_run(std::integral_constant<int, 1>{});
+        if constexpr (kL2Pre > 1)
+            if (npre > 1) do_run(std::integral_constant<int, 2>{});
+        while (act && r < r1) do_run(std::integral_constant<int, 0>{});
     }
     // ---- fibre lanes (xor butterfly, fp64), then the item's warps, then the Z CTAs -----------
     double db[VE], dw[VE];
@@ -360,6 +398,7 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
     constexpr int U = kL2U;
     constexpr int NRa = NRR > 0 ? NRR : 1;
     constexpr int NJJ = NRR * (NRR - 1) / 2;
+    constexpr int kL2Pre = NRR == 0 ? IFCTN_L2_PRE3 : IFCTN_L2_PRE4;
     using V = typename VecT<T>::V;
     using A = std::conditional_t<(NRR >= 2), double, T>;  // orders ≥ 5: see l2_kept
     extern __shared__ __align__(16) unsigned char l2sm_raw[];
@@ -413,26 +452,33 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
         for (int j = 0; j < NRR; ++j) f += dd[j] * P.rfs[j];
         return ld_stream(reinterpret_cast<const V*>(xb + (int64_t)f * I1p + cc * VE));
     };
-    V xpre[U];
-    bool pre = false;
+    V xpre[kL2Pre][U];
+    int npre = 0;
 #ifndef IFCTN_EXP_NO_XEARLY
-    if (P.x_early && q < ncell) {  // first round's X cells before the wait (L2Params::x_early)
+    if (P.x_early) {  // the first rounds' X cells before the wait (L2Params::x_early)
         int c2 = c, d2[NRa];
 #pragma unroll
         for (int j = 0; j < NRa; ++j) d2[j] = j < NRR ? dg[j] : 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            xpre[u] = zero_v<T>();
-            if (q + u * TL < ncell) xpre[u] = x_of(c2, d2);
-            advance(c2, d2);
-        }
-        pre = true;
+        for (int t = 0; t < kL2Pre; ++t)
+            if (q + t * U * TL < ncell) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    xpre[t][u] = zero_v<T>();
+                    if (q + (t * U + u) * TL < ncell) xpre[t][u] = x_of(c2, d2);
+                    advance(c2, d2);
+                }
+                npre = t + 1;
+            }
     }
 #endif
-    pdl_wait();
-    pdl_launch();
-    // ---- P_v into shared memory ----------------------------------------------------------------
+    // ---- P_v into shared memory (before the wait when the running solve writes neither pair) ----
     T* pv = reinterpret_cast<T*>(l2sm_raw) + (size_t)team * I1p;
+    const bool pv_early = (P.x_early >> 1) & 1;
+    if (!pv_early) {
+        pdl_wait();
+        pdl_launch();
+    }
     if (v_ok) {
         const T* hk = Hb + P.pk_off + jk * I1p;
         const T* hi = Hb + P.pi_off + ai * I1p;
@@ -446,6 +492,10 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
             for (int e = 0; e < VE; ++e) x[e] *= y[e];
             *reinterpret_cast<V*>(pv + c * VE) = VecT<T>::make(x);
         }
+    }
+    if (pv_early) {
+        pdl_wait();
+        pdl_launch();
     }
     __syncthreads();
     double tb = 0.0, tw = 0.0;
@@ -475,7 +525,7 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
                         pvv[t++] = Hb[P.jj_off[t3] + dg[j] * P.jj_ma[t3] + dg[j2] * P.jj_mb[t3]];
 #pragma unroll
                 for (int j = 0; j < NRR; ++j) hq[u][j] = *reinterpret_cast<const V*>(Hb + P.rv_off[j] + dg[j] * I1p + co[u]);
-                if constexpr (decltype(first)::value) xq[u] = xpre[u];
+                if constexpr (decltype(first)::value > 0) xq[u] = xpre[decltype(first)::value - 1][u];
                 else xq[u] = x_of(c, dg);
 #pragma unroll
                 for (int t2 = 0; t2 < 2 * NRR + NJJ; ++t2) sc *= (A)pvv[t2];
@@ -515,8 +565,10 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_red(const __grid
         }
         q += U * TL;
     };
-    if (pre) do_round(std::true_type{});
-    while (q < ncell) do_round(std::false_type{});
+    if (npre > 0) do_round(std::integral_constant<int, 1>{});
+    if constexpr (kL2Pre > 1)
+        if (npre > 1) do_round(std::integral_constant<int, 2>{});
+    while (q < ncell) do_round(std::integral_constant<int, 0>{});
     // ---- the team: lanes (xor butterfly inside the team), its warps in order, then the Z CTAs --
     for (int o = 1; o < 32 && o < TL; o <<= 1) {
         tb += __shfl_xor_sync(0xffffffffu, tb, o);
@@ -592,7 +644,8 @@ struct L2RefillParams {
     int ds[MAXN - 1];     // digits of the per-step fibre stride 8·32/CG
     int tv_off[MAXN - 1]; // H_{0,q}
     int pp_off[MAXP], pp_ld[MAXP];  // H_{q,q'}(i_q, i_q') = H[off + i_q'·ld + i_q], pairs in (q, q') order
-    int x_early;          // launch-time, as L2Params::x_early: first round's X and Ω loads before pdl_wait()
+    int x_early;          // launch-time, as L2Params::x_early: bit 0 — first rounds' X and Ω loads before
+                          // pdl_wait(); bit 1 — the H_{0,q} tables too (the running solve's pair has no mode 0)
 };
 
 template <typename T, int NO>
@@ -600,6 +653,7 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
     constexpr int VE = 16 / (int)sizeof(T);
     constexpr int U = kL2U;
     constexpr int NPP = NO * (NO - 1) / 2;
+    constexpr int kL2Pre = NO <= 2 ? IFCTN_L2_PRE3 : IFCTN_L2_PRE4;
     using V = typename VecT<T>::V;
     extern __shared__ __align__(16) unsigned char l2sm_raw[];
     __shared__ double sm[8 * 3];
@@ -616,27 +670,34 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
     const T* __restrict__ Hb = P.H;
     T* tab = reinterpret_cast<T*>(l2sm_raw);
     T* xb = P.X + e0;
-    V xpre[U];
-    uint32_t mpre[U];
-    bool pre = false;
+    V xpre[kL2Pre][U];
+    uint32_t mpre[kL2Pre][U];
+    int npre = 0;
 #ifndef IFCTN_EXP_NO_XEARLY
-    if (P.x_early && act && f < f1) {
+    if (P.x_early && act) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int fu = f + u * slots;
-            xpre[u] = zero_v<T>();
-            mpre[u] = ~0u;
-            if (fu < f1) {
-                const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
-                mpre[u] = P.mask[g >> 5] >> (g & 31u);
-                xpre[u] = *reinterpret_cast<const V*>(xb + (size_t)fu * I1p);
+        for (int t = 0; t < kL2Pre; ++t)
+            if (f + t * U * slots < f1) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int fu = f + (t * U + u) * slots;
+                    xpre[t][u] = zero_v<T>();
+                    mpre[t][u] = ~0u;
+                    if (fu < f1) {
+                        const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
+                        mpre[t][u] = P.mask[g >> 5] >> (g & 31u);
+                        xpre[t][u] = *reinterpret_cast<const V*>(xb + (size_t)fu * I1p);
+                    }
+                }
+                npre = t + 1;
             }
-        }
-        pre = true;
     }
 #endif
-    pdl_wait();
-    pdl_launch();
+    const bool tab_early = (P.x_early >> 1) & 1;
+    if (!tab_early) {
+        pdl_wait();
+        pdl_launch();
+    }
     // tables
     {
         int toff = 0;
@@ -650,6 +711,10 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
                 else *reinterpret_cast<V*>(tab + toff + t * VE) = zero_v<T>();
             }
             toff += n * VE;
+        }
+        if (tab_early) {
+            pdl_wait();
+            pdl_launch();
         }
         cp_async_wait_all();
     }
@@ -693,9 +758,9 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
 #pragma unroll
                     for (int t2 = 0; t2 < NPP; ++t2) sc *= pv[t2];
                 }
-                if constexpr (decltype(first)::value) {
-                    mw[u] = mpre[u];
-                    xq[u] = xpre[u];
+                if constexpr (decltype(first)::value > 0) {
+                    mw[u] = mpre[decltype(first)::value - 1][u];
+                    xq[u] = xpre[decltype(first)::value - 1][u];
                 } else {
                     const unsigned g = (unsigned)fu * (unsigned)I1p + (unsigned)e0;
                     mw[u] = P.mask[g >> 5] >> (g & 31u);
@@ -733,8 +798,10 @@ __global__ void __launch_bounds__(kL2Threads, IFCTN_L2_MINB) l2_refill(const __g
         }
         f += U * slots;
     };
-    if (pre) do_round(std::true_type{});
-    while (act && f < f1) do_round(std::false_type{});
+    if (npre > 0) do_round(std::integral_constant<int, 1>{});
+    if constexpr (kL2Pre > 1)
+        if (npre > 1) do_round(std::integral_constant<int, 2>{});
+    while (act && f < f1) do_round(std::integral_constant<int, 0>{});
     double n0 = qn.s0(), n1 = qn.s1(), n2 = qn.s2();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

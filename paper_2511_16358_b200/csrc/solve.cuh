@@ -645,12 +645,6 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     double* cv = rhs + Rp;
     double* cold = cv + Rp;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
-    unsigned long long pe = 0;  // peer exchange (peer.cuh): FROM_PROJ is the consumer
-    if constexpr (SM == SOLVE_FROM_PROJ)
-        if (P.use_peer) {
-            pe = peer_next_epoch(P.peer);
-            peer_publish_wait(P.peer, pe);
-        }
     const int nt = Rp / 4;
     const int ntg = nt * (nt + 1) / 2;     // Gram tiles; then nt rhs tiles
     const int ntasks = ntg + nt;
@@ -673,6 +667,19 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         }
     }
     auto stage = [&](int64_t a0, int na) { stage_factor_fp64<T>(P.Gik + a0 * R, na * R, Rp, gs, tid, nthr); };
+    // G_{i,k} was written by the solve of block (i,k): at least two kernels back, complete
+    // before this grid could start — its first tile is staged ahead of the wait, while the
+    // predecessor (the a2 pass of this block) still runs
+    if constexpr (SM != SOLVE_FROM_PROJ) stage(0, (int)min((int64_t)TA, P.Ii));
+    const T cold_pre = tid < R ? P.Gki[j * R + tid] : T(0);  // this block's previous solve: same argument
+    pdl_wait();
+    pdl_launch();
+    unsigned long long pe = 0;  // peer exchange (peer.cuh): FROM_PROJ is the consumer
+    if constexpr (SM == SOLVE_FROM_PROJ)
+        if (P.use_peer) {
+            pe = peer_next_epoch(P.peer);
+            peer_publish_wait(P.peer, pe);
+        }
     if constexpr (SM != SOLVE_FROM_PROJ) {
         double acc[4][4];
 #pragma unroll
@@ -681,8 +688,10 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
         for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
             const int na = (int)min((int64_t)TA, P.Ii - a0);
-            __syncthreads();
-            stage(a0, na);
+            if (a0 > 0) {
+                __syncthreads();
+                stage(a0, na);
+            }
             PHASE_CLK(6);
             for (int a = tid; a < na; a += nthr) {
                 om[a] = P.omega[j * P.Ii + a0 + a];
@@ -779,7 +788,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     PHASE_CLK(2);
     // + ρI, + ρ c_old
     if (tid < R) {
-        const double co = (double)P.Gki[j * R + tid];
+        const double co = (double)cold_pre;
         cold[tid] = co;
         A[tid * LDA + tid] += P.rho;
         rhs[tid] += P.rho * co;
@@ -942,9 +951,7 @@ template <typename T, int SM>
 __global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
     extern __shared__ __align__(16) double bsm[];
     __shared__ int ok;
-    pdl_wait();
-    pdl_launch();
-    block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok);
+    block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok);  // waits for its predecessor itself
 }
 
 // ---- a1: build H_{p,q} = G_{p,q}ᵀ G_{q,p} for one pair (K=R skinny product; FMA pipes) ---
