@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _abi
 from ._abi import (IFCTN_F32, IFCTN_F64, IFCTN_FLAG_NO_FUSE, IFCTN_FLAG_NO_GRAPH,  # noqa: F401
-                   IFCTN_FLAG_GRAM_GEMM, IFCTN_FLAG_NO_L2PASS, IFCTN_FLAG_NO_PDL, IFCTN_FLAG_NO_SOLVE_REDUCE, IFCTN_FLAG_NO_VBLOCK,
+                   IFCTN_FLAG_GRAM_GEMM, IFCTN_FLAG_NO_DMMA, IFCTN_FLAG_NO_L2PASS, IFCTN_FLAG_NO_PDL, IFCTN_FLAG_NO_SOLVE_REDUCE, IFCTN_FLAG_NO_VBLOCK,
                    IFCTN_FLAG_NONE, IFCTN_FLAG_X_FULL, IFCTN_MODEL, IFCTN_X, IfctnError,
                    ifctn_dist, ifctn_trace_row)
 

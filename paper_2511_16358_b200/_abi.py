@@ -22,6 +22,7 @@ IFCTN_FLAG_NO_SOLVE_REDUCE = 64
 IFCTN_FLAG_NO_L2PASS = 128
 IFCTN_FLAG_GRAM_GEMM = 256
 IFCTN_FLAG_NO_PDL = 512
+IFCTN_FLAG_NO_DMMA = 1024
 IFCTN_MAX_ORDER, IFCTN_MAX_RANK = 6, 64
 
 STATUS = ["IFCTN_OK", "IFCTN_E_ARG", "IFCTN_E_SHAPE", "IFCTN_E_RANKS", "IFCTN_E_WORKSPACE",

@@ -419,6 +419,9 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
 //     trailing-update chain and no CTA barriers; forward/back substitution; ‖Δc‖²;
 //   * row j of H_{k,i} (8 threads per a).
 constexpr int kBigThreads = 256;
+#ifndef IFCTN_BIG_MINB  // CTAs per SM the register allocation allows
+#define IFCTN_BIG_MINB 1
+#endif
 
 __host__ __device__ inline int big_solve_rp(int R) { return (R + 3) & ~3; }
 __host__ __device__ inline int big_solve_lda(int R) { return big_solve_rp(R) + 1; }  // odd: rows hit different banks
@@ -623,6 +626,97 @@ __global__ void __launch_bounds__(kBigThreads) gram_project(const SolveParams<T>
 #endif
 }
 
+// ---- a3 for large ranks on the fp64 tensor cores ---------------------------
+// D(8×8) += A(8×4, row-major) · B(4×8, column-major), all fp64 (SASS DMMA.8x8x4): lane l holds
+// A[l/4][l%4], B[l%4][l/4] and D[l/4][2(l%4)], D[l/4][2(l%4)+1].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// [Gram_j | rhs_j] = Σ_a g_a · [ω(a,j) g_aᵀ | β(a,j)] (Eq. 8) as one fp64 product with
+// M = R rows r, N = R + 1 columns (s < R: the Gram, s = R: the rhs), K = I_i, on m8n8k4 tiles:
+// NRT row tiles; the column tiles are the same NRT (the rhs column rides in the last one's
+// padding) or, when R = 8·NRT (EXTRA), one more.  Only tiles on or above the diagonal are
+// computed.  Warp w takes the k-steps (4 values of a) w, w + 8, … of a staged tile and holds
+// every output tile: per k-step NRT fragment loads of g (conflict-free for R ≡ 4 mod 8), two
+// scalar loads and NRT multiplies feed NRT(NRT+1)/2 (+NRT) DMMAs.  The 8 warps' partial tiles
+// are added into A / rhs in warp order (fixed order, deterministic).  a ≥ na reads row na − 1
+// with zero weights; rows/columns ≥ R of the tiles read finite padding and are not stored.
+// the later staging tiles of big_gram_mma (long modes only): a call, so that its loads in flight
+// do not add to the registers of the loop that holds every output tile
+template <typename T>
+__device__ __noinline__ void stage_factor_fp64_call(const T* src, int n, int pad, double* gs, int tid, int nthr) {
+    stage_factor_fp64<T>(src, n, pad, gs, tid, nthr);
+}
+
+template <typename T, int NRT, bool EXTRA>
+__device__ __forceinline__ void big_gram_mma(const SolveParams<T>& P, int64_t j, double* gs, double* A,
+                                             double* om, double* be, double* rhs) {
+    constexpr int NCT = NRT + (EXTRA ? 1 : 0);
+    constexpr int NTILE = NRT * (NRT + 1) / 2 + (EXTRA ? NRT : 0);
+    const int R = P.R, LDA = big_solve_lda(R), TA = P.ta;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, wi = tid >> 5, nw = nthr >> 5;
+    const int lk = lane & 3, lq = lane >> 2;
+    double acc[NTILE][2];
+#pragma unroll
+    for (int t = 0; t < NTILE; ++t) acc[t][0] = acc[t][1] = 0.0;
+    for (int64_t a0 = 0; a0 < P.Ii; a0 += TA) {
+        const int na = (int)min((int64_t)TA, P.Ii - a0);
+        if (a0 > 0) {
+            __syncthreads();
+            stage_factor_fp64_call<T>(P.Gik + a0 * R, na * R, big_solve_rp(R), gs, tid, nthr);
+        }
+        for (int a = tid; a < na; a += nthr) {
+            om[a] = P.omega[j * P.Ii + a0 + a];
+            be[a] = P.beta[j * P.Ii + a0 + a];
+        }
+        __syncthreads();
+        for (int ks = wi; 4 * ks < na; ks += nw) {
+            const int a = 4 * ks + lk;
+            const bool in = a < na;
+            const double w = in ? om[a] : 0.0, b = in ? be[a] : 0.0;
+            const double* gr = gs + min(a, na - 1) * R + lq;
+            double fa[NRT], fb[NCT];
+#pragma unroll
+            for (int t = 0; t < NRT; ++t) fa[t] = gr[8 * t];
+#pragma unroll
+            for (int t = 0; t < NRT; ++t) {
+                const int s = 8 * t + lq;
+                fb[t] = (t + 1 < NRT || s < R) ? w * fa[t] : (s == R ? b : 0.0);
+            }
+            if constexpr (EXTRA) fb[NRT] = lq == 0 ? b : 0.0;
+            int t = 0;
+#pragma unroll
+            for (int tr = 0; tr < NRT; ++tr)
+#pragma unroll
+                for (int tc = tr; tc < NCT; ++tc, ++t) dmma884(acc[t][0], acc[t][1], fa[tr], fb[tc]);
+        }
+    }
+    for (int h = 0; h < nw; ++h) {
+        __syncthreads();
+        if (wi == h) {
+            int t = 0;
+#pragma unroll
+            for (int tr = 0; tr < NRT; ++tr)
+#pragma unroll
+                for (int tc = tr; tc < NCT; ++tc, ++t) {
+                    const int r = 8 * tr + lq;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int s = 8 * tc + 2 * lk + e;
+                        if (r < R && s <= R && r <= s) {
+                            double* d = s < R ? A + r * LDA + s : rhs + r;
+                            *d = (h ? *d : 0.0) + acc[t][e];
+                        }
+                    }
+                }
+        }
+    }
+    __syncthreads();
+}
+
 #ifdef IFCTN_EXP_PHASE_CLOCKS  // diagnosis builds only: per-phase clocks of CTA 0
 #define PHASE_CLK(q) \
     if (j == 0 && threadIdx.x == 0) clk[q] = clock64();
@@ -681,6 +775,21 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             peer_publish_wait(P.peer, pe);
         }
     if constexpr (SM != SOLVE_FROM_PROJ) {
+      // ≤ 15 output tiles per warp: R ≤ 39 (P.mma, set at plan time); else the SIMT tiles below
+      bool by_mma = P.mma != 0;
+      if (by_mma) {
+        PHASE_CLK(6);
+        PHASE_CLK(7);
+        switch ((R + 7) >> 3) {
+            case 2: if (R & 7) big_gram_mma<T, 2, false>(P, j, gs, A, om, be, rhs); else big_gram_mma<T, 2, true>(P, j, gs, A, om, be, rhs); break;
+            case 3: if (R & 7) big_gram_mma<T, 3, false>(P, j, gs, A, om, be, rhs); else big_gram_mma<T, 3, true>(P, j, gs, A, om, be, rhs); break;
+            case 4: if (R & 7) big_gram_mma<T, 4, false>(P, j, gs, A, om, be, rhs); else big_gram_mma<T, 4, true>(P, j, gs, A, om, be, rhs); break;
+            case 5: if (R & 7) big_gram_mma<T, 5, false>(P, j, gs, A, om, be, rhs); else by_mma = false; break;
+            default: by_mma = false;
+        }
+        PHASE_CLK(1);
+      }
+      if (!by_mma) {
         double acc[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -746,6 +855,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             }
         }
         __syncthreads();
+      }
         if constexpr (SM == SOLVE_PROJECT) {
             // this rank's partial [upper triangle (r ≤ s, row-major), rhs] for the all-reduce
             double* pdst = P.use_peer ? peer_my_slot(P.peer) : P.proj;
@@ -948,7 +1058,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
 }
 
 template <typename T, int SM>
-__global__ void __launch_bounds__(kBigThreads) block_solve_big(const SolveParams<T> P) {
+__global__ void __launch_bounds__(kBigThreads, IFCTN_BIG_MINB) block_solve_big(const SolveParams<T> P) {
     extern __shared__ __align__(16) double bsm[];
     __shared__ int ok;
     block_solve_big_body<T, SM>(P, blockIdx.x, bsm, &ok);  // waits for its predecessor itself

@@ -402,6 +402,13 @@ EDGE = [
      "float32"),
     # G_{i,k} (12 × 2100) too large to stage at once: the tiled staging path of the solve
     ("rank12_long_mode", (8, 2100, 3), 12, "float32"),
+    # the fp64 tensor-core Gram (big_gram_mma): 2-5 row tiles, ranks that are multiples of 8 (the
+    # rhs column opens a tile of its own), I_i not a multiple of the k-step, R = 40 (SIMT tiles)
+    ("mma_tiles_f64", (74, 66, 69, 3), [[0, 16, 24, 3], [16, 0, 32, 2], [24, 32, 0, 2], [3, 2, 2, 0]],
+     "float64"),
+    ("mma_rank39_40", (98, 90, 4), [[0, 39, 4], [39, 0, 40], [4, 40, 0]], "float32"),
+    # R = 36 with G_{i,k} (36 × 400) staged in 32-column tiles
+    ("mma_rank36_tiled", (6, 400, 3), [[0, 36, 2], [36, 0, 3], [2, 3, 0]], "float32"),
 ]
 
 
@@ -421,6 +428,18 @@ def test_edge_shapes_one_sweep(label, dims, R, dtype):
         tol = 1e-7
     assert rel(s.factors().cpu().numpy(), G) <= tol
     assert rel(s.reconstruct().cpu().numpy(), X) <= tol
+
+
+def test_tensor_core_gram_matches_simt_gram():
+    """Large-rank Gram/RHS on the fp64 tensor cores (default) against the SIMT fp64 tiles
+    (IFCTN_FLAG_NO_DMMA): the same fp64 products in another summation order."""
+    from paper_2511_16358_b200 import IFCTN_FLAG_NO_DMMA
+    p = make_config("C2rs")
+    a, b = make_solver(p), make_solver(p, flags=IFCTN_FLAG_NO_DMMA)
+    a.sweep(3)
+    b.sweep(3)
+    assert rel(a.factors().cpu().numpy(), b.factors().cpu().numpy()) <= 1e-5
+    assert rel(a.reconstruct().cpu().numpy(), b.reconstruct().cpu().numpy()) <= 1e-5
 
 
 def test_fully_observed_and_single_observation():
