@@ -1268,11 +1268,11 @@ struct Solver : SolverBase {
                 b.sol_grid = dim3((unsigned)s.ld[k]);
                 if (q.R > MAXR_SMALL) {  // large-rank path (§8(f1)): a CTA per column
                     b.sol_threads = kBigThreads;
-                    // stage all of G_{i,k} at once when it fits in ≈ 96 KB, else 32-column tiles
-                    const size_t cap = std::min<size_t>(smem_limit - 8 * 1024, 96 * 1024);
+                    // stage all of G_{i,k} at once when it fits in ≈ 110 KB (two CTAs per SM), else 32-column tiles
+                    const size_t cap = std::min<size_t>(smem_limit - 8 * 1024, 110 * 1024);
                     q.ta = (int)s.ld[i];
                     if (big_solve_smem(q.R, q.ta, (int)s.esize) > cap) q.ta = 32;
-                    q.mma = (q.R <= 39 && !(flags & IFCTN_FLAG_NO_DMMA)) ? 1 : 0;
+                    q.mma = (q.R <= kBigMmaMaxR && !(flags & IFCTN_FLAG_NO_DMMA)) ? 1 : 0;
                     b.sol_smem = big_solve_smem(q.R, q.ta, (int)s.esize);
                     if (b.sol_smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "rank too large for the solve kernel");
                     for (int m = 0; m < 3; ++m) {  // allow the device maximum (static smem aside)

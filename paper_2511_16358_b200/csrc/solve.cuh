@@ -423,13 +423,16 @@ constexpr int kBigThreads = 256;
 #define IFCTN_BIG_MINB 1
 #endif
 
+constexpr int kBigMmaMaxR = 39;  // big_gram_mma: ≤ 15 output tiles (30 accumulators) per warp
+constexpr int kBigTPR = 4;       // big_gram_mma: tiles per round of its cross-warp sum (scratch: 8 warps × 4 × 64)
 __host__ __device__ inline int big_solve_rp(int R) { return (R + 3) & ~3; }
 __host__ __device__ inline int big_solve_lda(int R) { return big_solve_rp(R) + 1; }  // odd: rows hit different banks
 // shared memory: G tile (ta·R + Rp doubles) + fp64 [A: Rp rows of lda, ω, β (ta each),
-// rhs, c, c_old (Rp each)]
+// rhs, c, c_old (Rp each), the mma path's cross-warp scratch]
 __host__ __device__ inline size_t big_solve_smem(int R, int ta, int /*esize*/) {
     const int Rp = big_solve_rp(R);
-    return sizeof(double) * ((size_t)ta * R + Rp + (size_t)Rp * big_solve_lda(R) + 2 * (size_t)ta + 3 * (size_t)Rp);
+    return sizeof(double) * ((size_t)ta * R + Rp + (size_t)Rp * big_solve_lda(R) + 2 * (size_t)ta + 3 * (size_t)Rp +
+                             (R <= kBigMmaMaxR ? (kBigThreads / 32) * kBigTPR * 64 + 1 : 0));
 }
 
 // G_{i,k}(:, a0 …) (n = na·R elements of T) into shared memory as fp64, followed by `pad` zeros
@@ -653,11 +656,11 @@ __device__ __noinline__ void stage_factor_fp64_call(const T* src, int n, int pad
 
 template <typename T, int NRT, bool EXTRA>
 __device__ __forceinline__ void big_gram_mma(const SolveParams<T>& P, int64_t j, double* gs, double* A,
-                                             double* om, double* be, double* rhs) {
+                                             double* om, double* be, double* rhs, double* scr) {
     constexpr int NCT = NRT + (EXTRA ? 1 : 0);
     constexpr int NTILE = NRT * (NRT + 1) / 2 + (EXTRA ? NRT : 0);
     const int R = P.R, LDA = big_solve_lda(R), TA = P.ta;
-    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, wi = tid >> 5, nw = nthr >> 5;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, wi = tid >> 5, nw = kBigThreads / 32;
     const int lk = lane & 3, lq = lane >> 2;
     double acc[NTILE][2];
 #pragma unroll
@@ -694,24 +697,33 @@ __device__ __forceinline__ void big_gram_mma(const SolveParams<T>& P, int64_t j,
                 for (int tc = tr; tc < NCT; ++tc, ++t) dmma884(acc[t][0], acc[t][1], fa[tr], fb[tc]);
         }
     }
-    for (int h = 0; h < nw; ++h) {
+    // rounds of kBigTPR tiles: every warp writes its partial tiles (16 bytes per lane, contiguous),
+    // then one thread per entry sums the 8 partials in warp order and stores the entry
+    constexpr int NQ = (NTILE + kBigTPR - 1) / kBigTPR;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
         __syncthreads();
-        if (wi == h) {
-            int t = 0;
 #pragma unroll
-            for (int tr = 0; tr < NRT; ++tr)
+        for (int tt = 0; tt < kBigTPR; ++tt)
+            if (q * kBigTPR + tt < NTILE)
+                *reinterpret_cast<double2*>(scr + (wi * kBigTPR + tt) * 64 + 2 * lane) =
+                    make_double2(acc[q * kBigTPR + tt][0], acc[q * kBigTPR + tt][1]);
+        __syncthreads();
+        const int tt = tid >> 6, idx = tid & 63, t = q * kBigTPR + tt;
+        if (t < NTILE) {
+            double v[kBigThreads / 32];
 #pragma unroll
-                for (int tc = tr; tc < NCT; ++tc, ++t) {
-                    const int r = 8 * tr + lq;
+            for (int w8 = 0; w8 < kBigThreads / 32; ++w8) v[w8] = scr[(w8 * kBigTPR + tt) * 64 + idx];
+            double sum = v[0];
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int s = 8 * tc + 2 * lk + e;
-                        if (r < R && s <= R && r <= s) {
-                            double* d = s < R ? A + r * LDA + s : rhs + r;
-                            *d = (h ? *d : 0.0) + acc[t][e];
-                        }
-                    }
-                }
+            for (int w8 = 1; w8 < kBigThreads / 32; ++w8) sum += v[w8];
+            int tr = 0, rem = t;  // tile t = (tr, tr + rem) in the order the k-loop enumerates them
+            while (rem >= NCT - tr) {
+                rem -= NCT - tr;
+                ++tr;
+            }
+            const int r = 8 * tr + (idx >> 3), sc = 8 * (tr + rem) + (idx & 7);
+            if (r < R && sc <= R && r <= sc) *(sc < R ? A + r * LDA + sc : rhs + r) = sum;
         }
     }
     __syncthreads();
@@ -738,6 +750,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     double* rhs = be + TA;
     double* cv = rhs + Rp;
     double* cold = cv + Rp;
+    double* scr = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(cold + Rp) + 15) & ~uintptr_t(15));  // big_gram_mma
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
     const int nt = Rp / 4;
     const int ntg = nt * (nt + 1) / 2;     // Gram tiles; then nt rhs tiles
@@ -781,10 +794,10 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         PHASE_CLK(6);
         PHASE_CLK(7);
         switch ((R + 7) >> 3) {
-            case 2: if (R & 7) big_gram_mma<T, 2, false>(P, j, gs, A, om, be, rhs); else big_gram_mma<T, 2, true>(P, j, gs, A, om, be, rhs); break;
-            case 3: if (R & 7) big_gram_mma<T, 3, false>(P, j, gs, A, om, be, rhs); else big_gram_mma<T, 3, true>(P, j, gs, A, om, be, rhs); break;
-            case 4: if (R & 7) big_gram_mma<T, 4, false>(P, j, gs, A, om, be, rhs); else big_gram_mma<T, 4, true>(P, j, gs, A, om, be, rhs); break;
-            case 5: if (R & 7) big_gram_mma<T, 5, false>(P, j, gs, A, om, be, rhs); else by_mma = false; break;
+            case 2: if (R & 7) big_gram_mma<T, 2, false>(P, j, gs, A, om, be, rhs, scr); else big_gram_mma<T, 2, true>(P, j, gs, A, om, be, rhs, scr); break;
+            case 3: if (R & 7) big_gram_mma<T, 3, false>(P, j, gs, A, om, be, rhs, scr); else big_gram_mma<T, 3, true>(P, j, gs, A, om, be, rhs, scr); break;
+            case 4: if (R & 7) big_gram_mma<T, 4, false>(P, j, gs, A, om, be, rhs, scr); else big_gram_mma<T, 4, true>(P, j, gs, A, om, be, rhs, scr); break;
+            case 5: if (R & 7) big_gram_mma<T, 5, false>(P, j, gs, A, om, be, rhs, scr); else by_mma = false; break;
             default: by_mma = false;
         }
         PHASE_CLK(1);
