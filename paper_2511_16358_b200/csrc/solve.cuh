@@ -994,31 +994,29 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         // L y = rhs, Lᵀ c = y with rhs in registers (lane owns rows lane, lane + 32) and the
         // pivot value broadcast by shuffle; the L entries are independent shared loads
         double x0 = lane < R ? rhs[lane] : 0.0, x1 = lane + 32 < R ? rhs[lane + 32] : 0.0;
-        // The dependent chain per step is shuffle → fma: the pivot reciprocal d is folded into
-        // the column entries (l·d, off the chain) instead of scaling x_r before the broadcast.
         for (int r = 0; r < R; ++r) {
-            const double d = A[r * LDA + r];
-            const double lq0 = (lane > r && lane < R ? A[lane * LDA + r] : 0.0) * d;
-            const double lq1 = (lane + 32 > r && lane + 32 < R ? A[(lane + 32) * LDA + r] : 0.0) * d;
-            const double y = __shfl_sync(0xffffffffu, r < 32 ? x0 : x1, r & 31);
+            const double lq0 = lane > r && lane < R ? A[lane * LDA + r] : 0.0;
+            const double lq1 = lane + 32 > r && lane + 32 < R ? A[(lane + 32) * LDA + r] : 0.0;
+            const double own = (r < 32 ? x0 : x1) * A[r * LDA + r];
+            const double y = __shfl_sync(0xffffffffu, own, r & 31);
+            if (lane == (r & 31)) {
+                if (r < 32) x0 = y;
+                else x1 = y;
+            }
             x0 = fma(-lq0, y, x0);
             x1 = fma(-lq1, y, x1);
-            if (lane == (r & 31)) {
-                if (r < 32) x0 = y * d;
-                else x1 = y * d;
-            }
         }
         for (int r = R - 1; r >= 0; --r) {
-            const double d = A[r * LDA + r];
-            const double lr0 = (lane < r ? A[r * LDA + lane] : 0.0) * d;
-            const double lr1 = (lane + 32 < r ? A[r * LDA + lane + 32] : 0.0) * d;
-            const double c = __shfl_sync(0xffffffffu, r < 32 ? x0 : x1, r & 31);
+            const double lr0 = lane < r ? A[r * LDA + lane] : 0.0;
+            const double lr1 = lane + 32 < r ? A[r * LDA + lane + 32] : 0.0;
+            const double own = (r < 32 ? x0 : x1) * A[r * LDA + r];
+            const double c = __shfl_sync(0xffffffffu, own, r & 31);
+            if (lane == (r & 31)) {
+                if (r < 32) x0 = c;
+                else x1 = c;
+            }
             x0 = fma(-lr0, c, x0);
             x1 = fma(-lr1, c, x1);
-            if (lane == (r & 31)) {
-                if (r < 32) x0 = c * d;
-                else x1 = c * d;
-            }
         }
         if (lane < R) cv[lane] = x0;
         if (lane + 32 < R) cv[lane + 32] = x1;
