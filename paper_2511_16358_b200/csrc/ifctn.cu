@@ -1906,7 +1906,7 @@ struct Solver : SolverBase {
         const T* dt = truth_view(truth, &tmp, &tmpp);
         const int nb = 1024;
         rse_partial<T><<<nb, 256, 0, st>>>(dt, X, s.I1, s.I1p, s.nloc, rsep);
-        sum_pairs<<<1, 32, 0, st>>>(rsep, nb, rsep + 2 * nb);
+        sum_pairs<<<1, 256, 0, st>>>(rsep, nb, rsep + 2 * nb);
         CU(cudaGetLastError());
         allreduce_dev(rsep + 2 * nb, 2);
         CU(cudaMemcpyAsync(hscal + 8, rsep + 2 * nb, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -1289,12 +1289,38 @@ __global__ void __launch_bounds__(256) rse_partial(const T* truth, const T* X, i
     }
 }
 
-static __global__ void sum_pairs(const double* part, int n, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int i = 0; i < n; ++i) {
-            a += part[2 * i];
-            b += part[2 * i + 1];
+// out[0..1] = Σ_i part[2i], Σ_i part[2i+1] in a fixed tree (one CTA of 256 threads): a thread sums
+// its run of consecutive pairs in order, lanes by xor butterfly, the 8 warp sums in warp order
+static __global__ void __launch_bounds__(256) sum_pairs(const double* part, int n, double* out) {
+    __shared__ double sm[8][2];
+    const int tid = threadIdx.x, per = (n + 255) / 256;
+    double v[2][8];
+    double a = 0.0, b = 0.0;
+    for (int i0 = tid * per; i0 < min(n, (tid + 1) * per); i0 += 8) {
+        const int m = min(8, min(n, (tid + 1) * per) - i0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // loads in flight together, added in order
+            v[0][u] = u < m ? part[2 * (i0 + u)] : 0.0;
+            v[1][u] = u < m ? part[2 * (i0 + u) + 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a += v[0][u];
+            b += v[1][u];
+        }
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if ((tid & 31) == 0) {
+        sm[tid >> 5][0] = a;
+        sm[tid >> 5][1] = b;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        a = b = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a += sm[w][0];
+            b += sm[w][1];
         }
         out[0] = a;
         out[1] = b;
