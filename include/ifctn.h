@@ -79,10 +79,10 @@ typedef enum { IFCTN_F32 = 0, IFCTN_F64 = 1 } ifctn_dtype;
                                   L2-pass, solve and finaliser kernels are launched with
                                   programmatic stream serialization and wait for their
                                   predecessor themselves, griddepcontrol.wait)              */
-#define IFCTN_FLAG_NO_DMMA 1024u /* diagnostic: large ranks (9 < R <= 39) build Gram_j and rhs_j
-                                    with the SIMT fp64 register tiles (default: the fp64 tensor
-                                    cores, mma m8n8k4 = SASS DMMA; same fp64 accuracy, another
-                                    summation order)                                        */
+#define IFCTN_FLAG_NO_DMMA 1024u /* diagnostic: large ranks (R > 9) build Gram_j and rhs_j (R <= 39)
+                                    and refresh the H row with SIMT fp64 code (default: the fp64
+                                    tensor cores, mma m8n8k4 = SASS DMMA; same fp64 accuracy,
+                                    another summation order)                                */
 #define IFCTN_FLAG_GRAM_GEMM 256u /* experiment: large ranks (R > 9) build Gram_j and rhs_j of
                                      two columns per CTA in a separate register-tiled kernel
                                      (gram_project), then the FROM_PROJ solve; measured slower

@@ -332,7 +332,8 @@ struct SolveParams {
     int fused_reduce;    // block_solve: sum β(a,j), ω(a,j) from the a2 partial slots itself
     ReduceParams<T> red; //   (the reduce_partials launch of the block is then skipped)
     int ta;              // block_solve_big: columns a of G_{i,k} staged at once (≥ I_i: all)
-    int mma;             // block_solve_big: Gram/RHS on the fp64 tensor cores (big_gram_mma; 9 < R ≤ 39)
+    int mma;             // block_solve_big on the fp64 tensor cores: bit 0 — Gram/RHS (big_gram_mma; 9 < R ≤ 39),
+                         //   bit 1 — the H-row refresh (any R)
 };
 
 }  // namespace ifctn

@@ -1272,7 +1272,7 @@ struct Solver : SolverBase {
                     const size_t cap = std::min<size_t>(smem_limit - 8 * 1024, 110 * 1024);
                     q.ta = (int)s.ld[i];
                     if (big_solve_smem(q.R, q.ta, (int)s.esize) > cap) q.ta = 32;
-                    q.mma = (q.R <= kBigMmaMaxR && !(flags & IFCTN_FLAG_NO_DMMA)) ? 1 : 0;
+                    q.mma = (flags & IFCTN_FLAG_NO_DMMA) ? 0 : (2 | (q.R <= kBigMmaMaxR ? 1 : 0));  // Gram/RHS | H refresh
                     b.sol_smem = big_solve_smem(q.R, q.ta, (int)s.esize);
                     if (b.sol_smem > smem_limit) fail(IFCTN_E_UNSUPPORTED, "rank too large for the solve kernel");
                     for (int m = 0; m < 3; ++m) {  // allow the device maximum (static smem aside)

@@ -789,7 +789,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         }
     if constexpr (SM != SOLVE_FROM_PROJ) {
       // ≤ 15 output tiles per warp: R ≤ 39 (P.mma, set at plan time); else the SIMT tiles below
-      bool by_mma = P.mma != 0;
+      bool by_mma = (P.mma & 1) != 0;
       if (by_mma) {
         PHASE_CLK(6);
         PHASE_CLK(7);
@@ -1047,6 +1047,35 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             stage(a0, na);
             __syncthreads();
         }
+        if (P.mma & 2) {
+            // on the fp64 tensor cores: rows a in tiles of 8 (M), r in steps of 4 (K), c in column
+            // 0 of B; a warp keeps 4 row tiles in flight; lanes with l%4 = 0 hold column 0 of D
+            const int wi = tid >> 5, lk = lane & 3, lq = lane >> 2;
+            for (int rt = wi; rt * 8 < na; rt += 4 * (kBigThreads / 32)) {
+                double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int r0 = 0; r0 < R; r0 += 4) {
+                    const double b = (lq == 0 && r0 + lk < R) ? cv[r0 + lk] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int a = (rt + u * (kBigThreads / 32)) * 8 + lq;
+                        // rows ≥ na / entries r ≥ R: in-bounds shared memory times b = 0, or unused rows
+                        const double g = gs[min(a, na - 1) * R + r0 + lk];
+                        dmma884(d0[u], d1[u], g, b);
+                    }
+                }
+                if (lk == 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int a = (rt + u * (kBigThreads / 32)) * 8 + lq;
+                        if (a < na) {
+                            const int64_t ag = a0 + a;
+                            const int64_t o = P.k_lt_i ? (P.h_off + ag * P.h_ld + j) : (P.h_off + j * P.h_ld + ag);
+                            P.H[o] = (T)d0[u];
+                        }
+                    }
+                }
+            }
+        } else
         for (int a = row8; a < na; a += nthr >> 3) {
             double h = 0.0;
             for (int r = sub8; r < R; r += 8) h = fma(cv[r], gs[a * R + r], h);
