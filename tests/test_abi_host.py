@@ -34,6 +34,18 @@ def test_header_symbols_exported(abi):
     assert set(abi.SIGNATURES) == set(names)
 
 
+def test_binding_flags_match_the_header(abi):
+    """Every IFCTN_FLAG_* of include/ifctn.h has the same value in the binding (a drift would
+    silently select another kernel path), and the flags are distinct bits."""
+    src = open(os.path.join(ROOT, "include", "ifctn.h")).read()
+    flags = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(IFCTN_FLAG_[A-Z0-9_]+)\s+(\d+)u", src)}
+    assert len(flags) >= 9 and flags["IFCTN_FLAG_NONE"] == 0
+    for name, val in flags.items():
+        assert getattr(abi, name) == val, name
+    bits = [v for v in flags.values() if v]
+    assert all(v & (v - 1) == 0 for v in bits) and len(set(bits)) == len(bits)
+
+
 def test_library_is_sm100a(abi):
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", abi.LIB_PATH],
