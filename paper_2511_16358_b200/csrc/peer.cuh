@@ -57,6 +57,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000ull * 1000ull * 1000ull;  // 20 s
+
 // CTA-wide: publish epoch e, then wait for every rank's flag ≥ e (thread 0 spins).
 __device__ __forceinline__ void peer_publish_wait(const PeerCtx& X, unsigned long long e) {
     if (threadIdx.x == 0) {
@@ -64,7 +66,18 @@ __device__ __forceinline__ void peer_publish_wait(const PeerCtx& X, unsigned lon
         st_release_sys(reinterpret_cast<unsigned long long*>(X.bufs[X.rank]), e);
         for (int r = 0; r < X.W; ++r) {
             const unsigned long long* f = reinterpret_cast<const unsigned long long*>(X.bufs[r]);
+            unsigned spins = 0;
+            unsigned long long t0 = 0;
             while (ld_acquire_sys(f) < e) {
+                // watchdog: a peer that never publishes (a crashed or stuck rank) must not hang
+                // this GPU — after kPeerTimeoutNs the kernel traps (a launch failure, reported
+                // as IFCTN_E_CUDA by the next call) instead of spinning forever
+                if ((++spins & 0x3ffu) == 0) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (t0 == 0) t0 = t;
+                    else if (t - t0 > kPeerTimeoutNs) __trap();
+                }
             }
         }
     }
