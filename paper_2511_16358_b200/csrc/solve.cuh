@@ -431,7 +431,7 @@ __host__ __device__ inline int big_solve_lda(int R) { return big_solve_rp(R) + 1
 // rhs, c, c_old (Rp each), the mma path's cross-warp scratch]
 __host__ __device__ inline size_t big_solve_smem(int R, int ta, int /*esize*/) {
     const int Rp = big_solve_rp(R);
-    return sizeof(double) * ((size_t)ta * R + Rp + (size_t)Rp * big_solve_lda(R) + 2 * (size_t)ta + 3 * (size_t)Rp +
+    return sizeof(double) * ((size_t)ta * R + Rp + (size_t)(Rp + 1) * big_solve_lda(R) + 2 * (size_t)ta + 3 * (size_t)Rp +
                              (R <= kBigMmaMaxR ? (kBigThreads / 32) * kBigTPR * 64 + 1 : 0));
 }
 
@@ -745,7 +745,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     const int NG = R * (R + 1) / 2, NA = NG + R;
     double* gs = bsm;                      // G_{i,k}(:, a0 .. a0+ta) as fp64, row stride R
     double* A = gs + (size_t)TA * R + Rp;  // Gram (row-major, lda)
-    double* om = A + (size_t)Rp * LDA;     // ω(a, j)
+    double* om = A + (size_t)(Rp + 1) * LDA;  // ω(a, j); row Rp of A carries rhsᵀ through the factorisation
     double* be = om + TA;                  // β(a, j)
     double* rhs = be + TA;
     double* cv = rhs + Rp;
@@ -925,6 +925,10 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         for (int c = 0; c <= r; ++c) A[r * LDA + c] = (c == r) ? 1.0 : 0.0;
     if (tid == 0) *okp = 1;
     __syncthreads();
+    // Row Rp of the factored matrix is rhsᵀ: its panel solves and trailing updates ARE the forward
+    // substitution L y = rhs (y ends up in A[Rp][·]), so only Lᵀ c = y remains for the one warp.
+    for (int c = tid; c < Rp; c += nthr) A[Rp * LDA + c] = c < R ? rhs[c] : 0.0;
+    __syncthreads();
     for (int c0 = 0; c0 < Rp; c0 += 4) {
         if (tid == 0) {
             double L[4][4];
@@ -956,8 +960,8 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             if (!ok) *okp = 0;
         }
         __syncthreads();
-        const int m = Rp - c0 - 4;  // trailing size
-        if (tid < m) {              // panel row r: x = a · L11⁻ᵀ
+        const int m = Rp - c0 - 4 + 1;  // trailing rows, the rhs row included
+        if (tid < m) {                  // panel row r: x = a · L11⁻ᵀ
             const int r = c0 + 4 + tid;
             double x[4];
 #pragma unroll
@@ -976,7 +980,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
             const int r = c0 + 4 + rr;
             const double l0 = A[r * LDA + c0], l1 = A[r * LDA + c0 + 1], l2 = A[r * LDA + c0 + 2],
                          l3 = A[r * LDA + c0 + 3];
-            for (int c = c0 + 4 + (tid & 7); c <= r; c += 8) {
+            for (int c = c0 + 4 + (tid & 7); c <= min(r, Rp - 1); c += 8) {
                 const double* lc = A + c * LDA + c0;
                 double v = A[r * LDA + c];
                 v = fma(-l0, lc[0], v);
@@ -993,19 +997,7 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
         PHASE_CLK(3);
         // L y = rhs, Lᵀ c = y with rhs in registers (lane owns rows lane, lane + 32) and the
         // pivot value broadcast by shuffle; the L entries are independent shared loads
-        double x0 = lane < R ? rhs[lane] : 0.0, x1 = lane + 32 < R ? rhs[lane + 32] : 0.0;
-        for (int r = 0; r < R; ++r) {
-            const double lq0 = lane > r && lane < R ? A[lane * LDA + r] : 0.0;
-            const double lq1 = lane + 32 > r && lane + 32 < R ? A[(lane + 32) * LDA + r] : 0.0;
-            const double own = (r < 32 ? x0 : x1) * A[r * LDA + r];
-            const double y = __shfl_sync(0xffffffffu, own, r & 31);
-            if (lane == (r & 31)) {
-                if (r < 32) x0 = y;
-                else x1 = y;
-            }
-            x0 = fma(-lq0, y, x0);
-            x1 = fma(-lq1, y, x1);
-        }
+        double x0 = lane < R ? A[Rp * LDA + lane] : 0.0, x1 = lane + 32 < R ? A[Rp * LDA + lane + 32] : 0.0;  // y
         for (int r = R - 1; r >= 0; --r) {
             const double lr0 = lane < r ? A[r * LDA + lane] : 0.0;
             const double lr1 = lane + 32 < r ? A[r * LDA + lane + 32] : 0.0;
