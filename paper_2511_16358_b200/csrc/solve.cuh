@@ -409,15 +409,19 @@ __global__ void __launch_bounds__(128) block_solve(const SolveParams<T> P) {
 //   * G_{i,k} is staged in shared memory as fp64 in tiles of `ta` columns a — normally all of
 //     it at once; the loads of a batch are all in flight before the stores; reused by the H
 //     refresh;
-//   * Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ and rhs_j = G_{i,k} β(:,j) as register tiles:
-//     task = (4×4 tile of the Gram upper triangle, or a 4-row tile of the rhs; a-residue h mod
-//     KS), KS = the a-split that fills the CTA; the KS partial tiles are added in h order
-//     (fixed order, deterministic);
-//   * warp 0: + ρI, ρ c_old, then a left-looking (Crout) Cholesky: column c of L is one
-//     round of independent length-c dot products (lane l owns rows l, l+32; four partial
-//     sums), the pivot's 1/√d is broadcast by shuffle — one dependent step per column, no
-//     trailing-update chain and no CTA barriers; forward/back substitution; ‖Δc‖²;
-//   * row j of H_{k,i} (8 threads per a).
+//   * Gram_j = G_{i,k} diag(ω(:,j)) G_{i,k}ᵀ and rhs_j = G_{i,k} β(:,j): for R ≤ 39 one fp64
+//     tensor-core product (big_gram_mma below: DMMA m8n8k4, K split over the 8 warps, partial
+//     tiles summed in warp order through a scratch); else (and under IFCTN_FLAG_NO_DMMA) SIMT
+//     register tiles: task = (4×4 tile of the Gram upper triangle, or a 4-row tile of the rhs;
+//     a-residue h mod KS), KS = the a-split that fills the CTA; the KS partial tiles are added
+//     in h order (fixed order, deterministic);
+//   * + ρI, ρ c_old, then a right-looking Cholesky in 4×4 blocks over the whole CTA (thread 0
+//     factors the diagonal block in registers with rsqrt pivots, one thread per row solves the
+//     panel, all threads apply the rank-4 trailing update); rhsᵀ rides as row Rp of the matrix,
+//     so the same panel/trailing steps perform the forward substitution L y = rhs;
+//   * warp 0: back substitution Lᵀ c = y (lane owns rows lane, lane + 32; the pivot value is
+//     broadcast by shuffle); ‖Δc‖²;
+//   * row j of H_{k,i}: on DMMA (rows a in tiles of 8, c in column 0 of B), or 8 threads per a.
 constexpr int kBigThreads = 256;
 #ifndef IFCTN_BIG_MINB  // CTAs per SM the register allocation allows
 #define IFCTN_BIG_MINB 1
@@ -427,7 +431,7 @@ constexpr int kBigMmaMaxR = 39;  // big_gram_mma: ≤ 15 output tiles (30 accumu
 constexpr int kBigTPR = 4;       // big_gram_mma: tiles per round of its cross-warp sum (scratch: 8 warps × 4 × 64)
 __host__ __device__ inline int big_solve_rp(int R) { return (R + 3) & ~3; }
 __host__ __device__ inline int big_solve_lda(int R) { return big_solve_rp(R) + 1; }  // odd: rows hit different banks
-// shared memory: G tile (ta·R + Rp doubles) + fp64 [A: Rp rows of lda, ω, β (ta each),
+// shared memory: G tile (ta·R + Rp doubles) + fp64 [A: Rp + 1 rows of lda (row Rp: rhsᵀ), ω, β (ta each),
 // rhs, c, c_old (Rp each), the mma path's cross-warp scratch]
 __host__ __device__ inline size_t big_solve_smem(int R, int ta, int /*esize*/) {
     const int Rp = big_solve_rp(R);
@@ -995,8 +999,8 @@ __device__ __forceinline__ void block_solve_big_body(const SolveParams<T>& P, in
     if (tid < 32) {
         const bool ok = *okp != 0;
         PHASE_CLK(3);
-        // L y = rhs, Lᵀ c = y with rhs in registers (lane owns rows lane, lane + 32) and the
-        // pivot value broadcast by shuffle; the L entries are independent shared loads
+        // Lᵀ c = y with y (row Rp of the factored matrix) in registers (lane owns rows lane,
+        // lane + 32) and the pivot value broadcast by shuffle; the L entries are independent loads
         double x0 = lane < R ? A[Rp * LDA + lane] : 0.0, x1 = lane + 32 < R ? A[Rp * LDA + lane + 32] : 0.0;  // y
         for (int r = R - 1; r >= 0; --r) {
             const double lr0 = lane < r ? A[r * LDA + lane] : 0.0;
